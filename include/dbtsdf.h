@@ -1,0 +1,174 @@
+/*
+ * dbtsdf.h — C ABI of the B200 scan-integration engine (libdbtsdf.so).
+ *
+ * This is the drop-in boundary for the DB-TSDF hot path: the functions below
+ * replace the bodies of the reference's Python entry points (reference =
+ * /root/reference/pkg/src/bitsdf, cited as <file>:<line>). The Python mirror
+ * in paper_2509_20081_b200/ keeps the reference signatures and calls these
+ * through ctypes; any other host language binds the same symbols (see
+ * INTEGRATION.md). No torch / CUDA types appear in any signature: handles are
+ * opaque, buffers are plain pointers plus sizes, streams are `void*`.
+ *
+ * Return codes mirror the reference exception -> CLI exit-code map
+ * (cli.py:34-40): 0 ok, 1 generic BitsdfError, 2 ConfigurationError,
+ * 3 FormatError, 4 CorruptionError, 5 EvaluationError, 6 ResourceError.
+ * dbt_last_error() returns the message of the last failure on this thread.
+ *
+ * Threading: one host thread per grid handle (the reference is a single
+ * writer per grid, integrator.py:214-216). All work is ordered on the grid's
+ * CUDA stream; the *_device entry points are asynchronous on that stream.
+ */
+#ifndef DBTSDF_H
+#define DBTSDF_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DBT_API __attribute__((visibility("default")))
+#else
+#define DBT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBT_OK 0
+#define DBT_ERR_GENERIC 1
+#define DBT_ERR_CONFIG 2
+#define DBT_ERR_FORMAT 3
+#define DBT_ERR_CORRUPTION 4
+#define DBT_ERR_EVALUATION 5
+#define DBT_ERR_RESOURCE 6
+
+/* point dtypes accepted by the integrate calls */
+#define DBT_F32 0
+#define DBT_F64 1
+
+/* dbt_params.flags */
+#define DBT_FLAG_MAP_FRAME 1u        /* points already in the map frame; per-point sensor
+                                        positions supplied (integrate_point semantics) */
+#define DBT_FLAG_SKIP_NORM_CHECK 2u  /* caller already applied the degenerate-ray discard
+                                        (integrator.py:173-175 uses the 1-D norm) */
+#define DBT_FLAG_NO_DEDUP 4u         /* stamp every applied point (no centre dedup); for
+                                        measurement only, the grid result is identical */
+
+typedef struct dbt_grid dbt_grid; /* device-resident VoxelGrid (grid.py:39-58) */
+typedef struct dbt_bank dbt_bank; /* device copy of a KernelBank (kernels.py:122-141) */
+
+/* IntegrationParams (integrator.py:55-73) plus engine flags. */
+typedef struct dbt_params {
+  int32_t h_max;        /* 1 <= t_occ <= h_max <= 255 */
+  int32_t t_occ;
+  int32_t downsample;   /* keep every n-th point, >= 1 (integrator.py:223-229) */
+  int32_t first_return; /* first_return_per_voxel (integrator.py:256-262) */
+  uint32_t flags;
+  int32_t reserved;
+} dbt_params;
+
+/* FrameStats (integrator.py:76-81) plus device counters. */
+typedef struct dbt_stats {
+  int64_t points_in;        /* after downsampling */
+  int64_t points_discarded; /* points_in - #(degenerate or out-of-bounds) */
+  int64_t voxels_written;   /* mask cells changed (concurrent count) */
+  int64_t points_applied;   /* stamped returns (after first-return dedup) */
+  int64_t unique_centers;   /* distinct centre voxels swept */
+  int64_t knife_edges;      /* applied points whose bin raw index is within 1e-12 of an
+                               interior bin boundary (ulp-level transcendental risk) */
+  double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */
+  double device_ms;         /* CUDA-event time of the device work (H2D .. stats D2H) */
+} dbt_stats;
+
+DBT_API const char* dbt_last_error(void);
+DBT_API const char* dbt_version(void);
+DBT_API int dbt_device_count(int* out);
+
+/* ---- voxel store (grid.py:61-89, 178-202) ------------------------------ */
+/* Fresh grid: every voxel unobserved (mask 0xFFFFFFFF, sign free, hits 0).
+ * slab_x0/slab_x1 select the owned x-slab [x0, x1) for multi-GPU sharding;
+ * pass 0, dims[0] for a whole grid. */
+DBT_API int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origin[3],
+                    int device, int64_t slab_x0, int64_t slab_x1, dbt_grid** out);
+DBT_API int dbt_grid_destroy(dbt_grid* g);
+DBT_API int dbt_grid_reset(dbt_grid* g);
+DBT_API int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* device_bytes);
+/* Host C-order (nx,ny,nz) field arrays restricted to the slab, i.e. shape
+ * (x1-x0, ny, nz). Masks must be low-bit runs and signs 0/1 (else
+ * DBT_ERR_CORRUPTION: the device word stores the run length). */
+DBT_API int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits);
+DBT_API int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits);
+/* DBTSDF01 voxel records, F-order linear index ix + nx*(iy + ny*iz)
+ * (grid.py:178-185): 8 bytes each {mask u32, sign u8, hits u8, 0 u16}.
+ * Whole grid only (slab == full grid). */
+DBT_API int dbt_grid_to_records(dbt_grid* g, void* out_records);
+DBT_API int dbt_grid_from_records(dbt_grid* g, const void* records);
+/* Point query: n voxels given as global (ix,iy,iz) int64 triples inside the
+ * slab (signed_distance / is_observed, grid.py:138-158); outputs nullable. */
+DBT_API int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, uint8_t* sign,
+                            uint8_t* hits);
+
+/* ---- query / distance readout (grid.py:118-175) ------------------------ */
+DBT_API int dbt_popcount(dbt_grid* g, int32_t* out);                 /* popcount_array(grid.mask) */
+DBT_API int dbt_observed(dbt_grid* g, uint8_t* out);                 /* observed_array */
+DBT_API int dbt_signed_distance_field(dbt_grid* g, double* field, uint8_t* observed);
+DBT_API int dbt_grid_counts(dbt_grid* g, int64_t* observed, int64_t* occupied); /* cli info */
+
+/* ---- kernel bank (kernels.py:151-193) ---------------------------------- */
+/* distance_kernel: size^3 uint32 run masks indexed [dx+R][dy+R][dz+R];
+ * shadow offsets: per flat bin b_a*b_el+b_e a list of (dx,dy,dz) int32
+ * triples, concatenated, with shadow_counts[n_bins]. */
+DBT_API int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* distance_kernel,
+                    const int32_t* shadow_xyz, const int32_t* shadow_counts, int device,
+                    dbt_bank** out);
+DBT_API int dbt_bank_destroy(dbt_bank* b);
+
+/* ---- integration (integrator.py:163-287) ------------------------------- */
+/* One scan, sensor-frame points from HOST memory (pinned or pageable):
+ * H2D copy, transform pts@R.T+t, discard, bin, stamp, stats D2H; returns
+ * when the grid is updated. pose: 4x4 row-major float64. */
+DBT_API int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
+                        int64_t n, const double pose[16], const dbt_params* p, dbt_stats* out);
+/* S scans in one launch sequence (config 5): points concatenated, counts[S],
+ * poses[S*16]; out[S] per-scan stats (voxels_written reported on out[0]). */
+DBT_API int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
+                        const int64_t* counts, int32_t n_scans, const double* poses,
+                        const dbt_params* p, dbt_stats* out);
+/* Map-frame points with per-point sensor positions (integrate_point,
+ * integrator.py:163-189); outcome[i] = 1 applied, 0 discarded (nullable). */
+DBT_API int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map,
+                             const double* sensor, int64_t n, const dbt_params* p,
+                             dbt_stats* out, int8_t* outcome);
+/* Device-resident variant for benchmarking and multi-GPU: `d_points` is a
+ * device pointer on the grid's device, stream a cudaStream_t (NULL = the
+ * grid's stream). Asynchronous: the stats land in device memory and are read
+ * with dbt_stats_read after the stream is synchronised. */
+DBT_API int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, int dtype,
+                         const int64_t* counts, int32_t n_scans, const double* poses,
+                         const dbt_params* p, void* stream);
+DBT_API int dbt_stats_read(dbt_grid* g, dbt_stats* out, int32_t n_scans);
+DBT_API int dbt_synchronize(dbt_grid* g);
+
+/* ---- device binning (kernels.py:49-57), exposed for parity tests -------- */
+DBT_API int dbt_bin_index_array(const double* dirs, int64_t n, int32_t b_az, int32_t b_el,
+                        int64_t* b_a, int64_t* b_e, int device);
+
+/* ---- measurement hooks -------------------------------------------------- */
+/* When enabled, every engine kernel is bracketed by CUDA events on its
+ * stream and its time accumulated per kernel name. */
+DBT_API int dbt_profile_enable(dbt_grid* g, int on);
+/* Copies up to cap entries: names (NUL-separated, 32 bytes each), total ms
+ * and launch counts; returns the number of kernels in *n. */
+DBT_API int dbt_profile_read(dbt_grid* g, char* names, double* ms, int64_t* launches, int32_t cap,
+                     int32_t* n);
+DBT_API int dbt_profile_reset(dbt_grid* g);
+/* Kernel launches issued by the engine since load (all handles). */
+DBT_API int64_t dbt_launch_count(void);
+
+/* pinned host buffers for callers without a CUDA runtime of their own */
+DBT_API int dbt_host_alloc(int64_t bytes, void** out);
+DBT_API int dbt_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBTSDF_H */

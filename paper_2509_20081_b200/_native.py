@@ -1,0 +1,140 @@
+"""ctypes binding of libdbtsdf.so (include/dbtsdf.h).
+
+The engine is the only compute path: if the shared library is missing or no
+CUDA device is usable, every entry point raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import CODE_TO_ERROR, BitsdfError
+
+LIB_PATH = Path(__file__).resolve().parent / "libdbtsdf.so"
+
+DBT_F32 = 0
+DBT_F64 = 1
+FLAG_MAP_FRAME = 1
+FLAG_SKIP_NORM_CHECK = 2
+FLAG_NO_DEDUP = 4
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("h_max", ctypes.c_int32),
+        ("t_occ", ctypes.c_int32),
+        ("downsample", ctypes.c_int32),
+        ("first_return", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("points_in", ctypes.c_int64),
+        ("points_discarded", ctypes.c_int64),
+        ("voxels_written", ctypes.c_int64),
+        ("points_applied", ctypes.c_int64),
+        ("unique_centers", ctypes.c_int64),
+        ("knife_edges", ctypes.c_int64),
+        ("elapsed_ms", ctypes.c_double),
+        ("device_ms", ctypes.c_double),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/dbtsdf.h one to one
+SIGNATURES = {
+    "dbt_last_error": (ctypes.c_char_p, []),
+    "dbt_version": (ctypes.c_char_p, []),
+    "dbt_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "dbt_grid_create": (ctypes.c_int, [_c_i64p, ctypes.c_double, _c_dp, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "dbt_grid_destroy": (ctypes.c_int, [_vp]),
+    "dbt_grid_reset": (ctypes.c_int, [_vp]),
+    "dbt_grid_info": (ctypes.c_int, [_vp, _c_i64p, _c_i64p, _c_i64p]),
+    "dbt_grid_upload": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dbt_grid_download": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dbt_grid_to_records": (ctypes.c_int, [_vp, _vp]),
+    "dbt_grid_from_records": (ctypes.c_int, [_vp, _vp]),
+    "dbt_grid_gather": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
+    "dbt_popcount": (ctypes.c_int, [_vp, _vp]),
+    "dbt_observed": (ctypes.c_int, [_vp, _vp]),
+    "dbt_signed_distance_field": (ctypes.c_int, [_vp, _vp, _vp]),
+    "dbt_grid_counts": (ctypes.c_int, [_vp, _c_i64p, _c_i64p]),
+    "dbt_bank_create": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int,
+                                       ctypes.POINTER(_vp)]),
+    "dbt_bank_destroy": (ctypes.c_int, [_vp]),
+    "dbt_integrate_frame": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _c_dp,
+                                           ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
+    "dbt_integrate_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _c_dp,
+                                           ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
+    "dbt_integrate_points_map": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.POINTER(Params),
+                                                ctypes.POINTER(Stats), _vp]),
+    "dbt_integrate_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _c_dp,
+                                            ctypes.POINTER(Params), _vp]),
+    "dbt_stats_read": (ctypes.c_int, [_vp, ctypes.POINTER(Stats), ctypes.c_int32]),
+    "dbt_synchronize": (ctypes.c_int, [_vp]),
+    "dbt_bin_index_array": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp,
+                                           ctypes.c_int]),
+    "dbt_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "dbt_profile_read": (ctypes.c_int, [_vp, ctypes.c_char_p, _c_dp, _c_i64p, ctypes.c_int32,
+                                        ctypes.POINTER(ctypes.c_int32)]),
+    "dbt_profile_reset": (ctypes.c_int, [_vp]),
+    "dbt_launch_count": (ctypes.c_int64, []),
+    "dbt_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "dbt_host_free": (ctypes.c_int, [_vp]),
+}
+
+_LIB = None
+
+
+def lib():
+    """Load libdbtsdf.so once. Raises ImportError when it was not built."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA engine with "
+                "`python -m paper_2509_20081_b200.build` (there is no CPU fallback)"
+            )
+        L = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def check(rc: int) -> None:
+    if rc:
+        msg = lib().dbt_last_error().decode(errors="replace")
+        raise CODE_TO_ERROR.get(int(rc), BitsdfError)(msg)
+
+
+def ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = lib().dbt_device_count(ctypes.byref(n))
+    return int(n.value) if rc == 0 else 0
+
+
+def default_device() -> int:
+    """LOCAL_RANK under torchrun, else 0 (one process per GPU)."""
+    return int(os.environ.get("DBT_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def make_params(h_max=255, t_occ=2, downsample=1, first_return=False, flags=0) -> Params:
+    return Params(int(h_max), int(t_occ), int(downsample), int(bool(first_return)), int(flags), 0)

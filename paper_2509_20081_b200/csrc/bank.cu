@@ -1,0 +1,116 @@
+// bank.cu — device copy of the KernelBank (reference kernels.py:122-193).
+//
+// The bank is built on the host exactly as the reference builds it (one
+// shared K^3 distance kernel + one shadow offset list per azimuth-elevation
+// bin) and staged here once. Two device tables are derived:
+//  * the sweep table: for each of the 4 possible z-alignments of a centre,
+//    each of the K*K kernel rows and each 4-cell chunk of that row, the 4 run
+//    lengths packed into one u32 (63 marks a cell outside the kernel, which
+//    can never lower a stored run length <= 32);
+//  * the shadow table in CSR form, offsets as int8 (|o| <= R <= 15).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "engine.cuh"
+
+using namespace dbt;
+
+static uint64_t g_bank_serial = 0;
+
+extern "C" {
+
+int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* distance_kernel,
+                    const int32_t* shadow_xyz, const int32_t* shadow_counts, int device,
+                    dbt_bank** out) {
+  *out = nullptr;
+  if (size < 1 || size % 2 == 0)
+    return set_error(DBT_ERR_CONFIG, "kernel size must be odd and positive (kernels.py:160-161)");
+  if (size > kMaxK) return set_error(DBT_ERR_CONFIG, "kernel size above 31 is not supported on device");
+  if (b_az < 1 || b_el < 1) return set_error(DBT_ERR_CONFIG, "bin counts must be at least 1");
+  if ((int64_t)b_az * b_el > 65535) return set_error(DBT_ERR_CONFIG, "more than 65535 direction bins");
+  const int K = size, R = size / 2, K3 = K * K * K, rows = K * K;
+  const int CH = (K + 3 + 3) / 4;
+  std::vector<uint8_t> len(K3);
+  int max_d = 0;
+  for (int i = 0; i < K3; ++i) {
+    uint32_t m = distance_kernel[i];
+    int pc = __builtin_popcount(m);
+    int clz = m ? __builtin_clz(m) : 32;
+    if (pc + clz != 32)
+      return set_error(DBT_ERR_CORRUPTION, "distance kernel entry is not a low-bit run mask");
+    len[i] = (uint8_t)pc;
+    max_d = std::max(max_d, pc);
+  }
+  std::vector<uint32_t> dtab((size_t)4 * rows * CH);
+  for (int s = 0; s < 4; ++s)
+    for (int r = 0; r < rows; ++r)
+      for (int c = 0; c < CH; ++c) {
+        uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) {
+          int zk = 4 * c + i - s;
+          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)r * K + zk] : 63u;
+          v |= d << (8 * i);
+        }
+        dtab[((size_t)s * rows + r) * CH + c] = v;
+      }
+  const int nb = b_az * b_el;
+  std::vector<int32_t> start(nb + 1, 0);
+  int max_s = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (shadow_counts[b] < 0) return set_error(DBT_ERR_CONFIG, "negative shadow count");
+    start[b + 1] = start[b] + shadow_counts[b];
+    max_s = std::max(max_s, (int)shadow_counts[b]);
+  }
+  const int64_t total = start[nb];
+  std::vector<int8_t> sx((size_t)std::max<int64_t>(total, 1) * 4, 0);
+  for (int64_t i = 0; i < total; ++i)
+    for (int k = 0; k < 3; ++k) {
+      int32_t v = shadow_xyz[3 * i + k];
+      if (v < -R || v > R) return set_error(DBT_ERR_CONFIG, "shadow offset outside the kernel cube");
+      sx[4 * i + k] = (int8_t)v;
+    }
+
+  dbt_bank* b = new dbt_bank();
+  b->device = device;
+  b->K = K;
+  b->R = R;
+  b->b_az = b_az;
+  b->b_el = b_el;
+  b->n_bins = nb;
+  b->max_shadow = max_s;
+  b->total_shadow = total;
+  b->chunks_per_row = CH;
+  b->max_d = max_d;
+  b->serial = ++g_bank_serial;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_len, K3);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_dtab, dtab.size() * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_xyz, sx.size());
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_start, (nb + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_len, len.data(), K3, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_dtab, dtab.data(), dtab.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_shadow_xyz, sx.data(), sx.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(b->d_shadow_start, start.data(), (nb + 1) * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    int code = cuda_error(e, "kernel bank staging");
+    dbt_bank_destroy(b);
+    return code;
+  }
+  *out = b;
+  return DBT_OK;
+}
+
+int dbt_bank_destroy(dbt_bank* b) {
+  if (!b) return DBT_OK;
+  cudaSetDevice(b->device);
+  if (b->d_len) cudaFree(b->d_len);
+  if (b->d_dtab) cudaFree(b->d_dtab);
+  if (b->d_shadow_xyz) cudaFree(b->d_shadow_xyz);
+  if (b->d_shadow_start) cudaFree(b->d_shadow_start);
+  delete b;
+  return DBT_OK;
+}
+
+}  // extern "C"

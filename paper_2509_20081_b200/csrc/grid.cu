@@ -1,0 +1,506 @@
+// grid.cu — device voxel store: allocation, host sync, DBTSDF01 records and
+// the distance readout kernels (reference: grid.py:39-202).
+#include <algorithm>
+#include <cstring>
+
+#include "engine.cuh"
+
+using namespace dbt;
+
+namespace dbt {
+
+int grid_set_device(const dbt_grid* g) {
+  DBT_CUDA(cudaSetDevice(g->device));
+  return DBT_OK;
+}
+
+int ensure_stage(dbt_grid* g, int64_t bytes) {
+  if (bytes <= g->cap_stage) return DBT_OK;
+  if (g->d_stage) cudaFree(g->d_stage);
+  g->d_stage = nullptr;
+  g->cap_stage = 0;
+  DBT_CUDA(cudaMalloc(&g->d_stage, (size_t)bytes));
+  g->cap_stage = bytes;
+  return DBT_OK;
+}
+
+}  // namespace dbt
+
+namespace {
+
+constexpr int64_t kStageBytes = 256ll << 20;
+
+__global__ void fill_cells_kernel(uint32_t* __restrict__ cells, int64_t n) {
+  // n is a multiple of 4 (allocation is padded); 128-bit stores
+  const uint4 v = make_uint4(kFreshCell, kFreshCell, kFreshCell, kFreshCell);
+  uint4* p = reinterpret_cast<uint4*>(cells);
+  int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Host C-order slice (xs, ny, nz) of mask/sign/hits -> device words.
+// Validates the run-mask invariant (grid.py:118-121: (m & (m+1)) == 0, i.e.
+// popc(m) + clz(m) == 32) and sign in {0,1}.
+__global__ void encode_kernel(uint32_t* __restrict__ cells, const uint32_t* __restrict__ mask,
+                              const uint8_t* __restrict__ sign, const uint8_t* __restrict__ hits,
+                              int64_t n, int64_t nz, int64_t nzp, int* __restrict__ err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = mask[i];
+    int pc = __popc(m);
+    uint8_t s = sign[i];
+    if (pc + __clz(m) != 32 || s > 1) {
+      atomicOr(err, pc + __clz(m) != 32 ? 1 : 2);
+      continue;
+    }
+    int64_t row = i / nz, z = i - row * nz;
+    cells[row * nzp + z] = make_cell(pc, s, hits[i]);
+  }
+}
+
+
+__global__ void decode_kernel(const uint32_t* __restrict__ cells, uint32_t* __restrict__ mask,
+                              uint8_t* __restrict__ sign, uint8_t* __restrict__ hits, int64_t n,
+                              int64_t nz, int64_t nzp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = i / nz, z = i - row * nz;
+    uint32_t c = cells[row * nzp + z];
+    mask[i] = run_mask_of(cell_len(c));
+    sign[i] = (c & kFreeBit) ? 1 : 0;
+    hits[i] = (uint8_t)(c >> kHitsShift);
+  }
+}
+
+// Readout (grid.py:161-175). mode 0: popcount int32; 1: observed u8;
+// 2: signed distance f64 (+ observed u8).
+__global__ void readout_kernel(const uint32_t* __restrict__ cells, int mode, int32_t* __restrict__ pop,
+                               uint8_t* __restrict__ obs, double* __restrict__ sdf, double vs,
+                               int64_t n, int64_t nz, int64_t nzp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = i / nz, z = i - row * nz;
+    uint32_t c = cells[row * nzp + z];
+    // decode = popcount of the run mask; the run check is popc + clz == 32
+    uint32_t m = run_mask_of(cell_len(c));
+    int len = __popc(m);
+    int hits = c >> kHitsShift;
+    if (mode == 0) {
+      pop[i] = len;
+    } else {
+      uint8_t observed = !(m == 0xFFFFFFFFu && hits == 0);
+      obs[i] = observed;
+      if (mode == 2) {
+        // sigma * (popcount * voxel_size), sigma = -1 for occupied: keeps -0.0
+        double dist = __dmul_rn((double)len, vs);
+        double sigma = (c & kFreeBit) ? 1.0 : -1.0;
+        sdf[i] = __dmul_rn(sigma, dist);
+      }
+    }
+  }
+}
+
+__global__ void count_kernel(const uint32_t* __restrict__ cells, int64_t n, int64_t nz, int64_t nzp,
+                             unsigned long long* __restrict__ out) {
+  unsigned long long obs = 0, occ = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = i / nz, z = i - row * nz;
+    uint32_t c = cells[row * nzp + z];
+    obs += !(cell_len(c) == 32 && (c >> kHitsShift) == 0);
+    occ += !(c & kFreeBit);
+  }
+  for (int o = 16; o; o >>= 1) {
+    obs += __shfl_xor_sync(0xffffffffu, obs, o);
+    occ += __shfl_xor_sync(0xffffffffu, occ, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, obs);
+    atomicAdd(out + 1, occ);
+  }
+}
+
+// F-order record transpose (grid.py:178-185): records of iz slab [z0, z0+zc)
+// rec[(iz-z0)*nx*ny + iy*nx + ix] <- cell(ix, iy, iz). Tile 32 (x) x 32 (z)
+// per block at fixed iy so both the cell reads (along z) and the record
+// writes (along x) are coalesced.
+__global__ void to_records_kernel(const uint32_t* __restrict__ cells, uint64_t* __restrict__ rec,
+                                  int64_t nx, int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
+  __shared__ uint32_t tile[32][33];
+  int64_t iy = blockIdx.y;
+  int64_t xb = blockIdx.x * 32, zb = blockIdx.z * 32;
+  int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    int64_t ix = xb + k, iz = zb + tx;
+    uint32_t v = 0;
+    if (ix < nx && iz < zc) v = cells[(ix * ny + iy) * nzp + z0 + iz];
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    int64_t iz = zb + k, ix = xb + tx;
+    if (ix < nx && iz < zc) {
+      uint32_t c = tile[tx][k];
+      uint64_t r = (uint64_t)run_mask_of(cell_len(c)) | ((uint64_t)((c & kFreeBit) ? 1 : 0) << 32) |
+                   ((uint64_t)(c >> kHitsShift) << 40);
+      rec[iz * nx * ny + iy * nx + ix] = r;
+    }
+  }
+}
+
+__global__ void from_records_kernel(uint32_t* __restrict__ cells, const uint64_t* __restrict__ rec,
+                                    int64_t nx, int64_t ny, int64_t nzp, int64_t z0, int64_t zc,
+                                    int* __restrict__ err) {
+  __shared__ uint32_t tile[32][33];
+  int64_t iy = blockIdx.y;
+  int64_t xb = blockIdx.x * 32, zb = blockIdx.z * 32;
+  int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    int64_t iz = zb + k, ix = xb + tx;
+    uint32_t v = 0;
+    if (ix < nx && iz < zc) {
+      uint64_t r = rec[iz * nx * ny + iy * nx + ix];
+      uint32_t m = (uint32_t)r;
+      uint32_t s = (uint32_t)(r >> 32) & 0xFF;
+      uint32_t h = (uint32_t)(r >> 40) & 0xFF;
+      int pc = __popc(m);
+      if (pc + __clz(m) != 32 || s > 1) atomicOr(err, pc + __clz(m) != 32 ? 1 : 2);
+      v = make_cell(pc, s ? 1 : 0, h);
+    }
+    tile[tx][k] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    int64_t ix = xb + k, iz = zb + tx;
+    if (ix < nx && iz < zc) cells[(ix * ny + iy) * nzp + z0 + iz] = tile[k][tx];
+  }
+}
+
+__global__ void gather_kernel(const uint32_t* __restrict__ cells, const int64_t* __restrict__ xyz, int64_t n,
+                              int64_t x0, int64_t ny, int64_t nzp, uint32_t* __restrict__ mask,
+                              uint8_t* __restrict__ sign, uint8_t* __restrict__ hits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = cells[((xyz[3 * i] - x0) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
+    mask[i] = run_mask_of(cell_len(c));
+    sign[i] = (c & kFreeBit) ? 1 : 0;
+    hits[i] = (uint8_t)(c >> kHitsShift);
+  }
+}
+
+int grid_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+int check_grid(const dbt_grid* g) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  return grid_set_device(g);
+}
+
+int check_upload_error(dbt_grid* g) {
+  int err = 0;
+  DBT_CUDA(cudaMemcpyAsync(&err, &g->d_lcnt->error, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  if (err) {
+    // leave the grid fresh rather than half-written
+    fill_cells_kernel<<<grid_blocks(g->n_cells / 4), 256, 0, g->stream>>>(g->cells, g->n_cells);
+    DBT_CHECK_LAUNCH("fill_cells_kernel");
+    DBT_CUDA(cudaStreamSynchronize(g->stream));
+    if (err & 1)
+      return set_error(DBT_ERR_CORRUPTION,
+                       "distance mask is not a low-bit run (grid.py:118-129); the device word "
+                       "stores the run length");
+    return set_error(DBT_ERR_CORRUPTION, "sign byte outside {0 (occupied), 1 (free)}");
+  }
+  return DBT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origin[3], int device,
+                    int64_t slab_x0, int64_t slab_x1, dbt_grid** out) {
+  *out = nullptr;
+  for (int i = 0; i < 3; ++i)
+    if (dims[i] < 1) return set_error(DBT_ERR_CONFIG, "grid dims must be three positive counts");
+  for (int i = 0; i < 3; ++i)
+    if (dims[i] > kMaxDim)
+      return set_error(DBT_ERR_CONFIG, "grid dim exceeds 2^21-1 voxels (packed centre encoding)");
+  if (!(voxel_size > 0.0)) return set_error(DBT_ERR_CONFIG, "voxel_size must be positive");
+  if (slab_x0 < 0 || slab_x1 > dims[0] || slab_x0 >= slab_x1)
+    return set_error(DBT_ERR_CONFIG, "slab [x0, x1) must be a non-empty range inside [0, nx)");
+  dbt_grid* g = new dbt_grid();
+  g->device = device;
+  g->nx = dims[0];
+  g->ny = dims[1];
+  g->nz = dims[2];
+  g->nzp = (dims[2] + 3) & ~int64_t(3);
+  g->x0 = slab_x0;
+  g->x1 = slab_x1;
+  g->vs = voxel_size;
+  for (int i = 0; i < 3; ++i) g->org[i] = origin[i];
+  g->n_cells = (g->x1 - g->x0) * g->ny * g->nzp;
+  int rc = grid_set_device(g);
+  if (rc) {
+    delete g;
+    return rc;
+  }
+  // +64 cells of slack: the sweep's aligned 4-cell chunks may read up to 3
+  // cells past the last row of the slab (never written).
+  cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_error(e, "cudaMalloc(voxel grid)");
+  }
+  cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  cudaEventCreate(&g->ev_a);
+  cudaEventCreate(&g->ev_b);
+  cudaEventCreateWithFlags(&g->ev_meta, cudaEventDisableTiming);
+  e = cudaMalloc(&g->d_lcnt, sizeof(LaunchCounters));
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_scnt, sizeof(ScanCounters) * kMaxScansPerLaunch);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_poses, sizeof(double) * 12 * kMaxScansPerLaunch);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_scan_off, sizeof(int64_t) * (kMaxScansPerLaunch + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_src_off, sizeof(int64_t) * (kMaxScansPerLaunch + 1));
+  if (e == cudaSuccess) e = cudaHostAlloc(&g->h_lcnt, sizeof(LaunchCounters), cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(&g->h_scnt, sizeof(ScanCounters) * kMaxScansPerLaunch, cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(&g->h_meta, sizeof(int64_t) * 2 * (kMaxScansPerLaunch + 1), cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(&g->h_poses, sizeof(double) * 12 * kMaxScansPerLaunch, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    int code = cuda_error(e, "grid metadata allocation");
+    dbt_grid_destroy(g);
+    return code;
+  }
+  rc = dbt_grid_reset(g);
+  if (rc) {
+    dbt_grid_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return DBT_OK;
+}
+
+int dbt_grid_destroy(dbt_grid* g) {
+  if (!g) return DBT_OK;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  dbt::prof_flush(g);
+  for (auto e : g->event_pool) cudaEventDestroy(e);
+  void* dev[] = {g->cells,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
+                 g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_poses,   g->d_scan_off,
+                 g->d_src_off, g->d_scnt, g->d_lcnt, g->d_stage, g->d_rowoff, g->d_rowdx};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  void* host[] = {g->h_scnt, g->h_lcnt, g->h_meta, g->h_poses};
+  for (void* p : host)
+    if (p) cudaFreeHost(p);
+  if (g->ev_a) cudaEventDestroy(g->ev_a);
+  if (g->ev_b) cudaEventDestroy(g->ev_b);
+  if (g->ev_meta) cudaEventDestroy(g->ev_meta);
+  if (g->stream && g->own_stream) cudaStreamDestroy(g->stream);
+  delete g;
+  return DBT_OK;
+}
+
+int dbt_grid_reset(dbt_grid* g) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
+  DBT_CHECK_LAUNCH("fill_cells_kernel");
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  return DBT_OK;
+}
+
+int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* device_bytes) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  dims[0] = g->nx;
+  dims[1] = g->ny;
+  dims[2] = g->nz;
+  slab[0] = g->x0;
+  slab[1] = g->x1;
+  *device_bytes = (g->n_cells + 64) * (int64_t)sizeof(uint32_t);
+  return DBT_OK;
+}
+
+int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
+  rc = ensure_stage(g, xs * plane * 6);
+  if (rc) return rc;
+  DBT_CUDA(cudaMemsetAsync(&g->d_lcnt->error, 0, sizeof(int), g->stream));
+  uint8_t* st = (uint8_t*)g->d_stage;
+  for (int64_t x = 0; x < lx; x += xs) {
+    int64_t cx = std::min(xs, lx - x), n = cx * plane;
+    uint32_t* dm = (uint32_t*)st;
+    uint8_t* ds = st + 4 * n;
+    uint8_t* dh = ds + n;
+    DBT_CUDA(cudaMemcpyAsync(dm, mask + x * plane, 4 * n, cudaMemcpyHostToDevice, g->stream));
+    DBT_CUDA(cudaMemcpyAsync(ds, sign + x * plane, n, cudaMemcpyHostToDevice, g->stream));
+    DBT_CUDA(cudaMemcpyAsync(dh, hits + x * plane, n, cudaMemcpyHostToDevice, g->stream));
+    encode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, dm, ds, dh, n,
+                                                         g->nz, g->nzp, &g->d_lcnt->error);
+    DBT_CHECK_LAUNCH("encode_kernel");
+  }
+  return check_upload_error(g);
+}
+
+int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
+  rc = ensure_stage(g, xs * plane * 6);
+  if (rc) return rc;
+  uint8_t* st = (uint8_t*)g->d_stage;
+  for (int64_t x = 0; x < lx; x += xs) {
+    int64_t cx = std::min(xs, lx - x), n = cx * plane;
+    uint32_t* dm = (uint32_t*)st;
+    uint8_t* ds = st + 4 * n;
+    uint8_t* dh = ds + n;
+    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, dm, ds, dh, n,
+                                                         g->nz, g->nzp);
+    DBT_CHECK_LAUNCH("decode_kernel");
+    DBT_CUDA(cudaMemcpyAsync(mask + x * plane, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
+    DBT_CUDA(cudaMemcpyAsync(sign + x * plane, ds, n, cudaMemcpyDeviceToHost, g->stream));
+    DBT_CUDA(cudaMemcpyAsync(hits + x * plane, dh, n, cudaMemcpyDeviceToHost, g->stream));
+    DBT_CUDA(cudaStreamSynchronize(g->stream));  // staging reused by the next slice
+  }
+  return DBT_OK;
+}
+
+static int readout(dbt_grid* g, int mode, int32_t* pop, uint8_t* obs, double* sdf) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  const int64_t per = mode == 0 ? 4 : (mode == 1 ? 1 : 9);
+  int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * per)));
+  rc = ensure_stage(g, xs * plane * per);
+  if (rc) return rc;
+  uint8_t* st = (uint8_t*)g->d_stage;
+  for (int64_t x = 0; x < lx; x += xs) {
+    int64_t cx = std::min(xs, lx - x), n = cx * plane;
+    int32_t* dp = (int32_t*)st;
+    double* dsdf = (double*)st;
+    uint8_t* dob = mode == 2 ? st + 8 * n : st;
+    readout_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, mode, dp, dob,
+                                                          dsdf, g->vs, n, g->nz, g->nzp);
+    DBT_CHECK_LAUNCH("readout_kernel");
+    if (mode == 0) {
+      DBT_CUDA(cudaMemcpyAsync(pop + x * plane, dp, 4 * n, cudaMemcpyDeviceToHost, g->stream));
+    } else {
+      DBT_CUDA(cudaMemcpyAsync(obs + x * plane, dob, n, cudaMemcpyDeviceToHost, g->stream));
+      if (mode == 2)
+        DBT_CUDA(cudaMemcpyAsync(sdf + x * plane, dsdf, 8 * n, cudaMemcpyDeviceToHost, g->stream));
+    }
+    DBT_CUDA(cudaStreamSynchronize(g->stream));
+  }
+  return DBT_OK;
+}
+
+int dbt_popcount(dbt_grid* g, int32_t* out) { return readout(g, 0, out, nullptr, nullptr); }
+int dbt_observed(dbt_grid* g, uint8_t* out) { return readout(g, 1, nullptr, out, nullptr); }
+int dbt_signed_distance_field(dbt_grid* g, double* field, uint8_t* observed) {
+  return readout(g, 2, nullptr, observed, field);
+}
+
+int dbt_grid_counts(dbt_grid* g, int64_t* observed, int64_t* occupied) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  rc = ensure_stage(g, 16);
+  if (rc) return rc;
+  unsigned long long* d = (unsigned long long*)g->d_stage;
+  DBT_CUDA(cudaMemsetAsync(d, 0, 16, g->stream));
+  const int64_t n = (g->x1 - g->x0) * g->ny * g->nz;
+  count_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, n, g->nz, g->nzp, d);
+  DBT_CHECK_LAUNCH("count_kernel");
+  unsigned long long h[2];
+  DBT_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, g->stream));
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  *observed = (int64_t)h[0];
+  *occupied = (int64_t)h[1];
+  return DBT_OK;
+}
+
+int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, uint8_t* sign, uint8_t* hits) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    if (x < g->x0 || x >= g->x1 || y < 0 || y >= g->ny || z < 0 || z >= g->nz)
+      return set_error(DBT_ERR_CONFIG, "voxel index outside the grid (or the owned slab)");
+  }
+  if (n == 0) return DBT_OK;
+  rc = ensure_stage(g, n * 30);
+  if (rc) return rc;
+  uint8_t* st = (uint8_t*)g->d_stage;
+  int64_t* didx = (int64_t*)st;
+  uint32_t* dm = (uint32_t*)(st + 24 * n);
+  uint8_t* ds = st + 28 * n;
+  uint8_t* dh = ds + n;
+  DBT_CUDA(cudaMemcpyAsync(didx, xyz, 24 * n, cudaMemcpyHostToDevice, g->stream));
+  gather_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, didx, n, g->x0, g->ny, g->nzp, dm, ds, dh);
+  DBT_CHECK_LAUNCH("gather_kernel");
+  if (mask) DBT_CUDA(cudaMemcpyAsync(mask, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
+  if (sign) DBT_CUDA(cudaMemcpyAsync(sign, ds, n, cudaMemcpyDeviceToHost, g->stream));
+  if (hits) DBT_CUDA(cudaMemcpyAsync(hits, dh, n, cudaMemcpyDeviceToHost, g->stream));
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  return DBT_OK;
+}
+
+int dbt_grid_to_records(dbt_grid* g, void* out_records) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (g->x0 != 0 || g->x1 != g->nx)
+    return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
+  if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
+  const int64_t plane = g->nx * g->ny;
+  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
+  rc = ensure_stage(g, zs * plane * 8);
+  if (rc) return rc;
+  uint64_t* st = (uint64_t*)g->d_stage;
+  for (int64_t z = 0; z < g->nz; z += zs) {
+    int64_t zc = std::min(zs, g->nz - z);
+    dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
+    to_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc);
+    DBT_CHECK_LAUNCH("to_records_kernel");
+    DBT_CUDA(cudaMemcpyAsync((uint64_t*)out_records + z * plane, st, zc * plane * 8,
+                             cudaMemcpyDeviceToHost, g->stream));
+    DBT_CUDA(cudaStreamSynchronize(g->stream));
+  }
+  return DBT_OK;
+}
+
+int dbt_grid_from_records(dbt_grid* g, const void* records) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
+  if (g->x0 != 0 || g->x1 != g->nx)
+    return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
+  const int64_t plane = g->nx * g->ny;
+  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
+  rc = ensure_stage(g, zs * plane * 8);
+  if (rc) return rc;
+  DBT_CUDA(cudaMemsetAsync(&g->d_lcnt->error, 0, sizeof(int), g->stream));
+  uint64_t* st = (uint64_t*)g->d_stage;
+  for (int64_t z = 0; z < g->nz; z += zs) {
+    int64_t zc = std::min(zs, g->nz - z);
+    DBT_CUDA(cudaMemcpyAsync(st, (const uint64_t*)records + z * plane, zc * plane * 8,
+                             cudaMemcpyHostToDevice, g->stream));
+    dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
+    from_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc,
+                                                             &g->d_lcnt->error);
+    DBT_CHECK_LAUNCH("from_records_kernel");
+    DBT_CUDA(cudaStreamSynchronize(g->stream));
+  }
+  return check_upload_error(g);
+}
+
+}  // extern "C"

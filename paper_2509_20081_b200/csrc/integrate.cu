@@ -1,0 +1,821 @@
+// integrate.cu — the scan-integration hot path (reference integrator.py:139-287).
+//
+// One launch sequence per scan (or per batch of scans):
+//   prep_kernel    one thread per return: sensor->map transform (numpy's
+//                  matmul FMA chain, integrator.py:232), ray, norm, degenerate
+//                  and boundary discards (integrator.py:192-199), centre voxel
+//                  (grid.py:107-111), direction bin (kernels.py:49-57),
+//                  centre dedup / first-return in a device hash table
+//                  (integrator.py:256-262), per-scan counters.
+//   shadow_kernel  one thread per (applied return, shadow offset): saturating
+//                  hit increment + occupied sign (integrator.py:151-159) as a
+//                  16-bit CAS on the voxel word.
+//   sweep_kernel   one warp per unique centre voxel: the K^3 AND sweep
+//                  (integrator.py:145-149) as min(run length, d) with 64-bit
+//                  (4-voxel) loads, skip-if-unchanged, CAS only on change.
+//
+// Order independence: every voxel update is an atomic application of a
+// monotone function (min on the run length; h -> h + (h < h_max) with the
+// sign set when h >= T) and the functions for different returns commute, so
+// the final grid equals the reference's serial sorted-order stamping
+// (integrator.py:266-284) for any schedule. Duplicate centres stamp the same
+// mask (AND is idempotent), so the sweep runs once per distinct centre.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include <chrono>
+
+#include "engine.cuh"
+
+using namespace dbt;
+
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586;     // 2.0 * math.pi   (kernels.py:28)
+constexpr double kPi = 3.141592653589793;        // np.pi
+constexpr double kHalfPi = 1.5707963267948966;   // np.pi / 2       (kernels.py:56)
+constexpr double kKnifeEps = 1e-12;
+
+struct PrepArgs {
+  const void* pts;
+  const double* sensor;  // map-frame mode: per-point sensor positions
+  int dtype;
+  int S;
+  int ds;
+  int map_mode;
+  int64_t n;
+  const int64_t* scan_off;
+  const int64_t* src_off;
+  const double* poses;  // S x 12 : R row-major (9), t (3)
+  int64_t nx, ny, nz;
+  double vs, ox, oy, oz;
+  int R, b_az, b_el;
+  int skip_norm;
+  int first_return;
+  int key_scan_bits;  // first-return over several scans: key includes the scan
+  int no_dedup;       // DBT_FLAG_NO_DEDUP: sweep every applied return
+  uint64_t* center;
+  uint16_t* bin;
+  uint32_t* slot;
+  unsigned long long* hkey;
+  uint32_t* hmin;
+  uint64_t hmask;
+  uint64_t* uniq;
+  LaunchCounters* lc;
+  ScanCounters* sc;
+  int8_t* outcome;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+__device__ __forceinline__ int find_scan(const int64_t* off, int S, int64_t i) {
+  int lo = 0, hi = S;  // off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// bin_index_array (kernels.py:49-57) for one direction whose axis-1 norm is
+// nrm. The transcendental calls are CUDA's atan2/asin (<= 2 ulp); every other
+// step is the same IEEE operation numpy performs. Returns 1 in knife when a
+// raw index lies within kKnifeEps of an interior bin boundary, where an
+// ulp-level difference in atan2/asin could move the point to the next bin.
+__device__ __forceinline__ void bin_dev(double rx, double ry, double rz, double nrm, int b_az,
+                                        int b_el, int& ba, int& be, int& knife) {
+  double az = atan2(ry, rx);
+  if (az < 0.0) az = __dadd_rn(az, kTwoPi);
+  double ra = __dmul_rn(__ddiv_rn(az, kTwoPi), (double)b_az);
+  double q = __ddiv_rn(rz, nrm);
+  q = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);
+  double el = asin(q);
+  double re = __dmul_rn(__ddiv_rn(__dadd_rn(el, kHalfPi), kPi), (double)b_el);
+  long long ia = (long long)ra;  // astype(np.int64) truncates toward zero
+  long long ie = (long long)re;
+  ba = (int)(ia < 0 ? 0 : (ia > b_az - 1 ? b_az - 1 : ia));
+  be = (int)(ie < 0 ? 0 : (ie > b_el - 1 ? b_el - 1 : ie));
+  double na = rint(ra), ne = rint(re);
+  knife = (fabs(ra - na) < kKnifeEps && na >= 1.0 && na <= b_az - 1) ||
+          (fabs(re - ne) < kKnifeEps && ne >= 1.0 && ne <= b_el - 1);
+}
+
+__device__ __forceinline__ bool floor_index(double v, double o, double vs, long long& out) {
+  // np.floor((p - origin) / voxel_size).astype(np.int64) (grid.py:109-111);
+  // values outside int64 (incl. NaN/inf) become an out-of-bounds index.
+  double f = floor(__ddiv_rn(__dsub_rn(v, o), vs));
+  if (!(f >= -9.2e18 && f <= 9.2e18)) {
+    out = LLONG_MIN;
+    return false;
+  }
+  out = (long long)f;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool live = i < a.n;
+  int s = 0;
+  int ok = 0, knife = 0;
+  if (live) {
+    s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+    int64_t src = a.src_off[s] + (i - a.scan_off[s]) * a.ds;
+    double p0, p1, p2;
+    if (a.dtype == DBT_F32) {
+      const float* q = (const float*)a.pts + 3 * src;
+      p0 = q[0];
+      p1 = q[1];
+      p2 = q[2];
+    } else {
+      const double* q = (const double*)a.pts + 3 * src;
+      p0 = q[0];
+      p1 = q[1];
+      p2 = q[2];
+    }
+    double m0, m1, m2, t0, t1, t2;
+    if (a.map_mode) {
+      m0 = p0;
+      m1 = p1;
+      m2 = p2;
+      t0 = a.sensor[3 * src];
+      t1 = a.sensor[3 * src + 1];
+      t2 = a.sensor[3 * src + 2];
+    } else {
+      const double* P = a.poses + 12 * s;
+      t0 = P[9];
+      t1 = P[10];
+      t2 = P[11];
+      // pts @ R.T + t: OpenBLAS dgemm accumulates k = 0,1,2 with FMA
+      // (probed on both the build and the GPU-box hosts), then numpy adds t.
+      m0 = __dadd_rn(__fma_rn(p2, P[2], __fma_rn(p1, P[1], __dmul_rn(p0, P[0]))), t0);
+      m1 = __dadd_rn(__fma_rn(p2, P[5], __fma_rn(p1, P[4], __dmul_rn(p0, P[3]))), t1);
+      m2 = __dadd_rn(__fma_rn(p2, P[8], __fma_rn(p1, P[7], __dmul_rn(p0, P[6]))), t2);
+    }
+    double rx = __dsub_rn(m0, t0), ry = __dsub_rn(m1, t1), rz = __dsub_rn(m2, t2);
+    // np.linalg.norm(rays, axis=1): sqrt((x*x + y*y) + z*z), no FMA
+    double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
+    ok = a.skip_norm ? 1 : (nrm >= a.vs);
+    long long cx, cy, cz;
+    bool fx = floor_index(m0, a.ox, a.vs, cx);
+    bool fy = floor_index(m1, a.oy, a.vs, cy);
+    bool fz = floor_index(m2, a.oz, a.vs, cz);
+    ok = ok && fx && fy && fz && cx >= a.R && cy >= a.R && cz >= a.R && cx <= a.nx - 1 - a.R &&
+         cy <= a.ny - 1 - a.R && cz <= a.nz - 1 - a.R;
+    uint64_t packed = kEmptyKey;
+    if (ok) {
+      int ba, be;
+      bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, ba, be, knife);
+      a.bin[i] = (uint16_t)(ba * a.b_el + be);
+      packed = pack_center(cx, cy, cz);
+      uint64_t key = (uint64_t)((cx * a.ny + cy) * a.nz + cz);
+      if (a.key_scan_bits) key |= (uint64_t)s << 48;
+      uint64_t h = mix64(key) & a.hmask;
+      if (a.no_dedup) a.uniq[atomicAdd(&a.lc->n_unique, 1ull)] = packed;
+      while (true) {
+        unsigned long long prev = atomicCAS(&a.hkey[h], (unsigned long long)kEmptyKey, (unsigned long long)key);
+        if (prev == kEmptyKey) {
+          if (!a.no_dedup) a.uniq[atomicAdd(&a.lc->n_unique, 1ull)] = packed;
+          break;
+        }
+        if (prev == key) break;
+        h = (h + 1) & a.hmask;
+      }
+      if (a.first_return) atomicMin(&a.hmin[h], (uint32_t)i);
+      a.slot[i] = (uint32_t)h;
+    }
+    a.center[i] = packed;
+    if (a.outcome) a.outcome[i] = ok ? 1 : 0;
+  }
+  // per-scan counters, warp-aggregated when the warp lies inside one scan
+  unsigned act = __ballot_sync(0xffffffffu, live);
+  if (!act) return;
+  int s0 = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
+  bool uniform = __all_sync(0xffffffffu, !live || s == s0);
+  if (uniform) {
+    int nok = __popc(__ballot_sync(0xffffffffu, live && ok));
+    int nkn = __popc(__ballot_sync(0xffffffffu, live && ok && knife));
+    if (lane == __ffs(act) - 1) {
+      if (nok) atomicAdd(&a.sc[s0].n_ok, (unsigned long long)nok);
+      if (nkn) atomicAdd(&a.sc[s0].n_knife, (unsigned long long)nkn);
+    }
+  } else if (live) {
+    if (ok) atomicAdd(&a.sc[s].n_ok, 1ull);
+    if (ok && knife) atomicAdd(&a.sc[s].n_knife, 1ull);
+  }
+}
+
+struct ShadowArgs {
+  uint32_t* cells;
+  const uint64_t* center;
+  const uint16_t* bin;
+  const uint32_t* slot;
+  const uint32_t* hmin;
+  const int8_t* sxyz;
+  const int32_t* sstart;
+  int64_t n;
+  int log2s;  // threads per return = 1 << log2s >= max shadow count
+  int64_t x0, x1, ny, nzp;
+  int h_max, t_occ;
+  int first_return;
+  int S;
+  const int64_t* scan_off;
+  ScanCounters* sc;
+  LaunchCounters* lc;
+};
+
+__global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
+  const int64_t total = a.n << a.log2s;
+  const int64_t smask = (1ll << a.log2s) - 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t >> a.log2s;
+    int k = (int)(t & smask);
+    uint64_t c = a.center[i];
+    if (c == kEmptyKey) continue;
+    if (a.first_return) {
+      if (a.hmin[a.slot[i]] != (uint32_t)i) continue;
+      if (k == 0) {
+        int s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+        atomicAdd(&a.sc[s].n_applied, 1ull);
+      }
+    }
+    int b = a.bin[i];
+    int st = a.sstart[b];
+    if (k >= a.sstart[b + 1] - st) continue;
+    char4 o = reinterpret_cast<const char4*>(a.sxyz)[st + k];
+    int64_t cx, cy, cz;
+    unpack_center(c, cx, cy, cz);
+    int64_t gx = cx + o.x;
+    if (gx < a.x0 || gx >= a.x1) continue;
+    uint32_t* p = a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z);
+    // h += (h < h_max); sign <- occupied when h >= T (integrator.py:154-159)
+    uint32_t old = *p;
+    while (true) {
+      uint32_t h = old >> kHitsShift;
+      uint32_t hn = h + (h < (uint32_t)a.h_max ? 1u : 0u);
+      uint32_t nw = (old & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
+      if (hn >= (uint32_t)a.t_occ) nw &= ~kFreeBit;
+      if (nw == old) break;
+      uint32_t prev = atomicCAS(p, old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+  }
+}
+
+struct SweepArgs {
+  uint32_t* cells;
+  const uint64_t* uniq;
+  const LaunchCounters* lc_in;
+  unsigned long long* changed_out;
+  const uint32_t* dtab;   // [4][rows][CH]
+  const int64_t* rowoff;  // [rows]
+  int K, R;
+  int64_t x0, x1, ny, nzp;
+};
+
+// Lower cell p to run length d (generic path, any d in 0..32): CAS on the word.
+__device__ __forceinline__ int lower_cas(uint32_t* p, uint32_t old, int d) {
+  while (cell_len(old) > d) {
+    uint32_t prev = atomicCAS(p, old, cell_with_len(old, d));
+    if (prev == old) return 1;
+    old = prev;
+  }
+  return 0;
+}
+
+// Warp per unique centre. Row-major chunk order (row = (dx+R)*K + (dy+R),
+// 4-voxel chunks along z) so consecutive lanes read consecutive 16-byte
+// words of the same z-row: one 21-voxel row is six 128-bit loads.
+// FAST (every kernel distance <= 18): "d lowers the cell" is bit d of the
+// word, the update a fire-and-forget atomicAnd. Otherwise CAS per cell.
+template <int CH, bool FAST>
+__global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int rows = a.K * a.K;
+  uint32_t* dtab = reinterpret_cast<uint32_t*>(smem_raw);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(smem_raw + ((4 * rows * CH * 4 + 15) & ~15));
+  for (int i = threadIdx.x; i < 4 * rows * CH; i += blockDim.x) dtab[i] = a.dtab[i];
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) rowoff[i] = a.rowoff[i];
+  __syncthreads();
+
+  const int64_t n_unique = (int64_t)a.lc_in->n_unique;
+  const int64_t per = (n_unique + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per;
+  const int64_t hi = min(lo + per, n_unique);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  unsigned long long changed = 0;
+
+  for (int64_t u = lo + warp; u < hi; u += nwarps) {
+    int64_t cx, cy, cz;
+    unpack_center(a.uniq[u], cx, cy, cz);
+    const int64_t zs = cz - a.R;  // >= 0: boundary discard guarantees it
+    const int sh = (int)(zs & 3);
+    const int64_t base = ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(3));
+    // slab clip (multi-GPU): rows are dx-major, so the owned dx range is a
+    // contiguous range of chunk indices
+    const int64_t dxlo = max((int64_t)-a.R, a.x0 - cx);
+    const int64_t dxhi = min((int64_t)a.R, a.x1 - 1 - cx);
+    if (dxlo > dxhi) continue;
+    const int jlo = (int)((dxlo + a.R) * a.K * CH);
+    const int jhi = (int)((dxhi + a.R + 1) * a.K * CH);
+    const uint32_t* dt = dtab + sh * rows * CH;
+#pragma unroll 4
+    for (int j = jlo + lane; j < jhi; j += 32) {
+      const int row = j / CH;
+      const int ch = j - row * CH;
+      uint32_t* p = a.cells + base + rowoff[row] + 4 * ch;
+      const uint4 w = *reinterpret_cast<const uint4*>(p);
+      const uint32_t d4 = dt[j];
+      if (FAST) {
+        // bit d of the word is set <=> stored distance > d; d = 63 (outside
+        // the kernel) clamps to a zero probe
+        const uint32_t p0 = __funnelshift_lc(0u, 1u, d4 & 0xFF);
+        const uint32_t p1 = __funnelshift_lc(0u, 1u, (d4 >> 8) & 0xFF);
+        const uint32_t p2 = __funnelshift_lc(0u, 1u, (d4 >> 16) & 0xFF);
+        const uint32_t p3 = __funnelshift_lc(0u, 1u, d4 >> 24);
+        if ((w.x & p0) | (w.y & p1) | (w.z & p2) | (w.w & p3)) {
+          if (w.x & p0) changed += (atomicAnd(p + 0, kKeepSignHits | (p0 - 1u)) & p0) != 0;
+          if (w.y & p1) changed += (atomicAnd(p + 1, kKeepSignHits | (p1 - 1u)) & p1) != 0;
+          if (w.z & p2) changed += (atomicAnd(p + 2, kKeepSignHits | (p2 - 1u)) & p2) != 0;
+          if (w.w & p3) changed += (atomicAnd(p + 3, kKeepSignHits | (p3 - 1u)) & p3) != 0;
+        }
+      } else {
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int d = (d4 >> (8 * b)) & 0xFF;
+          if (d <= 32 && d < cell_len(ws[b])) changed += lower_cas(p + b, ws[b], d);
+        }
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  if (lane == 0 && changed) atomicAdd(a.changed_out, changed);
+}
+
+typedef void (*SweepFn)(SweepArgs);
+
+template <bool FAST>
+SweepFn sweep_fn_t(int CH) {
+  switch (CH) {
+    case 1: return sweep_kernel<1, FAST>;
+    case 2: return sweep_kernel<2, FAST>;
+    case 3: return sweep_kernel<3, FAST>;
+    case 4: return sweep_kernel<4, FAST>;
+    case 5: return sweep_kernel<5, FAST>;
+    case 6: return sweep_kernel<6, FAST>;
+    case 7: return sweep_kernel<7, FAST>;
+    case 8: return sweep_kernel<8, FAST>;
+    case 9: return sweep_kernel<9, FAST>;
+  }
+  return nullptr;
+}
+
+SweepFn sweep_fn(int CH, bool fast) { return fast ? sweep_fn_t<true>(CH) : sweep_fn_t<false>(CH); }
+
+size_t sweep_smem_bytes(int K, int CH) {
+  return ((size_t)(4 * K * K * CH * 4 + 15) & ~size_t(15)) + (size_t)K * K * 8;
+}
+
+__global__ void bin_kernel(const double* __restrict__ dirs, int64_t n, int b_az, int b_el,
+                           int64_t* __restrict__ oa, int64_t* __restrict__ oe) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double x = dirs[3 * i], y = dirs[3 * i + 1], z = dirs[3 * i + 2];
+    double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    int ba, be, kn;
+    bin_dev(x, y, z, nrm, b_az, b_el, ba, be, kn);
+    oa[i] = ba;
+    oe[i] = be;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+int grow(void** p, int64_t* cap, int64_t need, size_t elem) {
+  if (need <= *cap) return DBT_OK;
+  int64_t c = std::max<int64_t>(need, *cap + *cap / 2);
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  DBT_CUDA(cudaMalloc(p, (size_t)c * elem));
+  *cap = c;
+  return DBT_OK;
+}
+
+int ensure_points(dbt_grid* g, int64_t n) {
+  if (n <= g->cap_pts) return DBT_OK;
+  int64_t c = std::max<int64_t>(n, g->cap_pts + g->cap_pts / 2);
+  void* ptrs[] = {g->d_center, g->d_bin, g->d_slot};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (g->d_uniq) cudaFree(g->d_uniq);
+  g->d_center = nullptr;
+  g->d_bin = nullptr;
+  g->d_slot = nullptr;
+  g->d_uniq = nullptr;
+  g->cap_pts = 0;
+  DBT_CUDA(cudaMalloc(&g->d_center, c * sizeof(uint64_t)));
+  DBT_CUDA(cudaMalloc(&g->d_bin, c * sizeof(uint16_t)));
+  DBT_CUDA(cudaMalloc(&g->d_slot, c * sizeof(uint32_t)));
+  DBT_CUDA(cudaMalloc(&g->d_uniq, c * sizeof(uint64_t)));
+  g->cap_pts = c;
+  return DBT_OK;
+}
+
+int ensure_hash(dbt_grid* g, int64_t n) {
+  int64_t want = 1024;
+  while (want < 2 * n) want <<= 1;
+  if (want <= g->cap_hash) return DBT_OK;
+  if (g->d_hkey) cudaFree(g->d_hkey);
+  if (g->d_hmin) cudaFree(g->d_hmin);
+  g->d_hkey = nullptr;
+  g->d_hmin = nullptr;
+  g->cap_hash = 0;
+  DBT_CUDA(cudaMalloc(&g->d_hkey, want * sizeof(unsigned long long)));
+  DBT_CUDA(cudaMalloc(&g->d_hmin, want * sizeof(uint32_t)));
+  g->cap_hash = want;
+  return DBT_OK;
+}
+
+int ensure_rows(dbt_grid* g, const dbt_bank* b) {
+  if (g->tab_bank == b->serial && g->d_rowoff) return DBT_OK;
+  const int K = b->K, R = b->R, rows = K * K;
+  std::vector<int64_t> ro(rows);
+  for (int r = 0; r < rows; ++r) {
+    int dx = r / K - R, dy = r % K - R;
+    ro[r] = ((int64_t)dx * g->ny + dy) * g->nzp;
+  }
+  if (g->d_rowoff) cudaFree(g->d_rowoff);
+  g->d_rowoff = nullptr;
+  DBT_CUDA(cudaMalloc(&g->d_rowoff, rows * sizeof(int64_t)));
+  DBT_CUDA(cudaMemcpy(g->d_rowoff, ro.data(), rows * sizeof(int64_t), cudaMemcpyHostToDevice));
+  g->tab_bank = b->serial;
+  g->tab_K = K;
+  return DBT_OK;
+}
+
+int validate_params(const dbt_params* p) {
+  if (!p) return set_error(DBT_ERR_CONFIG, "null params");
+  if (!(1 <= p->t_occ && p->t_occ <= p->h_max && p->h_max <= 255))
+    return set_error(DBT_ERR_CONFIG, "need 1 <= T <= H_max <= 255 (integrator.py:64-67)");
+  if (p->downsample < 1) return set_error(DBT_ERR_CONFIG, "downsample factor must be >= 1");
+  return DBT_OK;
+}
+
+// Core launch sequence. Points are already on the device (d_pts). counts /
+// poses are host arrays. map_sensor (device) selects the map-frame mode.
+int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtype,
+                     const int64_t* counts, int S, const double* poses, const dbt_params* p,
+                     const double* d_map_sensor, int8_t* d_outcome, cudaStream_t st) {
+  if (S < 1 || S > kMaxScansPerLaunch) return set_error(DBT_ERR_CONFIG, "scan count per launch out of range");
+  if (b->device != g->device) return set_error(DBT_ERR_CONFIG, "bank and grid live on different devices");
+  if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
+  if (b->K > g->nx || b->K > g->ny || b->K > g->nz) {
+    // every return is discarded by the boundary rule; nothing to launch
+  }
+  const int ds = d_map_sensor ? 1 : p->downsample;
+  // offsets in pinned staging; wait until the previous launch consumed them
+  int64_t* h_scan = g->h_meta;
+  int64_t* h_src = g->h_meta + (kMaxScansPerLaunch + 1);
+  DBT_CUDA(cudaEventSynchronize(g->ev_meta));
+  h_scan[0] = 0;
+  h_src[0] = 0;
+  g->last_points_in.assign(S, 0);
+  for (int s = 0; s < S; ++s) {
+    if (counts[s] < 0) return set_error(DBT_ERR_CONFIG, "negative point count");
+    int64_t m = (counts[s] + ds - 1) / ds;
+    g->last_points_in[s] = m;
+    h_scan[s + 1] = h_scan[s] + m;
+    h_src[s + 1] = h_src[s] + counts[s];
+    if (!d_map_sensor) {
+      const double* P = poses + 16 * s;
+      double* D = g->h_poses + 12 * s;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) D[3 * r + c] = P[4 * r + c];
+      D[9] = P[3];
+      D[10] = P[7];
+      D[11] = P[11];
+    }
+  }
+  g->last_scans = S;
+  const int64_t n = h_scan[S];
+  int rc = ensure_points(g, std::max<int64_t>(n, 1));
+  if (!rc) rc = ensure_hash(g, std::max<int64_t>(n, 1));
+  if (!rc) rc = ensure_rows(g, b);
+  if (rc) return rc;
+  DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  DBT_CUDA(cudaMemcpyAsync(g->d_src_off, h_src, (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (!d_map_sensor)
+    DBT_CUDA(cudaMemcpyAsync(g->d_poses, g->h_poses, S * 12 * sizeof(double), cudaMemcpyHostToDevice, st));
+  DBT_CUDA(cudaEventRecord(g->ev_meta, st));
+  g->last_first_return = p->first_return ? 1 : 0;
+  DBT_CUDA(cudaMemsetAsync(g->d_scnt, 0, S * sizeof(ScanCounters), st));
+  DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters), st));
+  if (n == 0) return DBT_OK;
+  const int64_t hcap = [&] {
+    int64_t w = 1024;
+    while (w < 2 * n) w <<= 1;
+    return w;
+  }();
+  DBT_CUDA(cudaMemsetAsync(g->d_hkey, 0xFF, hcap * sizeof(unsigned long long), st));
+  if (p->first_return) DBT_CUDA(cudaMemsetAsync(g->d_hmin, 0xFF, hcap * sizeof(uint32_t), st));
+
+  PrepArgs pa;
+  pa.pts = d_pts;
+  pa.sensor = d_map_sensor;
+  pa.dtype = dtype;
+  pa.S = S;
+  pa.ds = ds;
+  pa.map_mode = d_map_sensor != nullptr;
+  pa.n = n;
+  pa.scan_off = g->d_scan_off;
+  pa.src_off = g->d_src_off;
+  pa.poses = g->d_poses;
+  pa.nx = g->nx;
+  pa.ny = g->ny;
+  pa.nz = g->nz;
+  pa.vs = g->vs;
+  pa.ox = g->org[0];
+  pa.oy = g->org[1];
+  pa.oz = g->org[2];
+  pa.R = b->R;
+  pa.b_az = b->b_az;
+  pa.b_el = b->b_el;
+  pa.skip_norm = (p->flags & DBT_FLAG_SKIP_NORM_CHECK) ? 1 : 0;
+  pa.first_return = p->first_return ? 1 : 0;
+  pa.key_scan_bits = (p->first_return && S > 1) ? 1 : 0;
+  pa.no_dedup = ((p->flags & DBT_FLAG_NO_DEDUP) && !p->first_return) ? 1 : 0;
+  pa.center = g->d_center;
+  pa.bin = g->d_bin;
+  pa.slot = g->d_slot;
+  pa.hkey = g->d_hkey;
+  pa.hmin = g->d_hmin;
+  pa.hmask = (uint64_t)(hcap - 1);
+  pa.uniq = g->d_uniq;
+  pa.lc = g->d_lcnt;
+  pa.sc = g->d_scnt;
+  pa.outcome = d_outcome;
+  int tok;
+  prof_begin(g, "prep_kernel", st, &tok);
+  prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa);
+  prof_end(g, st, tok);
+  DBT_CHECK_LAUNCH("prep_kernel");
+
+  if (b->max_shadow > 0) {
+    ShadowArgs sa;
+    sa.cells = g->cells;
+    sa.center = g->d_center;
+    sa.bin = g->d_bin;
+    sa.slot = g->d_slot;
+    sa.hmin = g->d_hmin;
+    sa.sxyz = b->d_shadow_xyz;
+    sa.sstart = b->d_shadow_start;
+    sa.n = n;
+    int l2 = 0;
+    while ((1 << l2) < b->max_shadow) ++l2;
+    sa.log2s = l2;
+    sa.x0 = g->x0;
+    sa.x1 = g->x1;
+    sa.ny = g->ny;
+    sa.nzp = g->nzp;
+    sa.h_max = p->h_max;
+    sa.t_occ = p->t_occ;
+    sa.first_return = p->first_return ? 1 : 0;
+    sa.S = S;
+    sa.scan_off = g->d_scan_off;
+    sa.sc = g->d_scnt;
+    sa.lc = g->d_lcnt;
+    int64_t total = n << l2;
+    unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
+    prof_begin(g, "shadow_kernel", st, &tok);
+    shadow_kernel<<<blocks, 256, 0, st>>>(sa);
+    prof_end(g, st, tok);
+    DBT_CHECK_LAUNCH("shadow_kernel");
+  }
+
+  const int CH = b->chunks_per_row;
+  const bool fast = b->max_d <= kMaxFastD;
+  SweepFn fn = sweep_fn(CH, fast);
+  if (!fn) return set_error(DBT_ERR_CONFIG, "unsupported kernel size for the sweep");
+  const size_t smem = sweep_smem_bytes(b->K, CH);
+  const int shape_key = CH * 2 + (fast ? 1 : 0);
+  if (g->sweep_ch != shape_key) {
+    DBT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, sms = 0;
+    DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+    DBT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    g->sweep_blocks = std::max(per_sm, 1) * sms;
+    g->sweep_ch = shape_key;
+  }
+  SweepArgs wa;
+  wa.cells = g->cells;
+  wa.uniq = g->d_uniq;
+  wa.lc_in = g->d_lcnt;
+  wa.changed_out = &g->d_lcnt->changed;
+  wa.dtab = b->d_dtab;
+  wa.rowoff = g->d_rowoff;
+  wa.K = b->K;
+  wa.R = b->R;
+  wa.x0 = g->x0;
+  wa.x1 = g->x1;
+  wa.ny = g->ny;
+  wa.nzp = g->nzp;
+  unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 7) / 8));
+  prof_begin(g, "sweep_kernel", st, &tok);
+  fn<<<blocks, 256, smem, st>>>(wa);
+  prof_end(g, st, tok);
+  DBT_CHECK_LAUNCH("sweep_kernel");
+  return DBT_OK;
+}
+
+int fetch_counters(dbt_grid* g, cudaStream_t st) {
+  DBT_CUDA(cudaMemcpyAsync(g->h_scnt, g->d_scnt, g->last_scans * sizeof(ScanCounters),
+                           cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaMemcpyAsync(g->h_lcnt, g->d_lcnt, sizeof(LaunchCounters), cudaMemcpyDeviceToHost, st));
+  return DBT_OK;
+}
+
+void fill_stats(dbt_grid* g, const dbt_params* p, dbt_stats* out, int S) {
+  for (int s = 0; s < S; ++s) {
+    dbt_stats& o = out[s];
+    std::memset(&o, 0, sizeof(o));
+    o.points_in = g->last_points_in[s];
+    int64_t nok = (int64_t)g->h_scnt[s].n_ok;
+    o.points_discarded = o.points_in - nok;
+    o.points_applied = p->first_return ? (int64_t)g->h_scnt[s].n_applied : nok;
+    o.knife_edges = (int64_t)g->h_scnt[s].n_knife;
+    if (s == 0) {
+      o.voxels_written = (int64_t)g->h_lcnt->changed;
+      o.unique_centers = (int64_t)g->h_lcnt->n_unique;
+    }
+  }
+}
+
+int check(dbt_grid* g, const dbt_bank* b) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  if (!b) return set_error(DBT_ERR_CONFIG, "null bank handle");
+  return grid_set_device(g);
+}
+
+int stage_raw(dbt_grid* g, int64_t bytes) { return grow(&g->d_raw, &g->cap_raw_bytes, bytes, 1); }
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, const int64_t* counts,
+                   int S, const double* poses, const dbt_params* p, dbt_stats* out) {
+  double t0 = now_ms();
+  int rc = check(g, b);
+  if (!rc) rc = validate_params(p);
+  if (rc) return rc;
+  int64_t total = 0;
+  for (int s = 0; s < S; ++s) total += counts[s];
+  if (total == 0) {
+    // empty scan: zeroed stats, no device work (integrator.py:219-221)
+    for (int s = 0; s < S; ++s) std::memset(&out[s], 0, sizeof(dbt_stats));
+    out[0].elapsed_ms = now_ms() - t0;
+    return DBT_OK;
+  }
+  const size_t esz = dtype == DBT_F32 ? 12 : 24;
+  rc = stage_raw(g, total * (int64_t)esz);
+  if (rc) return rc;
+  cudaStream_t st = g->stream;
+  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
+  rc = launch_integrate(g, b, g->d_raw, dtype, counts, S, poses, p, nullptr, nullptr, st);
+  if (rc) return rc;
+  rc = fetch_counters(g, st);
+  if (rc) return rc;
+  DBT_CUDA(cudaEventRecord(g->ev_b, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  fill_stats(g, p, out, S);
+  float dms = 0.f;
+  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
+  out[0].device_ms = dms;
+  out[0].elapsed_ms = now_ms() - t0;
+  return DBT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
+                        const double pose[16], const dbt_params* p, dbt_stats* out) {
+  return integrate_host(g, b, points, dtype, &n, 1, pose, p, out);
+}
+
+int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
+                        const int64_t* counts, int32_t n_scans, const double* poses,
+                        const dbt_params* p, dbt_stats* out) {
+  return integrate_host(g, b, points, dtype, counts, n_scans, poses, p, out);
+}
+
+int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map, const double* sensor,
+                             int64_t n, const dbt_params* p, dbt_stats* out, int8_t* outcome) {
+  double t0 = now_ms();
+  int rc = check(g, b);
+  if (!rc) rc = validate_params(p);
+  if (rc) return rc;
+  std::memset(out, 0, sizeof(dbt_stats));
+  if (n == 0) return DBT_OK;
+  dbt_params q = *p;
+  q.downsample = 1;
+  q.first_return = 0;
+  rc = stage_raw(g, n * 24);
+  if (!rc) rc = grow((void**)&g->d_sensor, &g->cap_sensor, n * 3, sizeof(double));
+  if (!rc && outcome) rc = grow((void**)&g->d_outcome, &g->cap_outcome, n, 1);
+  if (rc) return rc;
+  cudaStream_t st = g->stream;
+  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  DBT_CUDA(cudaMemcpyAsync(g->d_raw, p_map, n * 24, cudaMemcpyHostToDevice, st));
+  DBT_CUDA(cudaMemcpyAsync(g->d_sensor, sensor, n * 24, cudaMemcpyHostToDevice, st));
+  rc = launch_integrate(g, b, g->d_raw, DBT_F64, &n, 1, nullptr, &q, g->d_sensor,
+                        outcome ? g->d_outcome : nullptr, st);
+  if (rc) return rc;
+  rc = fetch_counters(g, st);
+  if (rc) return rc;
+  if (outcome) DBT_CUDA(cudaMemcpyAsync(outcome, g->d_outcome, n, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaEventRecord(g->ev_b, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  fill_stats(g, &q, out, 1);
+  float dms = 0.f;
+  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
+  out->device_ms = dms;
+  out->elapsed_ms = now_ms() - t0;
+  return DBT_OK;
+}
+
+int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, int dtype,
+                         const int64_t* counts, int32_t n_scans, const double* poses,
+                         const dbt_params* p, void* stream) {
+  int rc = check(g, b);
+  if (!rc) rc = validate_params(p);
+  if (rc) return rc;
+  cudaStream_t st = stream ? (cudaStream_t)stream : g->stream;
+  rc = launch_integrate(g, b, d_points, dtype, counts, n_scans, poses, p, nullptr, nullptr, st);
+  if (rc) return rc;
+  return fetch_counters(g, st);
+}
+
+int dbt_stats_read(dbt_grid* g, dbt_stats* out, int32_t n_scans) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  DBT_CUDA(cudaSetDevice(g->device));
+  DBT_CUDA(cudaDeviceSynchronize());
+  if (n_scans != g->last_scans) return set_error(DBT_ERR_CONFIG, "scan count differs from the last launch");
+  dbt_params q{};
+  q.first_return = g->last_first_return;
+  fill_stats(g, &q, out, n_scans);
+  return DBT_OK;
+}
+
+int dbt_synchronize(dbt_grid* g) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  DBT_CUDA(cudaSetDevice(g->device));
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  return DBT_OK;
+}
+
+int dbt_bin_index_array(const double* dirs, int64_t n, int32_t b_az, int32_t b_el, int64_t* b_a,
+                        int64_t* b_e, int device) {
+  if (n == 0) return DBT_OK;
+  DBT_CUDA(cudaSetDevice(device));
+  double* d_dirs = nullptr;
+  int64_t* d_out = nullptr;
+  DBT_CUDA(cudaMalloc(&d_dirs, n * 24));
+  cudaError_t e = cudaMalloc(&d_out, n * 16);
+  if (e != cudaSuccess) {
+    cudaFree(d_dirs);
+    return cuda_error(e, "cudaMalloc(bins)");
+  }
+  e = cudaMemcpy(d_dirs, dirs, n * 24, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    bin_kernel<<<blocks, 256>>>(d_dirs, n, b_az, b_el, d_out, d_out + n);
+    e = cudaGetLastError();
+    dbt::count_launch();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(b_a, d_out, n * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(b_e, d_out + n, n * 8, cudaMemcpyDeviceToHost);
+  cudaFree(d_dirs);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_error(e, "dbt_bin_index_array");
+  return DBT_OK;
+}
+
+}  // extern "C"
