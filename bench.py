@@ -1,0 +1,373 @@
+"""Benchmark: LiDAR points integrated per second (BASELINE.json metric).
+
+Workload (configs[1] of BASELINE.json, the largest single-GPU config the
+metric is quoted on): config 2 — 100-scan trajectory in the synthetic box
+room, 64 beams x 1024 azimuths (65 536 float32 returns per scan), 0.05 m
+voxels on the 400x400x100 room padded by 11 voxels (422x422x122; the literal
+grid discards every wall return), K=21 kernel, 40x40 bins, shadow radius 1.
+
+A step integrates the next scan of the trajectory into the grid that holds
+all previous scans (the grid is reset when the trajectory wraps, outside the
+timed region). L2 is flushed (256 MB write) between timed steps.
+
+  value : applied returns / device seconds, scans resident in HBM, CUDA
+          events on the launch stream around each step (prep + shadow + sweep
+          + counter copy), summed over K steps, max over ranks.
+  e2e   : same metric through the public API (integrate_frame with a
+          ScanFrame over PINNED host float32 points): H2D of the scan, the
+          launch sequence and the D2H of the FrameStats counters are inside
+          the timed region (host wall clock per call).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun (N>1) every rank owns an x-slab of the grid; rank 0 holds the
+scans and broadcasts each step's points over NCCL inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+CONFIG = 2
+METRIC = "LiDAR points integrated/sec (device-timed)"
+UNIT = "points/s"
+K_EDGE = 21
+
+
+def b_alg(shadow_cells: float) -> float:
+    """algorithmic bytes per applied return = 4*K^3 + 4*|S|
+    (mask read for every cube cell + hits/sign read-write on shadow cells),
+    defined on the reference's 4-byte mask layout."""
+    return 4.0 * K_EDGE ** 3 + 4.0 * shadow_cells
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms (nvidia-smi's
+    own loop mode) during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self._t = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [v.strip() for v in line.strip().split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.3)  # first samples before the timed region starts
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self._t.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [x for x in (num(r[0]) for r in self.rows) if x is not None]
+        mx = [x for x in (num(r[1]) for r in self.rows) if x is not None]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def gen_scans(w, n):
+    return [w.scan(k) for k in range(n)]
+
+
+def cpu_baseline(w, scans, budget_s=12.0, threads=None):
+    """Oracle port (C preprocessing + C serial-order stamping, x-slab threads
+    over all host cores) on the first scans of the same trajectory until the
+    time budget is spent. Returns applied returns / s."""
+    import oracle
+
+    threads = threads or oracle.os_threads()
+    ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
+    g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+    applied = 0
+    t0 = time.perf_counter()
+    k = 0
+    while k < len(scans):
+        st = oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
+        applied += st.points_in - st.points_discarded
+        k += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": applied / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"config-2 scans 0..{k - 1} ({k} scans, {applied} applied returns) in {el:.1f} s, "
+                      f"oracle C port (libm transcendentals), {threads} threads (x-slab stamping)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port of the Python reference, which cannot travel to the GPU box)
+    on the same workload, all host threads, one scan per step."""
+    if rank != 0:
+        return
+    import oracle
+
+    w = workloads.get(CONFIG)
+    n = args.warmup + args.steps
+    scans = gen_scans(w, min(n, w.n_scans))
+    threads = oracle.os_threads()
+    ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
+    g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+    applied, el = 0, 0.0
+    for s in range(n):
+        k = s % w.n_scans
+        if k == 0 and s > 0:
+            g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+        t0 = time.perf_counter()
+        st = oracle.integrate_frame(g, ob, scans[k % len(scans)], w.poses[k], threads=threads, c_prep=True)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            applied += st.points_in - st.points_discarded
+            el += dt
+    value = applied / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": config_desc(w),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed scans of config 2 (full scans), oracle C port of the "
+                                   f"reference integrate_frame, {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(w):
+    return {"workload": f"config {CONFIG}: synthetic room, 100-scan trajectory, 64x1024 float32 returns/scan, "
+                        f"{w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]} "
+                        "(400x400x100 padded by 11)",
+            "kernel": f"{K_EDGE}^3", "bins": "40x40", "shadow_radius": w.shadow_radius, "t_occ": 2, "h_max": 255,
+            "step": "one scan integrated into the trajectory grid", "l2": "flushed between steps (256 MB write)",
+            "parallelism": "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+
+    from paper_2509_20081_b200 import _native
+    from paper_2509_20081_b200 import (IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame, new_grid)
+    from paper_2509_20081_b200.sharded import ShardedGrid
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workloads.get(CONFIG)
+    n_total = args.warmup + args.steps
+    scans = gen_scans(w, min(n_total, w.n_scans))
+    bank = build_kernel_bank(size=K_EDGE, shadow_radius=w.shadow_radius)
+    shadow_cells = float(np.mean([len(o) for o in bank.shadow_offsets]))
+    params = IntegrationParams()
+    L = _native.lib()
+
+    # ---------------- device-resident value --------------------------------
+    sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local)
+    dev_scans = [torch.from_numpy(s).to(f"cuda:{local}") for s in scans] if rank == 0 else None
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+    stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
+    torch.cuda.set_stream(stream)
+    L.dbt_profile_enable(sg.local.handle, 1)
+
+    def do_step(s):
+        k = s % w.n_scans
+        if rank == 0:
+            pts = dev_scans[k % len(dev_scans)]
+        else:
+            pts = torch.empty((len(scans[k % len(scans)]), 3), dtype=torch.float32, device=f"cuda:{local}")
+        if dist is not None:
+            dist.broadcast(pts, 0)
+        sg.integrate_device(bank, pts, [pts.shape[0]], w.poses[k][None], params, stream=stream)
+
+    for s in range(args.warmup):
+        if s % w.n_scans == 0:
+            L.dbt_grid_reset(sg.local.handle)
+        do_step(s)
+    torch.cuda.synchronize()
+    L.dbt_profile_reset(sg.local.handle)
+    applied = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.dbt_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            s = args.warmup + i
+            if s % w.n_scans == 0:
+                L.dbt_grid_reset(sg.local.handle)
+            flush.zero_()
+            ev[i][0].record(stream)
+            do_step(s)
+            ev[i][1].record(stream)
+            if (i + 1) % 16 == 0 or i == args.steps - 1:
+                torch.cuda.synchronize()
+            st = sg.stats()[0]
+            applied += st.points_in - st.points_discarded
+        torch.cuda.synchronize()
+    launches = L.dbt_launch_count() - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist is not None:
+        t = torch.tensor([dev_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+    value = applied / (dev_ms / 1e3)
+
+    # per-kernel device time (CUDA events on the launch stream, same region)
+    names = ctypes.create_string_buffer(32 * 16)
+    ms = (ctypes.c_double * 16)()
+    cnt = (ctypes.c_int64 * 16)()
+    nk = ctypes.c_int32()
+    L.dbt_profile_read(sg.local.handle, names, ms, cnt, 16, ctypes.byref(nk))
+    kernels = {}
+    for i in range(nk.value):
+        nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+        kernels[nm] = {"ms_total": ms[i], "launches": int(cnt[i]), "avg_us": ms[i] / max(cnt[i], 1) * 1e3}
+    L.dbt_profile_enable(sg.local.handle, 0)
+
+    sweep = kernels.get("sweep_kernel", {"avg_us": float("nan"), "launches": 0})
+    peak, peak_src = measured_peaks()
+    applied_per_launch = applied / max(args.steps, 1)
+    alg_bytes = b_alg(shadow_cells) * applied_per_launch / max(world, 1)
+    achieved = alg_bytes / (sweep["avg_us"] * 1e-6) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": config_desc(w),
+        "gpu_launches": int(launches),
+        "kernels": kernels,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "alg_bytes_def": f"4*21^3 + 4*|S| = {b_alg(shadow_cells):.0f} B per applied return "
+                                      "(SURVEY.md 8(d)) x applied returns per scan"},
+    }
+
+    # ---------------- e2e through the public API (rank 0, N=1) --------------
+    if world == 1:
+        g = new_grid(w.dims, w.voxel_size, w.origin, device=local)
+        pinned = []
+        for s in scans:
+            buf = ctypes.c_void_p()
+            _native.check(L.dbt_host_alloc(s.nbytes, ctypes.byref(buf)))
+            arr = np.ctypeslib.as_array((ctypes.c_float * s.size).from_address(buf.value)).reshape(s.shape)
+            arr[...] = s
+            pinned.append((buf, arr))
+        e_el, e_pts, h2d = 0.0, 0, 0
+        for s in range(args.warmup + args.steps):
+            k = s % w.n_scans
+            if k == 0:
+                L.dbt_grid_reset(g.handle)
+            arr = pinned[k % len(pinned)][1]
+            if s >= args.warmup:
+                flush.zero_()
+                torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st = integrate_frame(g, bank, ScanFrame(points=arr, pose=w.poses[k]), params)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                e_el += dt
+                e_pts += st.points_in - st.points_discarded
+                h2d += arr.nbytes
+        line["e2e"] = {"value": e_pts / e_el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                       "d2h_bytes_per_step": 64, "ms_per_step": e_el / args.steps * 1e3,
+                       "api": "paper_2509_20081_b200.integrate_frame (dbt_integrate_frame), pinned float32 scans"}
+        for buf, _ in pinned:
+            L.dbt_host_free(buf)
+        # L2 read bandwidth microbenchmark (context for the L2-resident grid)
+        x = torch.ones(16 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 64 MB, L2 resident
+        x.sum()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            x.sum()
+        e1.record()
+        torch.cuda.synchronize()
+        l2 = 50 * x.numel() * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        line["roofline"]["l2_read_gbs_torch_sum"] = l2
+        line["roofline"]["frac_of_l2_read"] = achieved / l2
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(w, scans)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

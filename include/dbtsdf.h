@@ -97,6 +97,10 @@ DBT_API int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], i
  * DBT_ERR_CORRUPTION: the device word stores the run length). */
 DBT_API int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits);
 DBT_API int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits);
+/* Same for the global x-planes [x_begin, x_end) (inside the slab): arrays of
+ * shape (x_end-x_begin, ny, nz). Streams huge grids in pieces. */
+DBT_API int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
+                                    uint8_t* hits);
 /* DBTSDF01 voxel records, F-order linear index ix + nx*(iy + ny*iz)
  * (grid.py:178-185): 8 bytes each {mask u32, sign u8, hits u8, 0 u16}.
  * Whole grid only (slab == full grid). */
@@ -139,13 +143,15 @@ DBT_API int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const doubl
                              const double* sensor, int64_t n, const dbt_params* p,
                              dbt_stats* out, int8_t* outcome);
 /* Device-resident variant for benchmarking and multi-GPU: `d_points` is a
- * device pointer on the grid's device, stream a cudaStream_t (NULL = the
- * grid's stream). Asynchronous: the stats land in device memory and are read
+ * device pointer on the grid's device, `stream` a cudaStream_t with the CUDA
+ * convention (NULL = legacy default stream; dbt_grid_stream gives the grid's
+ * own stream). Asynchronous: the stats land in device memory and are read
  * with dbt_stats_read after the stream is synchronised. */
 DBT_API int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, int dtype,
                          const int64_t* counts, int32_t n_scans, const double* poses,
                          const dbt_params* p, void* stream);
 DBT_API int dbt_stats_read(dbt_grid* g, dbt_stats* out, int32_t n_scans);
+DBT_API int dbt_grid_stream(dbt_grid* g, void** stream);
 DBT_API int dbt_synchronize(dbt_grid* g);
 
 /* ---- device binning (kernels.py:49-57), exposed for parity tests -------- */

@@ -56,6 +56,10 @@ def lib():
                                 _i64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 _i64p]
         L.orc_stamp.restype = ctypes.c_int64
+        L.orc_stamp_slab.argtypes = [_u32p, _u8p, _u8p, _i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _u32p,
+                                     _i32p, _i64p, _i64p, _u8p, _i64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, _i64p]
+        L.orc_stamp_slab.restype = ctypes.c_int64
         _LIB = L
     return _LIB
 
@@ -105,14 +109,18 @@ class OracleGrid:
     mask: np.ndarray = None
     sign: np.ndarray = None
     hits: np.ndarray = None
+    slab: tuple = None  # (x0, x1) owned x-range; arrays hold only that slab
 
     def __post_init__(self):
         self.dims = tuple(int(d) for d in self.dims)
         self.origin = np.asarray(self.origin, dtype=np.float64)
+        if self.slab is None:
+            self.slab = (0, self.dims[0])
+        shp = (self.slab[1] - self.slab[0], self.dims[1], self.dims[2])
         if self.mask is None:
-            self.mask = np.full(self.dims, prep.FULL_MASK, dtype=np.uint32)
-            self.sign = np.ones(self.dims, dtype=np.uint8)
-            self.hits = np.zeros(self.dims, dtype=np.uint8)
+            self.mask = np.full(shp, prep.FULL_MASK, dtype=np.uint32)
+            self.sign = np.ones(shp, dtype=np.uint8)
+            self.hits = np.zeros(shp, dtype=np.uint8)
 
 
 @dataclass
@@ -135,8 +143,8 @@ def stamp(grid: OracleGrid, bank: OracleBank, centers, ok, bins, h_max=255, t_oc
     applied = ctypes.c_int64(0)
     for a in (grid.mask, grid.sign, grid.hits):
         assert a.flags.c_contiguous
-    written = L.orc_stamp(_ptr(grid.mask, _u32p), _ptr(grid.sign, _u8p), _ptr(grid.hits, _u8p), _ptr(dims, _i64p),
-                          int(bank.size), _ptr(bank.distance_kernel, _u32p), _ptr(bank.shadow_xyz, _i32p),
+    written = L.orc_stamp_slab(_ptr(grid.mask, _u32p), _ptr(grid.sign, _u8p), _ptr(grid.hits, _u8p),
+                          _ptr(dims, _i64p), int(grid.slab[0]), int(grid.slab[1]), int(bank.size), _ptr(bank.distance_kernel, _u32p), _ptr(bank.shadow_xyz, _i32p),
                           _ptr(bank.shadow_start, _i64p), _ptr(centers, _i64p), _ptr(ok, _u8p), _ptr(bins, _i64p),
                           int(len(ok)), int(h_max), int(t_occ), int(bool(first_return)), int(threads),
                           ctypes.byref(applied))

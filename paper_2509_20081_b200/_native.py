@@ -63,6 +63,7 @@ SIGNATURES = {
     "dbt_grid_info": (ctypes.c_int, [_vp, _c_i64p, _c_i64p, _c_i64p]),
     "dbt_grid_upload": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "dbt_grid_download": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dbt_grid_download_range": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp]),
     "dbt_grid_to_records": (ctypes.c_int, [_vp, _vp]),
     "dbt_grid_from_records": (ctypes.c_int, [_vp, _vp]),
     "dbt_grid_gather": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
@@ -83,6 +84,7 @@ SIGNATURES = {
                                             ctypes.POINTER(Params), _vp]),
     "dbt_stats_read": (ctypes.c_int, [_vp, ctypes.POINTER(Stats), ctypes.c_int32]),
     "dbt_synchronize": (ctypes.c_int, [_vp]),
+    "dbt_grid_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "dbt_bin_index_array": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp,
                                            ctypes.c_int]),
     "dbt_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),

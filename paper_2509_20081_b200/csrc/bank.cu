@@ -4,9 +4,11 @@
 // shared K^3 distance kernel + one shadow offset list per azimuth-elevation
 // bin) and staged here once. Two device tables are derived:
 //  * the sweep table: for each of the 4 possible z-alignments of a centre,
-//    each of the K*K kernel rows and each 4-cell chunk of that row, the 4 run
-//    lengths packed into one u32 (63 marks a cell outside the kernel, which
-//    can never lower a stored run length <= 32);
+//    each DISTINCT kernel z-row (identical rows are shared; 66 of the 441
+//    rows of the standard 21^3 kernel are distinct) and each 4-cell chunk of
+//    that row, the 4 run lengths packed into one u32 (63 marks a cell outside
+//    the kernel, which can never lower a stored run length <= 32), plus the
+//    row -> distinct-row map;
 //  * the shadow table in CSR form, offsets as int8 (|o| <= R <= 15).
 #include <algorithm>
 #include <cstring>
@@ -42,18 +44,35 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
     len[i] = (uint8_t)pc;
     max_d = std::max(max_d, pc);
   }
-  std::vector<uint32_t> dtab((size_t)4 * rows * CH);
+  // distinct kernel rows (the standard kernel depends on (|dx|,|dy|) and is
+  // symmetric in dx<->dy: 66 distinct rows of 441)
+  std::vector<int> rowid(rows);
+  std::vector<int> distinct;  // representative row of each distinct id
+  for (int r = 0; r < rows; ++r) {
+    int id = -1;
+    for (size_t q = 0; q < distinct.size() && id < 0; ++q)
+      if (std::memcmp(&len[(size_t)distinct[q] * K], &len[(size_t)r * K], K) == 0) id = (int)q;
+    if (id < 0) {
+      id = (int)distinct.size();
+      distinct.push_back(r);
+    }
+    rowid[r] = id;
+  }
+  const int nd = (int)distinct.size();
+  std::vector<uint32_t> dtab((size_t)4 * nd * CH);
   for (int s = 0; s < 4; ++s)
-    for (int r = 0; r < rows; ++r)
+    for (int q = 0; q < nd; ++q)
       for (int c = 0; c < CH; ++c) {
         uint32_t v = 0;
         for (int i = 0; i < 4; ++i) {
           int zk = 4 * c + i - s;
-          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)r * K + zk] : 63u;
+          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)distinct[q] * K + zk] : 63u;
           v |= d << (8 * i);
         }
-        dtab[((size_t)s * rows + r) * CH + c] = v;
+        dtab[((size_t)s * nd + q) * CH + c] = v;
       }
+  std::vector<uint16_t> rowd(rows);
+  for (int r = 0; r < rows; ++r) rowd[r] = (uint16_t)(rowid[r] * CH);
   const int nb = b_az * b_el;
   std::vector<int32_t> start(nb + 1, 0);
   int max_s = 0;
@@ -82,10 +101,13 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
   b->total_shadow = total;
   b->chunks_per_row = CH;
   b->max_d = max_d;
+  b->n_distinct = nd;
   b->serial = ++g_bank_serial;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_len, K3);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_dtab, dtab.size() * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_rowd, rows * sizeof(uint16_t));
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_rowd, rowd.data(), rows * sizeof(uint16_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_xyz, sx.size());
   if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_start, (nb + 1) * 4);
   if (e == cudaSuccess) e = cudaMemcpy(b->d_len, len.data(), K3, cudaMemcpyHostToDevice);
@@ -107,6 +129,7 @@ int dbt_bank_destroy(dbt_bank* b) {
   cudaSetDevice(b->device);
   if (b->d_len) cudaFree(b->d_len);
   if (b->d_dtab) cudaFree(b->d_dtab);
+  if (b->d_rowd) cudaFree(b->d_rowd);
   if (b->d_shadow_xyz) cudaFree(b->d_shadow_xyz);
   if (b->d_shadow_start) cudaFree(b->d_shadow_start);
   delete b;

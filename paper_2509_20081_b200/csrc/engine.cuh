@@ -112,7 +112,9 @@ struct dbt_bank {
   int max_shadow = 0;
   int64_t total_shadow = 0;
   uint8_t* d_len = nullptr;          // K^3 run lengths of distance_kernel
-  uint32_t* d_dtab = nullptr;        // sweep table: [4 shifts][K*K rows][CH] packed d bytes
+  uint32_t* d_dtab = nullptr;        // sweep table: [4 shifts][distinct rows][CH] packed d bytes
+  uint16_t* d_rowd = nullptr;        // K*K: distinct-row id * CH
+  int n_distinct = 0;
   int chunks_per_row = 0;            // CH = ceil((K+3)/4)
   int max_d = 0;                     // largest kernel run length (fast path needs <= 18)
   int8_t* d_shadow_xyz = nullptr;    // total_shadow x 4 (dx,dy,dz,0)
@@ -164,8 +166,7 @@ struct dbt_grid {
 
   // --- per-bank derived table (depends on ny, nzp) ---
   uint64_t tab_bank = 0;
-  int64_t* d_rowoff = nullptr;   // K*K row offsets (dx*ny+dy)*nzp
-  int8_t* d_rowdx = nullptr;     // K*K dx
+  int32_t* d_rowoff = nullptr;   // K*K row offsets (dx*ny+dy)*nzp (fit int32, checked)
   int tab_K = 0;
 
   // --- measurement ---

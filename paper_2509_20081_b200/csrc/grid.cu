@@ -294,7 +294,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   for (auto e : g->event_pool) cudaEventDestroy(e);
   void* dev[] = {g->cells,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_poses,   g->d_scan_off,
-                 g->d_src_off, g->d_scnt, g->d_lcnt, g->d_stage, g->d_rowoff, g->d_rowdx};
+                 g->d_src_off, g->d_scnt, g->d_lcnt, g->d_stage, g->d_rowoff};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {g->h_scnt, g->h_lcnt, g->h_meta, g->h_poses};
@@ -352,10 +352,14 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
   return check_upload_error(g);
 }
 
-int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits) {
+int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
+                            uint8_t* hits) {
   int rc = check_grid(g);
   if (rc) return rc;
-  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  if (x_begin < g->x0 || x_end > g->x1 || x_begin > x_end)
+    return set_error(DBT_ERR_CONFIG, "download range outside the grid's slab");
+  const int64_t lx = x_end - x_begin, plane = g->ny * g->nz;
+  if (lx == 0) return DBT_OK;
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
@@ -365,8 +369,8 @@ int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits)
     uint32_t* dm = (uint32_t*)st;
     uint8_t* ds = st + 4 * n;
     uint8_t* dh = ds + n;
-    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, dm, ds, dh, n,
-                                                         g->nz, g->nzp);
+    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + (x_begin - g->x0 + x) * g->ny * g->nzp, dm, ds,
+                                                         dh, n, g->nz, g->nzp);
     DBT_CHECK_LAUNCH("decode_kernel");
     DBT_CUDA(cudaMemcpyAsync(mask + x * plane, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
     DBT_CUDA(cudaMemcpyAsync(sign + x * plane, ds, n, cudaMemcpyDeviceToHost, g->stream));
@@ -374,6 +378,11 @@ int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits)
     DBT_CUDA(cudaStreamSynchronize(g->stream));  // staging reused by the next slice
   }
   return DBT_OK;
+}
+
+int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  return dbt_grid_download_range(g, g->x0, g->x1, mask, sign, hits);
 }
 
 static int readout(dbt_grid* g, int mode, int32_t* pop, uint8_t* obs, double* sdf) {

@@ -279,9 +279,10 @@ struct SweepArgs {
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
   unsigned long long* changed_out;
-  const uint32_t* dtab;   // [4][rows][CH]
-  const int64_t* rowoff;  // [rows]
-  int K, R;
+  const uint32_t* dtab;   // [4][nd][CH]
+  const uint16_t* rowd;   // [rows] distinct id * CH
+  const int32_t* rowoff;  // [rows]
+  int K, R, nd;
   int64_t x0, x1, ny, nzp;
 };
 
@@ -295,19 +296,31 @@ __device__ __forceinline__ int lower_cas(uint32_t* p, uint32_t old, int d) {
   return 0;
 }
 
+constexpr int kSweepUnroll = 4;
+
 // Warp per unique centre. Row-major chunk order (row = (dx+R)*K + (dy+R),
 // 4-voxel chunks along z) so consecutive lanes read consecutive 16-byte
-// words of the same z-row: one 21-voxel row is six 128-bit loads.
+// words of the same z-row: one 21-voxel row is six 128-bit loads. Each lane
+// issues kSweepUnroll independent loads before testing any of them (the
+// atomics below could alias later loads, so the compiler would not hoist
+// them itself).
 // FAST (every kernel distance <= 18): "d lowers the cell" is bit d of the
-// word, the update a fire-and-forget atomicAnd. Otherwise CAS per cell.
+// word and the update a fire-and-forget RED.AND. Otherwise CAS per cell.
+// Reads may be stale (L1) — harmless: cells only ever lose bits, so a stale
+// word can only cause a redundant AND, never a missed one.
 template <int CH, bool FAST>
 __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int rows = a.K * a.K;
+  const int ntab = 4 * a.nd * CH;
   uint32_t* dtab = reinterpret_cast<uint32_t*>(smem_raw);
-  int64_t* rowoff = reinterpret_cast<int64_t*>(smem_raw + ((4 * rows * CH * 4 + 15) & ~15));
-  for (int i = threadIdx.x; i < 4 * rows * CH; i += blockDim.x) dtab[i] = a.dtab[i];
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) rowoff[i] = a.rowoff[i];
+  int32_t* rowoff = reinterpret_cast<int32_t*>(dtab + ntab);
+  uint16_t* rowd = reinterpret_cast<uint16_t*>(rowoff + rows);
+  for (int i = threadIdx.x; i < ntab; i += blockDim.x) dtab[i] = a.dtab[i];
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    rowoff[i] = a.rowoff[i];
+    rowd[i] = a.rowd[i];
+  }
   __syncthreads();
 
   const int64_t n_unique = (int64_t)a.lc_in->n_unique;
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     unpack_center(a.uniq[u], cx, cy, cz);
     const int64_t zs = cz - a.R;  // >= 0: boundary discard guarantees it
     const int sh = (int)(zs & 3);
-    const int64_t base = ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(3));
+    uint32_t* const base = a.cells + ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(3));
     // slab clip (multi-GPU): rows are dx-major, so the owned dx range is a
     // contiguous range of chunk indices
     const int64_t dxlo = max((int64_t)-a.R, a.x0 - cx);
@@ -331,33 +344,44 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     if (dxlo > dxhi) continue;
     const int jlo = (int)((dxlo + a.R) * a.K * CH);
     const int jhi = (int)((dxhi + a.R + 1) * a.K * CH);
-    const uint32_t* dt = dtab + sh * rows * CH;
-#pragma unroll 4
-    for (int j = jlo + lane; j < jhi; j += 32) {
-      const int row = j / CH;
-      const int ch = j - row * CH;
-      uint32_t* p = a.cells + base + rowoff[row] + 4 * ch;
-      const uint4 w = *reinterpret_cast<const uint4*>(p);
-      const uint32_t d4 = dt[j];
-      if (FAST) {
-        // bit d of the word is set <=> stored distance > d; d = 63 (outside
-        // the kernel) clamps to a zero probe
-        const uint32_t p0 = __funnelshift_lc(0u, 1u, d4 & 0xFF);
-        const uint32_t p1 = __funnelshift_lc(0u, 1u, (d4 >> 8) & 0xFF);
-        const uint32_t p2 = __funnelshift_lc(0u, 1u, (d4 >> 16) & 0xFF);
-        const uint32_t p3 = __funnelshift_lc(0u, 1u, d4 >> 24);
-        if ((w.x & p0) | (w.y & p1) | (w.z & p2) | (w.w & p3)) {
-          if (w.x & p0) changed += (atomicAnd(p + 0, kKeepSignHits | (p0 - 1u)) & p0) != 0;
-          if (w.y & p1) changed += (atomicAnd(p + 1, kKeepSignHits | (p1 - 1u)) & p1) != 0;
-          if (w.z & p2) changed += (atomicAnd(p + 2, kKeepSignHits | (p2 - 1u)) & p2) != 0;
-          if (w.w & p3) changed += (atomicAnd(p + 3, kKeepSignHits | (p3 - 1u)) & p3) != 0;
-        }
-      } else {
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const uint32_t* dt = dtab + sh * a.nd * CH;
+    for (int j0 = jlo + lane; j0 < jhi; j0 += 32 * kSweepUnroll) {
+      uint4 w[kSweepUnroll];
+      uint32_t* p[kSweepUnroll];
+      uint32_t d4[kSweepUnroll];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int d = (d4 >> (8 * b)) & 0xFF;
-          if (d <= 32 && d < cell_len(ws[b])) changed += lower_cas(p + b, ws[b], d);
+      for (int k = 0; k < kSweepUnroll; ++k) {
+        const int j = j0 + 32 * k;
+        const bool v = j < jhi;
+        const int jj = v ? j : jlo;
+        const int row = jj / CH;
+        const int ch = jj - row * CH;
+        p[k] = base + rowoff[row] + 4 * ch;
+        d4[k] = v ? dt[rowd[row] + ch] : 0x3F3F3F3Fu;
+        w[k] = *reinterpret_cast<const uint4*>(p[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kSweepUnroll; ++k) {
+        if (FAST) {
+          // bit d of the word is set <=> stored distance > d; d = 63 (outside
+          // the kernel) clamps to a zero probe
+          const uint32_t p0 = __funnelshift_lc(0u, 1u, d4[k] & 0xFF);
+          const uint32_t p1 = __funnelshift_lc(0u, 1u, (d4[k] >> 8) & 0xFF);
+          const uint32_t p2 = __funnelshift_lc(0u, 1u, (d4[k] >> 16) & 0xFF);
+          const uint32_t p3 = __funnelshift_lc(0u, 1u, d4[k] >> 24);
+          if ((w[k].x & p0) | (w[k].y & p1) | (w[k].z & p2) | (w[k].w & p3)) {
+            if (w[k].x & p0) { atomicAnd(p[k] + 0, kKeepSignHits | (p0 - 1u)); ++changed; }
+            if (w[k].y & p1) { atomicAnd(p[k] + 1, kKeepSignHits | (p1 - 1u)); ++changed; }
+            if (w[k].z & p2) { atomicAnd(p[k] + 2, kKeepSignHits | (p2 - 1u)); ++changed; }
+            if (w[k].w & p3) { atomicAnd(p[k] + 3, kKeepSignHits | (p3 - 1u)); ++changed; }
+          }
+        } else {
+          const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int d = (d4[k] >> (8 * b)) & 0xFF;
+            if (d <= 32 && d < cell_len(ws[b])) changed += lower_cas(p[k] + b, ws[b], d);
+          }
         }
       }
     }
@@ -386,8 +410,8 @@ SweepFn sweep_fn_t(int CH) {
 
 SweepFn sweep_fn(int CH, bool fast) { return fast ? sweep_fn_t<true>(CH) : sweep_fn_t<false>(CH); }
 
-size_t sweep_smem_bytes(int K, int CH) {
-  return ((size_t)(4 * K * K * CH * 4 + 15) & ~size_t(15)) + (size_t)K * K * 8;
+size_t sweep_smem_bytes(int K, int CH, int nd) {
+  return (size_t)4 * nd * CH * 4 + (size_t)K * K * (4 + 2);
 }
 
 __global__ void bin_kernel(const double* __restrict__ dirs, int64_t n, int b_az, int b_el,
@@ -454,15 +478,18 @@ int ensure_hash(dbt_grid* g, int64_t n) {
 int ensure_rows(dbt_grid* g, const dbt_bank* b) {
   if (g->tab_bank == b->serial && g->d_rowoff) return DBT_OK;
   const int K = b->K, R = b->R, rows = K * K;
-  std::vector<int64_t> ro(rows);
+  std::vector<int32_t> ro(rows);
   for (int r = 0; r < rows; ++r) {
     int dx = r / K - R, dy = r % K - R;
-    ro[r] = ((int64_t)dx * g->ny + dy) * g->nzp;
+    int64_t v = ((int64_t)dx * g->ny + dy) * g->nzp;
+    if (v > INT32_MAX || v < INT32_MIN)
+      return set_error(DBT_ERR_CONFIG, "grid too large in y*z for 32-bit kernel row offsets");
+    ro[r] = (int32_t)v;
   }
   if (g->d_rowoff) cudaFree(g->d_rowoff);
   g->d_rowoff = nullptr;
-  DBT_CUDA(cudaMalloc(&g->d_rowoff, rows * sizeof(int64_t)));
-  DBT_CUDA(cudaMemcpy(g->d_rowoff, ro.data(), rows * sizeof(int64_t), cudaMemcpyHostToDevice));
+  DBT_CUDA(cudaMalloc(&g->d_rowoff, rows * sizeof(int32_t)));
+  DBT_CUDA(cudaMemcpy(g->d_rowoff, ro.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice));
   g->tab_bank = b->serial;
   g->tab_K = K;
   return DBT_OK;
@@ -611,10 +638,13 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   const bool fast = b->max_d <= kMaxFastD;
   SweepFn fn = sweep_fn(CH, fast);
   if (!fn) return set_error(DBT_ERR_CONFIG, "unsupported kernel size for the sweep");
-  const size_t smem = sweep_smem_bytes(b->K, CH);
+  const size_t smem = sweep_smem_bytes(b->K, CH, b->n_distinct);
   const int shape_key = CH * 2 + (fast ? 1 : 0);
   if (g->sweep_ch != shape_key) {
     DBT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // keep shared memory to what 8 resident blocks need; the rest stays L1
+    int carve = (int)std::min<size_t>(100, (smem * 8 * 100 + 233471) / 233472 + 1);
+    DBT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int per_sm = 0, sms = 0;
     DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
     DBT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
@@ -627,7 +657,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   wa.lc_in = g->d_lcnt;
   wa.changed_out = &g->d_lcnt->changed;
   wa.dtab = b->d_dtab;
+  wa.rowd = b->d_rowd;
   wa.rowoff = g->d_rowoff;
+  wa.nd = b->n_distinct;
   wa.K = b->K;
   wa.R = b->R;
   wa.x0 = g->x0;
@@ -767,7 +799,7 @@ int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, i
   int rc = check(g, b);
   if (!rc) rc = validate_params(p);
   if (rc) return rc;
-  cudaStream_t st = stream ? (cudaStream_t)stream : g->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
   rc = launch_integrate(g, b, d_points, dtype, counts, n_scans, poses, p, nullptr, nullptr, st);
   if (rc) return rc;
   return fetch_counters(g, st);
@@ -781,6 +813,12 @@ int dbt_stats_read(dbt_grid* g, dbt_stats* out, int32_t n_scans) {
   dbt_params q{};
   q.first_return = g->last_first_return;
   fill_stats(g, &q, out, n_scans);
+  return DBT_OK;
+}
+
+int dbt_grid_stream(dbt_grid* g, void** stream) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  *stream = (void*)g->stream;
   return DBT_OK;
 }
 

@@ -118,6 +118,16 @@ class VoxelGrid:
         self.push_host()
         self._host = None
 
+    def download_range(self, x_begin: int, x_end: int):
+        """(mask, sign, hits) of global x-planes [x_begin, x_end) without
+        touching the host mirror (streams grids too large to download whole)."""
+        self.push_host()
+        shp = (x_end - x_begin, self.dims[1], self.dims[2])
+        out = (np.empty(shp, np.uint32), np.empty(shp, np.uint8), np.empty(shp, np.uint8))
+        _native.check(_native.lib().dbt_grid_download_range(self.handle, int(x_begin), int(x_end),
+                                                            *(_native.ptr(a) for a in out)))
+        return out
+
     def synchronize(self):
         _native.check(_native.lib().dbt_synchronize(self.handle))
 

@@ -1,0 +1,128 @@
+"""Multi-GPU slab sharding of the voxel grid.
+
+One process per GPU (torchrun). Rank r owns the contiguous x-slab
+[x0_r, x1_r) of the global grid and allocates only that slab. Every voxel
+update (mask AND, saturating hit count, occupied sign) is local to its voxel
+and commutative, so a return's K^3 stamp splits exactly across slabs: there is
+no halo exchange and no reduction of grid data. The only collective on the
+data path is the broadcast of each launch's raw points (float32 xyz, 12 B per
+return) from the rank that read them, over NCCL / NVLink; every rank then runs
+the identical deterministic preprocessing against the GLOBAL grid dims
+(discards, bins, first-return) and stamps only the part of each cube inside
+its slab (csrc/integrate.cu clips the dx range per centre). FrameStats:
+points_in / points_discarded are identical on every rank; the changed-cell
+counts are summed with one all-reduce.
+
+The functions below take a ``torch.distributed`` process group and work with
+any backend (NCCL on the GPU box, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .grid import VoxelGrid
+from .integrator import FrameStats, IntegrationParams
+from .kernels import KernelBank
+
+DTYPE_CODES = {"float32": _native.DBT_F32, "float64": _native.DBT_F64}
+
+
+def slab_bounds(nx: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, disjoint x-slabs covering [0, nx); sizes differ by <= 1."""
+    if not 0 <= rank < world:
+        raise ValueError("rank outside [0, world)")
+    return nx * rank // world, nx * (rank + 1) // world
+
+
+def owner_of(x: int, nx: int, world: int) -> int:
+    """Rank whose slab holds global plane x."""
+    for r in range(world):
+        a, b = slab_bounds(nx, world, r)
+        if a <= x < b:
+            return r
+    raise ValueError("x outside the grid")
+
+
+def broadcast_batch(points, counts, poses, dist, group=None, src: int = 0, device=None):
+    """Broadcast one launch's scans from ``src``.
+
+    points: torch tensor (n, 3) float32/float64 on ``src`` (ignored elsewhere);
+    counts: int64 per-scan point counts, poses: (S, 4, 4) float64 — numpy on
+    ``src``. Returns (points tensor on ``device``, counts ndarray, poses ndarray)
+    on every rank. Metadata travels as one small int64/float64 tensor pair;
+    the point payload is one broadcast of the raw buffer.
+    """
+    import torch
+
+    rank = dist.get_rank(group)
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    if rank == src:
+        hdr = torch.tensor([int(points.shape[0]), 0 if points.dtype == torch.float32 else 1, len(counts)],
+                           dtype=torch.int64, device=dev)
+    else:
+        hdr = torch.zeros(3, dtype=torch.int64, device=dev)
+    dist.broadcast(hdr, src, group=group)
+    n, code, S = (int(v) for v in hdr.tolist())
+    if rank == src:
+        meta_i = torch.as_tensor(np.asarray(counts, dtype=np.int64), device=dev)
+        meta_f = torch.as_tensor(np.asarray(poses, dtype=np.float64).reshape(S, 16), device=dev)
+        payload = points.to(dev).contiguous()
+    else:
+        meta_i = torch.zeros(S, dtype=torch.int64, device=dev)
+        meta_f = torch.zeros((S, 16), dtype=torch.float64, device=dev)
+        payload = torch.empty((n, 3), dtype=torch.float32 if code == 0 else torch.float64, device=dev)
+    dist.broadcast(meta_i, src, group=group)
+    dist.broadcast(meta_f, src, group=group)
+    dist.broadcast(payload, src, group=group)
+    return payload, meta_i.cpu().numpy(), meta_f.cpu().numpy().reshape(S, 4, 4)
+
+
+def reduce_stats(stats: list, dist, group=None, device=None) -> list:
+    """Sum the per-rank changed-cell counts (the only rank-dependent field)."""
+    import torch
+
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    t = torch.tensor([s.voxels_written for s in stats], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, group=group)
+    out = []
+    for s, w in zip(stats, t.cpu().tolist()):
+        out.append(FrameStats(s.points_in, s.points_discarded, int(w), s.elapsed_ms, s.points_applied,
+                              s.unique_centers, s.knife_edges, s.device_ms))
+    return out
+
+
+class ShardedGrid:
+    """This rank's slab of a globally-sized grid, device resident."""
+
+    def __init__(self, dims, voxel_size, origin, rank: int, world: int, device: int | None = None):
+        self.dims = tuple(int(d) for d in dims)
+        self.rank, self.world = rank, world
+        self.slab = slab_bounds(self.dims[0], world, rank)
+        self.local = VoxelGrid(self.dims, voxel_size, origin, device=device, slab=self.slab)
+
+    def integrate_device(self, bank: KernelBank, points, counts, poses, params: IntegrationParams, stream=None):
+        """Stamp this rank's slab from device-resident points (torch CUDA
+        tensor). Asynchronous on ``stream`` (a torch.cuda.Stream or None for
+        the current torch stream); read stats with ``stats``."""
+        import torch
+
+        dtype = _native.DBT_F32 if points.dtype == torch.float32 else _native.DBT_F64
+        counts = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+        poses = np.ascontiguousarray(np.asarray(poses, dtype=np.float64).reshape(-1))
+        st = torch.cuda.current_stream() if stream is None else stream
+        prm = params.native()
+        self._last_scans = len(counts)
+        _native.check(_native.lib().dbt_integrate_device(
+            self.local.handle, bank.device_handle(self.local.device), ctypes.c_void_p(points.data_ptr()), dtype,
+            counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
+            poses.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(prm),
+            ctypes.c_void_p(st.cuda_stream)))
+
+    def stats(self) -> list:
+        out = (_native.Stats * self._last_scans)()
+        _native.check(_native.lib().dbt_stats_read(self.local.handle, out, self._last_scans))
+        return [FrameStats.from_native(out[i]) for i in range(self._last_scans)]

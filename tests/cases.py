@@ -1,0 +1,203 @@
+"""Parity cases shared by tests/golden/make_golden.py (which runs the
+reference on them) and the oracle / GPU parity tests (which must reproduce
+the stored hashes). Inputs are regenerated from seeds; their hashes are stored
+with the golden outputs so generator drift on another host is reported as
+such, not as a kernel mismatch.
+
+Each case: grid (dims, voxel_size, origin), optional non-fresh initial
+state, bank parameters, integration params and a list of frames
+(sensor-frame points + pose) or of integrate_point hits (map-frame point +
+sensor position).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import os
+import sys
+from dataclasses import dataclass, field
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import workloads  # noqa: E402
+
+FULL = 0xFFFFFFFF
+
+
+def sha(a) -> str:
+    a = np.ascontiguousarray(a)
+    h = hashlib.sha256()
+    h.update(str(a.dtype).encode())
+    h.update(str(a.shape).encode())
+    h.update(a.tobytes())
+    return h.hexdigest()[:32]
+
+
+def yaw_pose(yaw, t):
+    T = np.eye(4)
+    c, s = math.cos(yaw), math.sin(yaw)
+    T[:3, :3] = [[c, -s, 0], [s, c, 0], [0, 0, 1]]
+    T[:3, 3] = t
+    return T
+
+
+@dataclass
+class Case:
+    name: str
+    dims: tuple
+    voxel_size: float
+    origin: tuple
+    bank: dict
+    params: dict = field(default_factory=dict)
+    frames: list = field(default_factory=list)   # [(points, pose)]
+    hits: tuple | None = None                    # (p_map (n,3), sensor (n,3)) for integrate_point
+    init: tuple | None = None                    # (mask, sign, hits) non-fresh start
+    slow: bool = False                           # large grid: skip in quick runs
+
+    def input_hash(self) -> str:
+        h = hashlib.sha256()
+        for p, pose in self.frames:
+            h.update(np.ascontiguousarray(p).tobytes())
+            h.update(np.ascontiguousarray(pose).tobytes())
+        if self.hits is not None:
+            h.update(np.ascontiguousarray(self.hits[0]).tobytes())
+            h.update(np.ascontiguousarray(self.hits[1]).tobytes())
+        if self.init is not None:
+            for a in self.init:
+                h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()[:32]
+
+
+def _random_state(rng, dims, h_hi=256):
+    k = rng.integers(0, 33, size=dims)
+    mask = np.where(k > 0, (FULL >> (32 - np.maximum(k, 1))).astype(np.uint64), 0).astype(np.uint32)
+    hits = rng.integers(0, h_hi, size=dims).astype(np.uint8)
+    sign = rng.integers(0, 2, size=dims).astype(np.uint8)
+    return mask, sign, hits
+
+
+def _random_hits(rng, n, dims, vs, margin=11):
+    lo = margin * vs
+    his = [(d - margin) * vs for d in dims]
+    pts = rng.uniform([lo] * 3, his, size=(n, 3))
+    dirs = rng.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    return pts, pts - dirs
+
+
+def small_cases() -> list:
+    cases = []
+    eye = np.eye(4)
+    b3 = dict(size=21, shadow_radius=3)
+    # test_integrator-style random frames (uniform in [1.2, 2.9]^3, 41^3 grid)
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(1.2, 2.9, size=(500, 3))
+    cases.append(Case("frame500_default", (41, 41, 41), 0.1, (0, 0, 0), b3, {}, [(pts, eye)]))
+    cases.append(Case("frame500_first_return", (41, 41, 41), 0.1, (0, 0, 0), b3,
+                      {"first_return_per_voxel": True}, [(pts, eye)]))
+    cases.append(Case("frame500_downsample3", (41, 41, 41), 0.1, (0, 0, 0), b3, {"downsample": 3}, [(pts, eye)]))
+    # rotated + translated poses over several frames (FMA-chain transform)
+    rng = np.random.default_rng(21)
+    frames = []
+    for k in range(4):
+        p = rng.uniform(-1.2, 1.2, size=(400, 3)).astype(np.float32)
+        frames.append((p, yaw_pose(rng.uniform(0, 2 * np.pi), (3.2, 3.1, 3.0))))
+    cases.append(Case("yaw_frames_f32", (64, 64, 64), 0.1, (0, 0, 0), dict(size=21, shadow_radius=2), {"t_occ": 1},
+                      frames))
+    # non-fresh start: random run masks, hits 0..255 (incl. > h_max), random signs
+    for model, hm, t in (("hemisphere", 7, 3), ("cone", 200, 2), ("hemisphere", 255, 1)):
+        rng = np.random.default_rng(31 + hm)
+        dims = (48, 48, 48)
+        init = _random_state(rng, dims)
+        frames = [(rng.uniform(1.15, 3.6, size=(300, 3)), yaw_pose(0.3 * k, (0.05 * k, 0.02, -0.01))) for k in range(3)]
+        cases.append(Case(f"nonfresh_{model}_h{hm}_t{t}", dims, 0.1, (0, 0, 0),
+                          dict(size=21, shadow_radius=3 if model == "cone" else 2, shadow_model=model,
+                               cone_half_angle_deg=40.0), {"h_max": hm, "t_occ": t}, frames, init=init))
+    # other kernel sizes
+    rng = np.random.default_rng(41)
+    p = rng.uniform(0.45, 2.75, size=(300, 3))
+    cases.append(Case("k9_bins8", (32, 32, 32), 0.1, (0, 0, 0), dict(size=9, b_az=8, b_el=8, shadow_radius=2), {},
+                      [(p, eye)]))
+    p = rng.uniform(1.2, 5.2, size=(300, 3))
+    cases.append(Case("k23_wide", (64, 64, 64), 0.1, (0, 0, 0), dict(size=23, shadow_radius=4), {"t_occ": 1},
+                      [(p, eye)]))
+    # reference acceptance C1 shape: integrate_point hits, random directions
+    rng = np.random.default_rng(42)
+    pm, sens = _random_hits(rng, 10_000, (64, 64, 64), 0.1)
+    cases.append(Case("c1_points10k", (64, 64, 64), 0.1, (0, 0, 0), b3, {"t_occ": 2}, hits=(pm, sens)))
+    # boundary + degenerate + NaN/inf returns mixed in
+    rng = np.random.default_rng(51)
+    p = rng.uniform(-0.5, 4.6, size=(400, 3))
+    p[:5] = [[0.0, 0.0, 0.001], [np.nan, 1, 1], [np.inf, 1, 1], [1e30, 0, 0], [0.05, 0.0, 0.0]]
+    cases.append(Case("edge_returns", (41, 41, 41), 0.1, (0, 0, 0), b3, {}, [(p, yaw_pose(0.0, (2.0, 2.0, 2.0)))]))
+    cases.append(Case("empty_scan", (41, 41, 41), 0.1, (0, 0, 0), b3, {}, [(np.zeros((0, 3)), eye)]))
+    return cases
+
+
+def config_cases(include_slow=True) -> list:
+    cases = []
+    w = workloads.get(1)
+    cases.append(Case("cfg1_scan0", w.dims, w.voxel_size, w.origin, dict(size=21, shadow_radius=w.shadow_radius), {},
+                      [(w.scan(0), w.poses[0])]))
+    w = workloads.get(2)
+    cases.append(Case("cfg2_scans0-2", w.dims, w.voxel_size, w.origin, dict(size=21, shadow_radius=w.shadow_radius),
+                      {}, [(w.scan(k), w.poses[k]) for k in range(3)]))
+    cases.append(Case("cfg2_scan0_rs3", w.dims, w.voxel_size, w.origin, dict(size=21, shadow_radius=3), {},
+                      [(w.scan(0), w.poses[0])]))
+    if include_slow:
+        w = workloads.get(3)
+        cases.append(Case("cfg3_scans0-1", w.dims, w.voxel_size, w.origin, dict(size=21, shadow_radius=w.shadow_radius),
+                          {}, [(w.scan(k), w.poses[k]) for k in range(2)], slow=True))
+        # config-4 scene/sensor at 0.02 m on a 1000x1000x400 window (the full
+        # 6.4e9-voxel grid needs 38 GB of reference host arrays)
+        w4 = workloads.get(4)
+        cases.append(Case("cfg4_window_scan0", (1000, 1000, 400), w4.voxel_size, (0.0, 90.0, -0.22),
+                          dict(size=21, shadow_radius=w4.shadow_radius), {}, [(w4.scan(0), w4.poses[0])], slow=True))
+    return cases
+
+
+def bank_specs() -> list:
+    return [
+        dict(size=21, shadow_radius=1),
+        dict(size=21, shadow_radius=2),
+        dict(size=21, shadow_radius=3),
+        dict(size=21, shadow_radius=3, shadow_model="cone", cone_half_angle_deg=30.0),
+        dict(size=21, shadow_radius=2, shadow_model="cone", cone_half_angle_deg=40.0),
+        dict(size=9, b_az=8, b_el=8, shadow_radius=2),
+        dict(size=3, b_az=1, b_el=1, shadow_radius=1),
+        dict(size=23, shadow_radius=4),
+    ]
+
+
+def bank_key(spec: dict) -> str:
+    return ",".join(f"{k}={spec[k]}" for k in sorted(spec))
+
+
+def bank_hashes(bank) -> dict:
+    offs = [np.asarray(o, dtype=np.int64).reshape(-1, 3) for o in bank.shadow_offsets]
+    counts = np.array([len(o) for o in offs], dtype=np.int64)
+    return {
+        "distance_kernel": sha(np.asarray(bank.distance_kernel, dtype=np.uint32)),
+        "shadow_counts": sha(counts),
+        "shadow_offsets": sha(np.concatenate(offs)),
+        "bin_dirs": sha(np.asarray(bank.bin_dirs, dtype=np.float64)),
+    }
+
+
+def bin_dir_sets() -> dict:
+    """Direction sets whose (b_a, b_e) from the reference bin_index_array are
+    stored: random normals (test_kernels.py:32-37 shape) and bin centres."""
+    rng = np.random.default_rng(3)
+    out = {"normal200": rng.normal(size=(200, 3)), "normal100k": rng.normal(size=(100_000, 3))}
+    centres = []
+    for ba in range(40):
+        for be in range(40):
+            a = (ba + 0.5) * 2 * math.pi / 40
+            e = (be + 0.5) * math.pi / 40 - math.pi / 2
+            centres.append([math.cos(e) * math.cos(a), math.cos(e) * math.sin(a), math.sin(e)])
+    out["bin_centres"] = np.array(centres)
+    out["axes"] = np.array([[1, 0, 0], [0, 0, 1], [0, -1, 0], [-1, 0, 0], [0, 1, 0], [0, 0, -1], [1, 1, 0],
+                            [-1, -1, 0], [1, -1, 0], [3, 4, 0], [1, 1, 1]], dtype=np.float64)
+    return out

@@ -1,0 +1,95 @@
+"""Generate tests/golden/golden.json by running the REFERENCE implementation.
+
+Runs only in the build container, where the reference is importable from
+/root/reference/pkg/src (it does not exist on the GPU box). For every case in
+tests/cases.py it integrates the seeded inputs with the reference's own
+``integrate_frame`` / ``integrate_point`` and stores sha256 prefixes of the
+final mask/sign/hits arrays plus the FrameStats, the input hashes, the kernel
+bank table hashes (``build_kernel_bank``) and the reference's
+``bin_index_array`` output on fixed direction sets.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--fast]
+"""
+
+from __future__ import annotations
+
+import json
+import platform
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import cases  # noqa: E402
+from bitsdf.grid import new_grid  # noqa: E402  (reference)
+from bitsdf.integrator import IntegrationParams, ScanFrame, integrate_frame, integrate_point  # noqa: E402
+from bitsdf.kernels import bin_index_array, build_kernel_bank  # noqa: E402
+
+
+def run_case(c: cases.Case) -> dict:
+    bank = build_kernel_bank(**c.bank)
+    g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 40)
+    if c.init is not None:
+        g.mask[...] = c.init[0]
+        g.sign[...] = c.init[1]
+        g.hits[...] = c.init[2]
+    params = IntegrationParams(**c.params)
+    stats = []
+    t0 = time.perf_counter()
+    for pts, pose in c.frames:
+        st = integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), params, threads=8)
+        stats.append([st.points_in, st.points_discarded, st.voxels_written])
+    applied = None
+    if c.hits is not None:
+        applied = 0
+        for p, s in zip(*c.hits):
+            applied += integrate_point(g, bank, p, s, params) == "applied"
+    el = time.perf_counter() - t0
+    out = {
+        "input": c.input_hash(),
+        "mask": cases.sha(g.mask),
+        "sign": cases.sha(g.sign),
+        "hits": cases.sha(g.hits),
+        "stats": stats,
+        "applied": applied,
+        "observed": int(np.count_nonzero(~((g.mask == 0xFFFFFFFF) & (g.hits == 0)))),
+        "occupied": int(np.count_nonzero(g.sign == 0)),
+        "ref_seconds": round(el, 2),
+    }
+    print(f"{c.name}: {el:.1f}s stats={stats} applied={applied}", flush=True)
+    return out
+
+
+def main():
+    fast = "--fast" in sys.argv
+    out_path = HERE / "golden.json"
+    gold = json.loads(out_path.read_text()) if out_path.exists() else {}
+    gold["_meta"] = {
+        "generator": "tests/golden/make_golden.py (reference bitsdf imported from /root/reference/pkg/src)",
+        "numpy": np.__version__,
+        "python": platform.python_version(),
+        "machine": platform.processor() or platform.machine(),
+    }
+    gold.setdefault("banks", {})
+    for spec in cases.bank_specs():
+        gold["banks"][cases.bank_key(spec)] = cases.bank_hashes(build_kernel_bank(**spec))
+    gold.setdefault("bins", {})
+    for name, dirs in cases.bin_dir_sets().items():
+        b_a, b_e = bin_index_array(dirs, 40, 40)
+        gold["bins"][name] = {"input": cases.sha(dirs), "b_a": cases.sha(b_a.astype(np.int64)),
+                              "b_e": cases.sha(b_e.astype(np.int64))}
+    gold.setdefault("cases", {})
+    all_cases = cases.small_cases() + cases.config_cases(include_slow=not fast)
+    for c in all_cases:
+        gold["cases"][c.name] = run_case(c)
+        out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))
+    print("wrote", out_path)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,101 @@
+"""Multi-rank slab sharding on CPU: world_size 2 over gloo.
+
+Exercises the same host logic the NCCL path uses (paper_2509_20081_b200/
+sharded.py): slab partition, the broadcast protocol (header, per-scan
+counts/poses, raw float32 payload), per-rank preprocessing against the global
+dims, slab-restricted stamping (here the oracle's slab stamping stands in for
+the device engine, which the GPU tests cover per slab) and the stats
+all-reduce. The gathered slabs must reproduce the reference's golden grid and
+FrameStats for config 1 and the 3-scan config-2 case.
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+import cases
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case_name, out_path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import cases as C
+    import oracle
+    from paper_2509_20081_b200 import sharded
+    from paper_2509_20081_b200.integrator import FrameStats
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = next(x for x in C.config_cases(include_slow=False) if x.name == case_name)
+    x0, x1 = sharded.slab_bounds(c.dims[0], world, rank)
+    g = oracle.OracleGrid(c.dims, c.voxel_size, c.origin, slab=(x0, x1))
+    ob = oracle.OracleBank.build(**c.bank)
+    stats_all = []
+    for pts, pose in c.frames:
+        if rank == 0:
+            payload, counts, poses = torch.from_numpy(pts), np.array([len(pts)]), pose[None]
+        else:
+            payload, counts, poses = None, None, None
+        pts_r, counts_r, poses_r = sharded.broadcast_batch(payload, counts, poses, dist)
+        assert pts_r.dtype == torch.float32 and int(counts_r[0]) == len(pts)
+        st = oracle.integrate_frame(g, ob, pts_r.numpy(), poses_r[0], threads=2)
+        local = FrameStats(st.points_in, st.points_discarded, st.voxels_written)
+        stats_all.append(sharded.reduce_stats([local], dist)[0])
+    parts = [None] * world
+    dist.all_gather_object(parts, (x0, x1, g.mask, g.sign, g.hits))
+    if rank == 0:
+        parts.sort(key=lambda t: t[0])
+        assert parts[0][0] == 0 and parts[-1][1] == c.dims[0]
+        assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+        mask = np.concatenate([p[2] for p in parts])
+        sign = np.concatenate([p[3] for p in parts])
+        hits = np.concatenate([p[4] for p in parts])
+        np.savez(out_path, mask_sha=C.sha(mask), sign_sha=C.sha(sign), hits_sha=C.sha(hits),
+                 stats=np.array([[s.points_in, s.points_discarded, s.voxels_written] for s in stats_all]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case_name", ["cfg1_scan0", "cfg2_scans0-2"])
+def test_two_rank_slab_sharding_reproduces_reference(case_name, golden, tmp_path):
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "r0.npz"
+    mp.spawn(_worker, args=(2, _free_port(), case_name, str(out)), nprocs=2, join=True)
+    r = np.load(out)
+    ref = golden["cases"][case_name]
+    assert str(r["mask_sha"]) == ref["mask"]
+    assert str(r["sign_sha"]) == ref["sign"]
+    assert str(r["hits_sha"]) == ref["hits"]
+    assert r["stats"].tolist() == ref["stats"]
+
+
+def test_slab_bounds_partition():
+    from paper_2509_20081_b200.sharded import owner_of, slab_bounds
+
+    for nx in (1, 7, 222, 4000):
+        for world in (1, 2, 3, 8):
+            if world > nx:
+                continue
+            b = [slab_bounds(nx, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == nx
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            assert max(x1 - x0 for x0, x1 in b) - min(x1 - x0 for x0, x1 in b) <= 1
+            assert owner_of(nx - 1, nx, world) == world - 1
