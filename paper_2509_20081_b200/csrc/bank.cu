@@ -3,11 +3,11 @@
 // The bank is built on the host exactly as the reference builds it (one
 // shared K^3 distance kernel + one shadow offset list per azimuth-elevation
 // bin) and staged here once. Two device tables are derived:
-//  * the sweep table: for each of the 4 possible z-alignments of a centre,
+//  * the sweep table: for each of the 8 possible z-alignments of a centre,
 //    each DISTINCT kernel z-row (identical rows are shared; 66 of the 441
-//    rows of the standard 21^3 kernel are distinct) and each 4-cell chunk of
-//    that row, the 4 run lengths packed into one u32 (63 marks a cell outside
-//    the kernel, which can never lower a stored run length <= 32), plus the
+//    rows of the standard 21^3 kernel are distinct) and each 8-voxel chunk of
+//    that row, the 8 run lengths packed into a uint2 (0xFF marks a voxel
+//    outside the kernel, which can never lower a distance <= 32), plus the
 //    row -> distinct-row map;
 //  * the shadow table in CSR form, offsets as int8 (|o| <= R <= 15).
 #include <algorithm>
@@ -32,7 +32,7 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
   if (b_az < 1 || b_el < 1) return set_error(DBT_ERR_CONFIG, "bin counts must be at least 1");
   if ((int64_t)b_az * b_el > 65535) return set_error(DBT_ERR_CONFIG, "more than 65535 direction bins");
   const int K = size, R = size / 2, K3 = K * K * K, rows = K * K;
-  const int CH = (K + 3 + 3) / 4;
+  const int CH = (K + 7 + 7) / 8;
   std::vector<uint8_t> len(K3);
   int max_d = 0;
   for (int i = 0; i < K3; ++i) {
@@ -59,17 +59,17 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
     rowid[r] = id;
   }
   const int nd = (int)distinct.size();
-  std::vector<uint32_t> dtab((size_t)4 * nd * CH);
-  for (int s = 0; s < 4; ++s)
+  std::vector<uint2> dtab((size_t)8 * nd * CH);
+  for (int s = 0; s < 8; ++s)
     for (int q = 0; q < nd; ++q)
       for (int c = 0; c < CH; ++c) {
-        uint32_t v = 0;
-        for (int i = 0; i < 4; ++i) {
-          int zk = 4 * c + i - s;
-          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)distinct[q] * K + zk] : 63u;
-          v |= d << (8 * i);
+        uint32_t v[2] = {0, 0};
+        for (int i = 0; i < 8; ++i) {
+          int zk = 8 * c + i - s;
+          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)distinct[q] * K + zk] : 0xFFu;
+          v[i >> 2] |= d << (8 * (i & 3));
         }
-        dtab[((size_t)s * nd + q) * CH + c] = v;
+        dtab[((size_t)s * nd + q) * CH + c] = make_uint2(v[0], v[1]);
       }
   std::vector<uint16_t> rowd(rows);
   for (int r = 0; r < rows; ++r) rowd[r] = (uint16_t)(rowid[r] * CH);
@@ -105,13 +105,13 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
   b->serial = ++g_bank_serial;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_len, K3);
-  if (e == cudaSuccess) e = cudaMalloc(&b->d_dtab, dtab.size() * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_dtab, dtab.size() * sizeof(uint2));
   if (e == cudaSuccess) e = cudaMalloc(&b->d_rowd, rows * sizeof(uint16_t));
   if (e == cudaSuccess) e = cudaMemcpy(b->d_rowd, rowd.data(), rows * sizeof(uint16_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_xyz, sx.size());
   if (e == cudaSuccess) e = cudaMalloc(&b->d_shadow_start, (nb + 1) * 4);
   if (e == cudaSuccess) e = cudaMemcpy(b->d_len, len.data(), K3, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(b->d_dtab, dtab.data(), dtab.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(b->d_dtab, dtab.data(), dtab.size() * sizeof(uint2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(b->d_shadow_xyz, sx.data(), sx.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(b->d_shadow_start, start.data(), (nb + 1) * 4, cudaMemcpyHostToDevice);

@@ -23,9 +23,16 @@
 // word is lossless for every grid the reference can produce (runs; sign 0/1)
 // at half the record size.
 //
+// Distance cache: one byte per voxel, dist[v] >= run length of cells[v] at
+// all times (equal after upload/reset). The sweep reads it (8 voxels per
+// 64-bit load) to find the voxels a return lowers, then applies RED.AND to
+// the word and stores the new distance into the cache. Cache stores race
+// only with other lowering stores, so a cache byte can end up stale-high
+// (a later redundant AND) but never below the word: no update is ever lost.
+//
 // Layout in HBM: C-order (x, y, z) like the reference arrays, x restricted to
-// the owned slab [x0, x1), z stride padded to a multiple of 4 words so every
-// z-row starts 16-byte aligned and a 4-voxel chunk is one 128-bit load.
+// the owned slab [x0, x1), z stride padded to a multiple of 8 voxels so every
+// z-row of the cache starts 8-byte aligned (and of the words 32-byte aligned).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -112,10 +119,10 @@ struct dbt_bank {
   int max_shadow = 0;
   int64_t total_shadow = 0;
   uint8_t* d_len = nullptr;          // K^3 run lengths of distance_kernel
-  uint32_t* d_dtab = nullptr;        // sweep table: [4 shifts][distinct rows][CH] packed d bytes
+  uint2* d_dtab = nullptr;           // sweep table: [8 shifts][distinct rows][CH] 8 packed d bytes
   uint16_t* d_rowd = nullptr;        // K*K: distinct-row id * CH
   int n_distinct = 0;
-  int chunks_per_row = 0;            // CH = ceil((K+3)/4)
+  int chunks_per_row = 0;            // CH = ceil((K+7)/8) 8-voxel chunks per kernel row
   int max_d = 0;                     // largest kernel run length (fast path needs <= 18)
   int8_t* d_shadow_xyz = nullptr;    // total_shadow x 4 (dx,dy,dz,0)
   int32_t* d_shadow_start = nullptr; // n_bins + 1
@@ -127,7 +134,8 @@ struct dbt_grid {
   int64_t nx = 0, ny = 0, nz = 0, nzp = 0;  // global dims, padded z stride
   int64_t x0 = 0, x1 = 0;                   // owned slab
   double vs = 0, org[3] = {0, 0, 0};
-  uint32_t* cells = nullptr;
+  uint32_t* cells = nullptr;                // authoritative voxel words
+  uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   int64_t n_cells = 0;                      // (x1-x0)*ny*nzp
   cudaStream_t stream = nullptr;
   bool own_stream = true;

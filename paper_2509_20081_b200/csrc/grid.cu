@@ -61,6 +61,13 @@ __global__ void encode_kernel(uint32_t* __restrict__ cells, const uint32_t* __re
 }
 
 
+// dist[v] = run length of cells[v] over the whole slab (after host writes)
+__global__ void rebuild_dist_kernel(const uint32_t* __restrict__ cells, uint8_t* __restrict__ dist, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dist[i] = (uint8_t)cell_len(cells[i]);
+}
+
 __global__ void decode_kernel(const uint32_t* __restrict__ cells, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits, int64_t n,
                               int64_t nz, int64_t nzp) {
@@ -208,6 +215,7 @@ int check_upload_error(dbt_grid* g) {
     // leave the grid fresh rather than half-written
     fill_cells_kernel<<<grid_blocks(g->n_cells / 4), 256, 0, g->stream>>>(g->cells, g->n_cells);
     DBT_CHECK_LAUNCH("fill_cells_kernel");
+    DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)g->n_cells, g->stream));
     DBT_CUDA(cudaStreamSynchronize(g->stream));
     if (err & 1)
       return set_error(DBT_ERR_CORRUPTION,
@@ -215,6 +223,9 @@ int check_upload_error(dbt_grid* g) {
                        "stores the run length");
     return set_error(DBT_ERR_CORRUPTION, "sign byte outside {0 (occupied), 1 (free)}");
   }
+  rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
+  DBT_CHECK_LAUNCH("rebuild_dist_kernel");
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
   return DBT_OK;
 }
 
@@ -238,7 +249,7 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   g->nx = dims[0];
   g->ny = dims[1];
   g->nz = dims[2];
-  g->nzp = (dims[2] + 3) & ~int64_t(3);
+  g->nzp = (dims[2] + 7) & ~int64_t(7);
   g->x0 = slab_x0;
   g->x1 = slab_x1;
   g->vs = voxel_size;
@@ -252,7 +263,9 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   // +64 cells of slack: the sweep's aligned 4-cell chunks may read up to 3
   // cells past the last row of the slab (never written).
   cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
   if (e != cudaSuccess) {
+    if (g->cells) cudaFree(g->cells);
     delete g;
     return cuda_error(e, "cudaMalloc(voxel grid)");
   }
@@ -292,7 +305,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   dbt::prof_flush(g);
   for (auto e : g->event_pool) cudaEventDestroy(e);
-  void* dev[] = {g->cells,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
+  void* dev[] = {g->cells,  g->dist,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_poses,   g->d_scan_off,
                  g->d_src_off, g->d_scnt, g->d_lcnt, g->d_stage, g->d_rowoff};
   for (void* p : dev)
@@ -313,6 +326,7 @@ int dbt_grid_reset(dbt_grid* g) {
   if (rc) return rc;
   fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
   DBT_CHECK_LAUNCH("fill_cells_kernel");
+  DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   return DBT_OK;
 }
@@ -324,7 +338,7 @@ int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* 
   dims[2] = g->nz;
   slab[0] = g->x0;
   slab[1] = g->x1;
-  *device_bytes = (g->n_cells + 64) * (int64_t)sizeof(uint32_t);
+  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint32_t) + 1);
   return DBT_OK;
 }
 

@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
 
 struct SweepArgs {
   uint32_t* cells;
+  uint8_t* dist;
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
   unsigned long long* changed_out;
-  const uint32_t* dtab;   // [4][nd][CH]
+  const uint2* dtab;      // [8][nd][CH]
   const uint16_t* rowd;   // [rows] distinct id * CH
   const int32_t* rowoff;  // [rows]
   int K, R, nd;
@@ -287,7 +288,8 @@ struct SweepArgs {
 };
 
 // Lower cell p to run length d (generic path, any d in 0..32): CAS on the word.
-__device__ __forceinline__ int lower_cas(uint32_t* p, uint32_t old, int d) {
+__device__ __forceinline__ int lower_cas(uint32_t* p, int d) {
+  uint32_t old = *p;
   while (cell_len(old) > d) {
     uint32_t prev = atomicCAS(p, old, cell_with_len(old, d));
     if (prev == old) return 1;
@@ -298,22 +300,22 @@ __device__ __forceinline__ int lower_cas(uint32_t* p, uint32_t old, int d) {
 
 constexpr int kSweepUnroll = 4;
 
-// Warp per unique centre. Row-major chunk order (row = (dx+R)*K + (dy+R),
-// 4-voxel chunks along z) so consecutive lanes read consecutive 16-byte
-// words of the same z-row: one 21-voxel row is six 128-bit loads. Each lane
-// issues kSweepUnroll independent loads before testing any of them (the
-// atomics below could alias later loads, so the compiler would not hoist
-// them itself).
-// FAST (every kernel distance <= 18): "d lowers the cell" is bit d of the
-// word and the update a fire-and-forget RED.AND. Otherwise CAS per cell.
-// Reads may be stale (L1) — harmless: cells only ever lose bits, so a stale
-// word can only cause a redundant AND, never a missed one.
+// Warp per unique centre. Chunks of 8 voxels along z, row-major over the
+// K*K kernel rows (row = (dx+R)*K + (dy+R)); a 21-voxel row is 3 or 4 64-bit
+// loads of the distance cache depending on the centre's z alignment. Each
+// lane issues kSweepUnroll independent loads before testing any of them (the
+// updates below could alias later loads, so the compiler would not hoist
+// them). A byte lane with d < cached distance marks a voxel this return
+// lowers: RED.AND on its word (FAST: every kernel distance <= 18, where the
+// update is the AND with 0xFF800000 | ((1 << d) - 1); otherwise a CAS), then
+// the new distance goes to the cache. Stale cache reads (L1) only cause
+// redundant updates, never missed ones (cache >= word, see engine.cuh).
 template <int CH, bool FAST>
 __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int rows = a.K * a.K;
-  const int ntab = 4 * a.nd * CH;
-  uint32_t* dtab = reinterpret_cast<uint32_t*>(smem_raw);
+  const int ntab = 8 * a.nd * CH;
+  uint2* dtab = reinterpret_cast<uint2*>(smem_raw);
   int32_t* rowoff = reinterpret_cast<int32_t*>(dtab + ntab);
   uint16_t* rowd = reinterpret_cast<uint16_t*>(rowoff + rows);
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) dtab[i] = a.dtab[i];
@@ -335,52 +337,52 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     int64_t cx, cy, cz;
     unpack_center(a.uniq[u], cx, cy, cz);
     const int64_t zs = cz - a.R;  // >= 0: boundary discard guarantees it
-    const int sh = (int)(zs & 3);
-    uint32_t* const base = a.cells + ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(3));
+    const int sh = (int)(zs & 7);
+    // chunks this alignment needs per row (3 or 4 for K = 21); j -> row by a
+    // 16-bit reciprocal (exact for j < 2^15)
+    const int nch = (sh + a.K + 7) >> 3;
+    const uint32_t magic = (65536u + nch - 1) / nch;
+    const int64_t base = ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(7));
     // slab clip (multi-GPU): rows are dx-major, so the owned dx range is a
     // contiguous range of chunk indices
     const int64_t dxlo = max((int64_t)-a.R, a.x0 - cx);
     const int64_t dxhi = min((int64_t)a.R, a.x1 - 1 - cx);
     if (dxlo > dxhi) continue;
-    const int jlo = (int)((dxlo + a.R) * a.K * CH);
-    const int jhi = (int)((dxhi + a.R + 1) * a.K * CH);
-    const uint32_t* dt = dtab + sh * a.nd * CH;
+    const int jlo = (int)((dxlo + a.R) * a.K * nch);
+    const int jhi = (int)((dxhi + a.R + 1) * a.K * nch);
+    const uint2* dt = dtab + sh * a.nd * CH;
     for (int j0 = jlo + lane; j0 < jhi; j0 += 32 * kSweepUnroll) {
-      uint4 w[kSweepUnroll];
-      uint32_t* p[kSweepUnroll];
-      uint32_t d4[kSweepUnroll];
+      uint2 w[kSweepUnroll], d8[kSweepUnroll];
+      int64_t off[kSweepUnroll];
 #pragma unroll
       for (int k = 0; k < kSweepUnroll; ++k) {
         const int j = j0 + 32 * k;
         const bool v = j < jhi;
         const int jj = v ? j : jlo;
-        const int row = jj / CH;
-        const int ch = jj - row * CH;
-        p[k] = base + rowoff[row] + 4 * ch;
-        d4[k] = v ? dt[rowd[row] + ch] : 0x3F3F3F3Fu;
-        w[k] = *reinterpret_cast<const uint4*>(p[k]);
+        const int row = (int)(((uint32_t)jj * magic) >> 16);
+        const int ch = jj - row * nch;
+        off[k] = base + rowoff[row] + 8 * ch;
+        d8[k] = v ? dt[rowd[row] + ch] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+        w[k] = *reinterpret_cast<const uint2*>(a.dist + off[k]);
       }
 #pragma unroll
       for (int k = 0; k < kSweepUnroll; ++k) {
-        if (FAST) {
-          // bit d of the word is set <=> stored distance > d; d = 63 (outside
-          // the kernel) clamps to a zero probe
-          const uint32_t p0 = __funnelshift_lc(0u, 1u, d4[k] & 0xFF);
-          const uint32_t p1 = __funnelshift_lc(0u, 1u, (d4[k] >> 8) & 0xFF);
-          const uint32_t p2 = __funnelshift_lc(0u, 1u, (d4[k] >> 16) & 0xFF);
-          const uint32_t p3 = __funnelshift_lc(0u, 1u, d4[k] >> 24);
-          if ((w[k].x & p0) | (w[k].y & p1) | (w[k].z & p2) | (w[k].w & p3)) {
-            if (w[k].x & p0) { atomicAnd(p[k] + 0, kKeepSignHits | (p0 - 1u)); ++changed; }
-            if (w[k].y & p1) { atomicAnd(p[k] + 1, kKeepSignHits | (p1 - 1u)); ++changed; }
-            if (w[k].z & p2) { atomicAnd(p[k] + 2, kKeepSignHits | (p2 - 1u)); ++changed; }
-            if (w[k].w & p3) { atomicAnd(p[k] + 3, kKeepSignHits | (p3 - 1u)); ++changed; }
-          }
-        } else {
-          const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+        const uint32_t lt0 = __vcmpltu4(d8[k].x, w[k].x);
+        const uint32_t lt1 = __vcmpltu4(d8[k].y, w[k].y);
+        if (lt0 | lt1) {
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int d = (d4[k] >> (8 * b)) & 0xFF;
-            if (d <= 32 && d < cell_len(ws[b])) changed += lower_cas(p[k] + b, ws[b], d);
+          for (int b = 0; b < 8; ++b) {
+            const uint32_t lt = b < 4 ? lt0 : lt1;
+            if (!((lt >> (8 * (b & 3))) & 0xFF)) continue;
+            const uint32_t d = ((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF;
+            uint32_t* cp = a.cells + off[k] + b;
+            if (FAST) {
+              atomicAnd(cp, kKeepSignHits | ((1u << d) - 1u));
+              ++changed;
+            } else {
+              changed += lower_cas(cp, (int)d);
+            }
+            a.dist[off[k] + b] = (uint8_t)d;
           }
         }
       }
@@ -411,7 +413,7 @@ SweepFn sweep_fn_t(int CH) {
 SweepFn sweep_fn(int CH, bool fast) { return fast ? sweep_fn_t<true>(CH) : sweep_fn_t<false>(CH); }
 
 size_t sweep_smem_bytes(int K, int CH, int nd) {
-  return (size_t)4 * nd * CH * 4 + (size_t)K * K * (4 + 2);
+  return (size_t)8 * nd * CH * sizeof(uint2) + (size_t)K * K * (4 + 2);
 }
 
 __global__ void bin_kernel(const double* __restrict__ dirs, int64_t n, int b_az, int b_el,
@@ -653,6 +655,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
   SweepArgs wa;
   wa.cells = g->cells;
+  wa.dist = g->dist;
   wa.uniq = g->d_uniq;
   wa.lc_in = g->d_lcnt;
   wa.changed_out = &g->d_lcnt->changed;
