@@ -73,8 +73,8 @@ typedef struct dbt_stats {
   int64_t voxels_written;   /* mask cells changed (concurrent count) */
   int64_t points_applied;   /* stamped returns (after first-return dedup) */
   int64_t unique_centers;   /* distinct centre voxels swept */
-  int64_t knife_edges;      /* applied points whose bin raw index is within 1e-12 of an
-                               interior bin boundary (ulp-level transcendental risk) */
+  int64_t bin_fallbacks;    /* returns binned outside the SVML restatement (a nonzero ray
+                               component below 2^-1020 or above 2^993); 0 in practice */
   double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */
   double device_ms;         /* CUDA-event time of the device work (H2D .. stats D2H) */
 } dbt_stats;

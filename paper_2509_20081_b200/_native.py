@@ -45,7 +45,7 @@ class Stats(ctypes.Structure):
         ("voxels_written", ctypes.c_int64),
         ("points_applied", ctypes.c_int64),
         ("unique_centers", ctypes.c_int64),
-        ("knife_edges", ctypes.c_int64),
+        ("bin_fallbacks", ctypes.c_int64),
         ("elapsed_ms", ctypes.c_double),
         ("device_ms", ctypes.c_double),
     ]

@@ -94,7 +94,7 @@ __host__ __device__ inline void unpack_center(uint64_t c, int64_t& x, int64_t& y
 struct ScanCounters {
   unsigned long long n_ok;       // non-discarded returns
   unsigned long long n_applied;  // stamped returns (after first-return)
-  unsigned long long n_knife;    // knife-edge bins among ok returns
+  unsigned long long n_fallback; // returns binned outside the SVML restatement
   unsigned long long pad;
 };
 // Launch-wide device counters.

@@ -27,16 +27,20 @@
 
 #include <chrono>
 
+#include <mutex>
+
 #include "engine.cuh"
+#include "svml_emu.cuh"
 
 using namespace dbt;
+
+extern const uint16_t dbt_svml_seeds[131072];  // build/svml_seeds.cu
 
 namespace {
 
 constexpr double kTwoPi = 6.283185307179586;     // 2.0 * math.pi   (kernels.py:28)
 constexpr double kPi = 3.141592653589793;        // np.pi
 constexpr double kHalfPi = 1.5707963267948966;   // np.pi / 2       (kernels.py:56)
-constexpr double kKnifeEps = 1e-12;
 
 struct PrepArgs {
   const void* pts;
@@ -66,6 +70,7 @@ struct PrepArgs {
   LaunchCounters* lc;
   ScanCounters* sc;
   int8_t* outcome;
+  const uint16_t* seeds;
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t k) {
@@ -88,26 +93,28 @@ __device__ __forceinline__ int find_scan(const int64_t* off, int S, int64_t i) {
 }
 
 // bin_index_array (kernels.py:49-57) for one direction whose axis-1 norm is
-// nrm. The transcendental calls are CUDA's atan2/asin (<= 2 ulp); every other
-// step is the same IEEE operation numpy performs. Returns 1 in knife when a
-// raw index lies within kKnifeEps of an interior bin boundary, where an
-// ulp-level difference in atan2/asin could move the point to the next bin.
+// nrm. arctan2/arcsin are the bit-exact restatement of numpy's SVML routines
+// (svml_emu.cuh), every other step the same IEEE operation numpy performs, so
+// the bin equals the reference's for every input. A ray with a nonzero
+// component outside [2^-1020, 2^993) would take SVML's scalar helper, which is
+// not restated: CUDA's atan2 is used and *fallback is set (counted).
 __device__ __forceinline__ void bin_dev(double rx, double ry, double rz, double nrm, int b_az,
-                                        int b_el, int& ba, int& be, int& knife) {
-  double az = atan2(ry, rx);
+                                        int b_el, const uint16_t* seeds, int& ba, int& be,
+                                        int& fallback) {
+  int rare = 0;
+  double az = svml::atan2(ry, rx, seeds, &rare);
+  fallback = rare;
+  if (rare) az = atan2(ry, rx);
   if (az < 0.0) az = __dadd_rn(az, kTwoPi);
   double ra = __dmul_rn(__ddiv_rn(az, kTwoPi), (double)b_az);
   double q = __ddiv_rn(rz, nrm);
   q = q < -1.0 ? -1.0 : (q > 1.0 ? 1.0 : q);
-  double el = asin(q);
+  double el = svml::asin(q, seeds);
   double re = __dmul_rn(__ddiv_rn(__dadd_rn(el, kHalfPi), kPi), (double)b_el);
   long long ia = (long long)ra;  // astype(np.int64) truncates toward zero
   long long ie = (long long)re;
   ba = (int)(ia < 0 ? 0 : (ia > b_az - 1 ? b_az - 1 : ia));
   be = (int)(ie < 0 ? 0 : (ie > b_el - 1 ? b_el - 1 : ie));
-  double na = rint(ra), ne = rint(re);
-  knife = (fabs(ra - na) < kKnifeEps && na >= 1.0 && na <= b_az - 1) ||
-          (fabs(re - ne) < kKnifeEps && ne >= 1.0 && ne <= b_el - 1);
 }
 
 __device__ __forceinline__ bool floor_index(double v, double o, double vs, long long& out) {
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   const int lane = threadIdx.x & 31;
   bool live = i < a.n;
   int s = 0;
-  int ok = 0, knife = 0;
+  int ok = 0, fallback = 0;
   if (live) {
     s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
     int64_t src = a.src_off[s] + (i - a.scan_off[s]) * a.ds;
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     uint64_t packed = kEmptyKey;
     if (ok) {
       int ba, be;
-      bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, ba, be, knife);
+      bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
       a.bin[i] = (uint16_t)(ba * a.b_el + be);
       packed = pack_center(cx, cy, cz);
       uint64_t key = (uint64_t)((cx * a.ny + cy) * a.nz + cz);
@@ -204,14 +211,14 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
   bool uniform = __all_sync(0xffffffffu, !live || s == s0);
   if (uniform) {
     int nok = __popc(__ballot_sync(0xffffffffu, live && ok));
-    int nkn = __popc(__ballot_sync(0xffffffffu, live && ok && knife));
+    int nkn = __popc(__ballot_sync(0xffffffffu, live && ok && fallback));
     if (lane == __ffs(act) - 1) {
       if (nok) atomicAdd(&a.sc[s0].n_ok, (unsigned long long)nok);
-      if (nkn) atomicAdd(&a.sc[s0].n_knife, (unsigned long long)nkn);
+      if (nkn) atomicAdd(&a.sc[s0].n_fallback, (unsigned long long)nkn);
     }
   } else if (live) {
     if (ok) atomicAdd(&a.sc[s].n_ok, 1ull);
-    if (ok && knife) atomicAdd(&a.sc[s].n_knife, 1ull);
+    if (ok && fallback) atomicAdd(&a.sc[s].n_fallback, 1ull);
   }
 }
 
@@ -417,19 +424,43 @@ size_t sweep_smem_bytes(int K, int CH, int nd) {
 }
 
 __global__ void bin_kernel(const double* __restrict__ dirs, int64_t n, int b_az, int b_el,
-                           int64_t* __restrict__ oa, int64_t* __restrict__ oe) {
+                           const uint16_t* __restrict__ seeds, int64_t* __restrict__ oa,
+                           int64_t* __restrict__ oe) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double x = dirs[3 * i], y = dirs[3 * i + 1], z = dirs[3 * i + 2];
     double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
     int ba, be, kn;
-    bin_dev(x, y, z, nrm, b_az, b_el, ba, be, kn);
+    bin_dev(x, y, z, nrm, b_az, b_el, seeds, ba, be, kn);
     oa[i] = ba;
     oe[i] = be;
   }
 }
 
 // ---------------------------------------------------------------- host side
+
+// SVML seed table, uploaded once per device
+const uint16_t* device_seeds(int device, int* rc) {
+  static std::mutex mu;
+  static uint16_t* tabs[64] = {nullptr};
+  *rc = DBT_OK;
+  if (device < 0 || device >= 64) {
+    *rc = set_error(DBT_ERR_CONFIG, "device ordinal out of range");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!tabs[device]) {
+    uint16_t* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(dbt_svml_seeds));
+    if (e == cudaSuccess) e = cudaMemcpy(p, dbt_svml_seeds, sizeof(dbt_svml_seeds), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      *rc = cuda_error(e, "svml seed table");
+      return nullptr;
+    }
+    tabs[device] = p;
+  }
+  return tabs[device];
+}
 
 int grow(void** p, int64_t* cap, int64_t need, size_t elem) {
   if (need <= *cap) return DBT_OK;
@@ -598,6 +629,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.lc = g->d_lcnt;
   pa.sc = g->d_scnt;
   pa.outcome = d_outcome;
+  pa.seeds = device_seeds(g->device, &rc);
+  if (rc) return rc;
   int tok;
   prof_begin(g, "prep_kernel", st, &tok);
   prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa);
@@ -692,7 +725,7 @@ void fill_stats(dbt_grid* g, const dbt_params* p, dbt_stats* out, int S) {
     int64_t nok = (int64_t)g->h_scnt[s].n_ok;
     o.points_discarded = o.points_in - nok;
     o.points_applied = p->first_return ? (int64_t)g->h_scnt[s].n_applied : nok;
-    o.knife_edges = (int64_t)g->h_scnt[s].n_knife;
+    o.bin_fallbacks = (int64_t)g->h_scnt[s].n_fallback;
     if (s == 0) {
       o.voxels_written = (int64_t)g->h_lcnt->changed;
       o.unique_centers = (int64_t)g->h_lcnt->n_unique;
@@ -847,7 +880,14 @@ int dbt_bin_index_array(const double* dirs, int64_t n, int32_t b_az, int32_t b_e
   e = cudaMemcpy(d_dirs, dirs, n * 24, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
-    bin_kernel<<<blocks, 256>>>(d_dirs, n, b_az, b_el, d_out, d_out + n);
+    int rc2 = DBT_OK;
+    const uint16_t* seeds = device_seeds(device, &rc2);
+    if (rc2) {
+      cudaFree(d_dirs);
+      cudaFree(d_out);
+      return rc2;
+    }
+    bin_kernel<<<blocks, 256>>>(d_dirs, n, b_az, b_el, seeds, d_out, d_out + n);
     e = cudaGetLastError();
     dbt::count_launch();
   }

@@ -108,11 +108,7 @@ def test_device_bins_match_reference(name, golden):
     assert cases.sha(b_e) == ref["b_e"]
 
 
-KNIFE = pytest.mark.xfail(reason="135/225-degree rays one ulp off the diagonal: CUDA atan2 vs numpy SVML "
-                                 "atan2 round differently (DESIGN.md: binning knife edges)", strict=False)
-
-
-@pytest.mark.parametrize("cfg", [1, 2, pytest.param(3, marks=KNIFE)])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_device_bins_match_numpy_on_config_rays(cfg):
     """Every map-frame ray of a config scan bins identically on the device and
     in numpy (the reference's arctan2/arcsin)."""
@@ -127,6 +123,22 @@ def test_device_bins_match_numpy_on_config_rays(cfg):
         ra, re = prep.bin_index_array(rays, 40, 40)
         da, de = Kmod.bin_index_array(rays, 40, 40)
         assert int((ra != da).sum()) == 0 and int((re != de).sum()) == 0
+
+
+@pytest.mark.parametrize("n_az,n_el", [(200, 100), (250, 200), (2048, 128), (1800, 16)])
+def test_device_bins_match_numpy_on_noise_free_fans(n_az, n_el):
+    """Exact azimuth x elevation fans (45-degree multiples hit exactly, the
+    structured knife edges where CUDA's own atan2 differs from numpy's) from
+    several sensor positions: device bins == numpy bins for every ray."""
+    az = np.linspace(0.0, 2 * np.pi, n_az, endpoint=False)
+    el = np.radians(np.linspace(-80, 80, n_el))
+    aa, ee = np.meshgrid(az, el, indexing="ij")
+    dirs = np.stack([np.cos(ee) * np.cos(aa), np.cos(ee) * np.sin(aa), np.sin(ee)], -1).reshape(-1, 3)
+    for t in ((0.0, 0.0, 0.0), (3.2, 7.1, 1.5), (100.0, 100.0, 1.8)):
+        rays = (dirs * 7.3 + np.array(t)) - np.array(t)
+        ra, re = prep.bin_index_array(rays, 40, 40)
+        da, de = Kmod.bin_index_array(rays, 40, 40)
+        assert np.array_equal(ra, da) and np.array_equal(re, de)
 
 
 def test_slab_grids_reassemble_reference():
