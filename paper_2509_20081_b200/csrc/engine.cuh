@@ -149,6 +149,7 @@ struct dbt_grid {
   uint32_t* d_slot = nullptr;
   uint64_t* d_uniq = nullptr;   // unique packed centres
   int64_t cap_hash = 0;
+  uint32_t hash_epoch = 0;      // epoch tag of live hash keys (no per-launch clear)
   unsigned long long* d_hkey = nullptr;
   uint32_t* d_hmin = nullptr;
   double* d_sensor = nullptr;   // map-frame mode per-point sensor (n x 3)
@@ -156,15 +157,12 @@ struct dbt_grid {
   int8_t* d_outcome = nullptr;
   int64_t cap_outcome = 0;
   // per-scan metadata
-  double* d_poses = nullptr;        // kMaxScansPerLaunch x 12
   int64_t* d_scan_off = nullptr;    // kMaxScansPerLaunch + 1 (downsampled)
-  int64_t* d_src_off = nullptr;     // kMaxScansPerLaunch + 1 (raw)
   dbt::ScanCounters* d_scnt = nullptr;
   dbt::LaunchCounters* d_lcnt = nullptr;
   dbt::ScanCounters* h_scnt = nullptr;   // pinned mirrors
   dbt::LaunchCounters* h_lcnt = nullptr;
   int64_t* h_meta = nullptr;             // pinned staging for offsets
-  double* h_poses = nullptr;
   int last_scans = 0;
   std::vector<int64_t> last_points_in;
   std::vector<int64_t> last_points_in_host;

@@ -273,18 +273,16 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   cudaEventCreate(&g->ev_a);
   cudaEventCreate(&g->ev_b);
   cudaEventCreateWithFlags(&g->ev_meta, cudaEventDisableTiming);
-  e = cudaMalloc(&g->d_lcnt, sizeof(LaunchCounters));
-  if (e == cudaSuccess) e = cudaMalloc(&g->d_scnt, sizeof(ScanCounters) * kMaxScansPerLaunch);
-  if (e == cudaSuccess) e = cudaMalloc(&g->d_poses, sizeof(double) * 12 * kMaxScansPerLaunch);
-  if (e == cudaSuccess) e = cudaMalloc(&g->d_scan_off, sizeof(int64_t) * (kMaxScansPerLaunch + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&g->d_src_off, sizeof(int64_t) * (kMaxScansPerLaunch + 1));
-  if (e == cudaSuccess) e = cudaHostAlloc(&g->h_lcnt, sizeof(LaunchCounters), cudaHostAllocDefault);
-  if (e == cudaSuccess)
-    e = cudaHostAlloc(&g->h_scnt, sizeof(ScanCounters) * kMaxScansPerLaunch, cudaHostAllocDefault);
-  if (e == cudaSuccess)
-    e = cudaHostAlloc(&g->h_meta, sizeof(int64_t) * 2 * (kMaxScansPerLaunch + 1), cudaHostAllocDefault);
-  if (e == cudaSuccess)
-    e = cudaHostAlloc(&g->h_poses, sizeof(double) * 12 * kMaxScansPerLaunch, cudaHostAllocDefault);
+  static_assert(sizeof(LaunchCounters) % 32 == 0, "counter block alignment");
+  const size_t cnt_bytes = sizeof(LaunchCounters) + sizeof(ScanCounters) * kMaxScansPerLaunch;
+  e = cudaMalloc(&g->d_lcnt, cnt_bytes);
+  if (e == cudaSuccess) g->d_scnt = reinterpret_cast<ScanCounters*>(g->d_lcnt + 1);
+  // per-launch metadata, packed: scan_off (S+1) | src_off (S+1) | poses (12 S)
+  const size_t meta_bytes = sizeof(int64_t) * (2 * (kMaxScansPerLaunch + 1) + 12 * kMaxScansPerLaunch);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_scan_off, meta_bytes);
+  if (e == cudaSuccess) e = cudaHostAlloc(&g->h_lcnt, cnt_bytes, cudaHostAllocDefault);
+  if (e == cudaSuccess) g->h_scnt = reinterpret_cast<ScanCounters*>(g->h_lcnt + 1);
+  if (e == cudaSuccess) e = cudaHostAlloc(&g->h_meta, meta_bytes, cudaHostAllocDefault);
   if (e != cudaSuccess) {
     int code = cuda_error(e, "grid metadata allocation");
     dbt_grid_destroy(g);
@@ -306,11 +304,11 @@ int dbt_grid_destroy(dbt_grid* g) {
   dbt::prof_flush(g);
   for (auto e : g->event_pool) cudaEventDestroy(e);
   void* dev[] = {g->cells,  g->dist,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
-                 g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_poses,   g->d_scan_off,
-                 g->d_src_off, g->d_scnt, g->d_lcnt, g->d_stage, g->d_rowoff};
+                 g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_scan_off,
+                 g->d_lcnt, g->d_stage, g->d_rowoff};
   for (void* p : dev)
     if (p) cudaFree(p);
-  void* host[] = {g->h_scnt, g->h_lcnt, g->h_meta, g->h_poses};
+  void* host[] = {g->h_lcnt, g->h_meta};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   if (g->ev_a) cudaEventDestroy(g->ev_a);

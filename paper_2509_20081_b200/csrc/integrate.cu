@@ -71,7 +71,37 @@ struct PrepArgs {
   ScanCounters* sc;
   int8_t* outcome;
   const uint16_t* seeds;
+  int inline_meta;     // single scan: pose below, offsets trivial (no device metadata)
+  double pose0[12];
+  uint64_t epoch;      // hash-key epoch tag (bits 52..63); stale slots count as empty
+  // fused shadow update (no first-return, small shadow sets)
+  int fuse_shadow;
+  uint32_t* cells;
+  const int8_t* sxyz;
+  const int32_t* sstart;
+  int64_t x0, x1, nzp;
+  int h_max, t_occ;
 };
+
+constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
+constexpr int kEpochShift = 52;
+constexpr uint32_t kMaxEpoch = 4095;
+
+// h += (h < h_max); sign <- occupied when h >= T (integrator.py:154-159) as a
+// 32-bit CAS on the voxel word
+__device__ __forceinline__ void shadow_update(uint32_t* p, uint32_t h_max, uint32_t t_occ) {
+  uint32_t old = *p;
+  while (true) {
+    uint32_t h = old >> kHitsShift;
+    uint32_t hn = h + (h < h_max ? 1u : 0u);
+    uint32_t nw = (old & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
+    if (hn >= t_occ) nw &= ~kFreeBit;
+    if (nw == old) break;
+    uint32_t prev = atomicCAS(p, old, nw);
+    if (prev == old) break;
+    old = prev;
+  }
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t k) {
   k ^= k >> 33;
@@ -129,15 +159,22 @@ __device__ __forceinline__ bool floor_index(double v, double o, double vs, long 
   return true;
 }
 
-__global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
+__global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool live = i < a.n;
   int s = 0;
   int ok = 0, fallback = 0;
+  bool append = false;  // this lane owns a new sweep work item (unique centre)
+  uint64_t packed = kEmptyKey;
   if (live) {
-    s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
-    int64_t src = a.src_off[s] + (i - a.scan_off[s]) * a.ds;
+    int64_t src;
+    if (a.inline_meta) {
+      src = i * a.ds;
+    } else {
+      s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+      src = a.src_off[s] + (i - a.scan_off[s]) * a.ds;
+    }
     double p0, p1, p2;
     if (a.dtype == DBT_F32) {
       const float* q = (const float*)a.pts + 3 * src;
@@ -159,7 +196,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
       t1 = a.sensor[3 * src + 1];
       t2 = a.sensor[3 * src + 2];
     } else {
-      const double* P = a.poses + 12 * s;
+      const double* P = a.inline_meta ? a.pose0 : a.poses + 12 * s;
       t0 = P[9];
       t1 = P[10];
       t2 = P[11];
@@ -179,30 +216,76 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepArgs a) {
     bool fz = floor_index(m2, a.oz, a.vs, cz);
     ok = ok && fx && fy && fz && cx >= a.R && cy >= a.R && cz >= a.R && cx <= a.nx - 1 - a.R &&
          cy <= a.ny - 1 - a.R && cz <= a.nz - 1 - a.R;
-    uint64_t packed = kEmptyKey;
     if (ok) {
       int ba, be;
       bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
       a.bin[i] = (uint16_t)(ba * a.b_el + be);
       packed = pack_center(cx, cy, cz);
       uint64_t key = (uint64_t)((cx * a.ny + cy) * a.nz + cz);
-      if (a.key_scan_bits) key |= (uint64_t)s << 48;
+      if (a.key_scan_bits) key |= (uint64_t)s << 40;
       uint64_t h = mix64(key) & a.hmask;
-      if (a.no_dedup) a.uniq[atomicAdd(&a.lc->n_unique, 1ull)] = packed;
+      key |= a.epoch;
+      append = a.no_dedup != 0;
+      unsigned long long cur = __ldcg(&a.hkey[h]);
       while (true) {
-        unsigned long long prev = atomicCAS(&a.hkey[h], (unsigned long long)kEmptyKey, (unsigned long long)key);
-        if (prev == kEmptyKey) {
-          if (!a.no_dedup) a.uniq[atomicAdd(&a.lc->n_unique, 1ull)] = packed;
-          break;
+        if (cur == key) break;  // centre already inserted this launch
+        if ((cur & ~kKeyMask) != a.epoch) {
+          // slot is empty for this launch (older epoch): claim it
+          unsigned long long prev = atomicCAS(&a.hkey[h], cur, (unsigned long long)key);
+          if (prev == cur) {
+            if (!a.no_dedup) append = true;
+            break;
+          }
+          cur = prev;  // lost the race: re-examine the same slot
+          continue;
         }
-        if (prev == key) break;
         h = (h + 1) & a.hmask;
+        cur = __ldcg(&a.hkey[h]);
+      }
+      if (a.fuse_shadow) {
+        // up to 8 shadow cells: independent loads, then independent first CAS
+        // attempts; only a lost race takes the retry loop
+        const int b0 = a.sstart[ba * a.b_el + be], nsh = a.sstart[ba * a.b_el + be + 1] - b0;
+        uint32_t* ptr[8];
+        uint32_t old[8], prev[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          ptr[k] = nullptr;
+          if (k < nsh) {
+            const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
+            const int64_t gx = cx + o.x;
+            if (gx >= a.x0 && gx < a.x1) ptr[k] = a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z);
+          }
+          old[k] = ptr[k] ? __ldcg(ptr[k]) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          prev[k] = old[k];
+          if (!ptr[k]) continue;
+          const uint32_t h = old[k] >> kHitsShift;
+          const uint32_t hn = h + (h < (uint32_t)a.h_max ? 1u : 0u);
+          uint32_t nw = (old[k] & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
+          if (hn >= (uint32_t)a.t_occ) nw &= ~kFreeBit;
+          if (nw != old[k]) prev[k] = atomicCAS(ptr[k], old[k], nw);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (ptr[k] && prev[k] != old[k]) shadow_update(ptr[k], (uint32_t)a.h_max, (uint32_t)a.t_occ);
       }
       if (a.first_return) atomicMin(&a.hmin[h], (uint32_t)i);
       a.slot[i] = (uint32_t)h;
     }
     a.center[i] = packed;
     if (a.outcome) a.outcome[i] = ok ? 1 : 0;
+  }
+  // sweep work items: one atomicAdd per warp on the launch-wide counter
+  const unsigned app = __ballot_sync(0xffffffffu, append);
+  if (app) {
+    const int leader = __ffs(app) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(&a.lc->n_unique, (unsigned long long)__popc(app));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (append) a.uniq[base + __popc(app & ((1u << lane) - 1u))] = packed;
   }
   // per-scan counters, warp-aggregated when the warp lies inside one scan
   unsigned act = __ballot_sync(0xffffffffu, live);
@@ -265,19 +348,8 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     unpack_center(c, cx, cy, cz);
     int64_t gx = cx + o.x;
     if (gx < a.x0 || gx >= a.x1) continue;
-    uint32_t* p = a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z);
-    // h += (h < h_max); sign <- occupied when h >= T (integrator.py:154-159)
-    uint32_t old = *p;
-    while (true) {
-      uint32_t h = old >> kHitsShift;
-      uint32_t hn = h + (h < (uint32_t)a.h_max ? 1u : 0u);
-      uint32_t nw = (old & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
-      if (hn >= (uint32_t)a.t_occ) nw &= ~kFreeBit;
-      if (nw == old) break;
-      uint32_t prev = atomicCAS(p, old, nw);
-      if (prev == old) break;
-      old = prev;
-    }
+    shadow_update(a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z), (uint32_t)a.h_max,
+                  (uint32_t)a.t_occ);
   }
 }
 
@@ -504,6 +576,8 @@ int ensure_hash(dbt_grid* g, int64_t n) {
   g->cap_hash = 0;
   DBT_CUDA(cudaMalloc(&g->d_hkey, want * sizeof(unsigned long long)));
   DBT_CUDA(cudaMalloc(&g->d_hmin, want * sizeof(uint32_t)));
+  DBT_CUDA(cudaMemset(g->d_hkey, 0, want * sizeof(unsigned long long)));  // epoch 0: never live
+  g->hash_epoch = 0;
   g->cap_hash = want;
   return DBT_OK;
 }
@@ -548,51 +622,65 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     // every return is discarded by the boundary rule; nothing to launch
   }
   const int ds = d_map_sensor ? 1 : p->downsample;
-  // offsets in pinned staging; wait until the previous launch consumed them
-  int64_t* h_scan = g->h_meta;
-  int64_t* h_src = g->h_meta + (kMaxScansPerLaunch + 1);
-  DBT_CUDA(cudaEventSynchronize(g->ev_meta));
-  h_scan[0] = 0;
-  h_src[0] = 0;
+  if (g->nx * g->ny * g->nz >= (1ll << 40))
+    return set_error(DBT_ERR_CONFIG, "grid has 2^40 voxels or more (hash key width)");
   g->last_points_in.assign(S, 0);
+  int64_t n = 0;
   for (int s = 0; s < S; ++s) {
     if (counts[s] < 0) return set_error(DBT_ERR_CONFIG, "negative point count");
-    int64_t m = (counts[s] + ds - 1) / ds;
-    g->last_points_in[s] = m;
-    h_scan[s + 1] = h_scan[s] + m;
-    h_src[s + 1] = h_src[s] + counts[s];
-    if (!d_map_sensor) {
-      const double* P = poses + 16 * s;
-      double* D = g->h_poses + 12 * s;
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) D[3 * r + c] = P[4 * r + c];
-      D[9] = P[3];
-      D[10] = P[7];
-      D[11] = P[11];
-    }
+    g->last_points_in[s] = (counts[s] + ds - 1) / ds;
+    n += g->last_points_in[s];
   }
   g->last_scans = S;
-  const int64_t n = h_scan[S];
+  g->last_first_return = p->first_return ? 1 : 0;
   int rc = ensure_points(g, std::max<int64_t>(n, 1));
   if (!rc) rc = ensure_hash(g, std::max<int64_t>(n, 1));
   if (!rc) rc = ensure_rows(g, b);
   if (rc) return rc;
-  DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  DBT_CUDA(cudaMemcpyAsync(g->d_src_off, h_src, (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  if (!d_map_sensor)
-    DBT_CUDA(cudaMemcpyAsync(g->d_poses, g->h_poses, S * 12 * sizeof(double), cudaMemcpyHostToDevice, st));
-  DBT_CUDA(cudaEventRecord(g->ev_meta, st));
-  g->last_first_return = p->first_return ? 1 : 0;
-  DBT_CUDA(cudaMemsetAsync(g->d_scnt, 0, S * sizeof(ScanCounters), st));
-  DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters), st));
+  const bool inline_meta = (S == 1);
+  if (!inline_meta) {
+    // one H2D copy of [scan_off (S+1) | src_off (S+1) | poses (12 S)] from
+    // pinned staging; wait until the previous launch consumed it
+    DBT_CUDA(cudaEventSynchronize(g->ev_meta));
+    int64_t* h_scan = g->h_meta;
+    int64_t* h_src = h_scan + (S + 1);
+    double* h_pose = reinterpret_cast<double*>(h_src + (S + 1));
+    h_scan[0] = 0;
+    h_src[0] = 0;
+    for (int s = 0; s < S; ++s) {
+      h_scan[s + 1] = h_scan[s] + g->last_points_in[s];
+      h_src[s + 1] = h_src[s] + counts[s];
+      if (!d_map_sensor) {
+        const double* P = poses + 16 * s;
+        double* D = h_pose + 12 * s;
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) D[3 * r + c] = P[4 * r + c];
+        D[9] = P[3];
+        D[10] = P[7];
+        D[11] = P[11];
+      }
+    }
+    const size_t bytes = (size_t)(2 * (S + 1) + (d_map_sensor ? 0 : 12 * S)) * 8;
+    DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, bytes, cudaMemcpyHostToDevice, st));
+    DBT_CUDA(cudaEventRecord(g->ev_meta, st));
+  }
+  // launch + per-scan counters: one contiguous block, one memset
+  DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
   if (n == 0) return DBT_OK;
   const int64_t hcap = [&] {
     int64_t w = 1024;
     while (w < 2 * n) w <<= 1;
     return w;
   }();
-  DBT_CUDA(cudaMemsetAsync(g->d_hkey, 0xFF, hcap * sizeof(unsigned long long), st));
+  // epoch-tagged hash keys: slots of older launches count as empty, so the
+  // table is cleared only when the 12-bit epoch wraps
+  if (g->hash_epoch >= kMaxEpoch) {
+    DBT_CUDA(cudaMemsetAsync(g->d_hkey, 0, g->cap_hash * sizeof(unsigned long long), st));
+    g->hash_epoch = 0;
+  }
+  ++g->hash_epoch;
   if (p->first_return) DBT_CUDA(cudaMemsetAsync(g->d_hmin, 0xFF, hcap * sizeof(uint32_t), st));
+  const bool fuse_shadow = !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8;
 
   PrepArgs pa;
   pa.pts = d_pts;
@@ -603,8 +691,26 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.map_mode = d_map_sensor != nullptr;
   pa.n = n;
   pa.scan_off = g->d_scan_off;
-  pa.src_off = g->d_src_off;
-  pa.poses = g->d_poses;
+  pa.src_off = g->d_scan_off + (S + 1);
+  pa.poses = reinterpret_cast<const double*>(g->d_scan_off + 2 * (S + 1));
+  pa.inline_meta = inline_meta ? 1 : 0;
+  if (inline_meta && !d_map_sensor) {
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) pa.pose0[3 * r + c] = poses[4 * r + c];
+    pa.pose0[9] = poses[3];
+    pa.pose0[10] = poses[7];
+    pa.pose0[11] = poses[11];
+  }
+  pa.epoch = (uint64_t)g->hash_epoch << kEpochShift;
+  pa.fuse_shadow = fuse_shadow ? 1 : 0;
+  pa.cells = g->cells;
+  pa.sxyz = b->d_shadow_xyz;
+  pa.sstart = b->d_shadow_start;
+  pa.x0 = g->x0;
+  pa.x1 = g->x1;
+  pa.nzp = g->nzp;
+  pa.h_max = p->h_max;
+  pa.t_occ = p->t_occ;
   pa.nx = g->nx;
   pa.ny = g->ny;
   pa.nz = g->nz;
@@ -633,11 +739,11 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   if (rc) return rc;
   int tok;
   prof_begin(g, "prep_kernel", st, &tok);
-  prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pa);
+  prep_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(pa);
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("prep_kernel");
 
-  if (b->max_shadow > 0) {
+  if (b->max_shadow > 0 && !fuse_shadow) {
     ShadowArgs sa;
     sa.cells = g->cells;
     sa.center = g->d_center;
@@ -658,7 +764,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sa.t_occ = p->t_occ;
     sa.first_return = p->first_return ? 1 : 0;
     sa.S = S;
-    sa.scan_off = g->d_scan_off;
+    sa.scan_off = g->d_scan_off;  // only read when S > 1 (first-return)
     sa.sc = g->d_scnt;
     sa.lc = g->d_lcnt;
     int64_t total = n << l2;
@@ -711,9 +817,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
 }
 
 int fetch_counters(dbt_grid* g, cudaStream_t st) {
-  DBT_CUDA(cudaMemcpyAsync(g->h_scnt, g->d_scnt, g->last_scans * sizeof(ScanCounters),
+  DBT_CUDA(cudaMemcpyAsync(g->h_lcnt, g->d_lcnt, sizeof(LaunchCounters) + g->last_scans * sizeof(ScanCounters),
                            cudaMemcpyDeviceToHost, st));
-  DBT_CUDA(cudaMemcpyAsync(g->h_lcnt, g->d_lcnt, sizeof(LaunchCounters), cudaMemcpyDeviceToHost, st));
   return DBT_OK;
 }
 
