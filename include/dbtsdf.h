@@ -52,6 +52,8 @@ extern "C" {
                                         (integrator.py:173-175 uses the 1-D norm) */
 #define DBT_FLAG_NO_DEDUP 4u         /* stamp every applied point (no centre dedup); for
                                         measurement only, the grid result is identical */
+#define DBT_FLAG_NO_SKIP 8u          /* sweep centres whose stamp is already applied too
+                                        (measurement only; identical grid) */
 
 typedef struct dbt_grid dbt_grid; /* device-resident VoxelGrid (grid.py:39-58) */
 typedef struct dbt_bank dbt_bank; /* device copy of a KernelBank (kernels.py:122-141) */
@@ -72,7 +74,9 @@ typedef struct dbt_stats {
   int64_t points_discarded; /* points_in - #(degenerate or out-of-bounds) */
   int64_t voxels_written;   /* mask cells changed (concurrent count) */
   int64_t points_applied;   /* stamped returns (after first-return dedup) */
-  int64_t unique_centers;   /* distinct centre voxels swept */
+  int64_t unique_centers;   /* distinct centre voxels of the launch */
+  int64_t centers_skipped;  /* of those, centres whose stamp an earlier launch already
+                               applied (AND idempotent: no sweep needed) */
   int64_t bin_fallbacks;    /* returns binned outside the SVML restatement (a nonzero ray
                                component below 2^-1020 or above 2^993); 0 in practice */
   double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */

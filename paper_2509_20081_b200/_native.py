@@ -21,6 +21,7 @@ DBT_F64 = 1
 FLAG_MAP_FRAME = 1
 FLAG_SKIP_NORM_CHECK = 2
 FLAG_NO_DEDUP = 4
+FLAG_NO_SKIP = 8
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_dp = ctypes.POINTER(ctypes.c_double)
@@ -45,6 +46,7 @@ class Stats(ctypes.Structure):
         ("voxels_written", ctypes.c_int64),
         ("points_applied", ctypes.c_int64),
         ("unique_centers", ctypes.c_int64),
+        ("centers_skipped", ctypes.c_int64),
         ("bin_fallbacks", ctypes.c_int64),
         ("elapsed_ms", ctypes.c_double),
         ("device_ms", ctypes.c_double),

@@ -102,6 +102,9 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
   b->chunks_per_row = CH;
   b->max_d = max_d;
   b->n_distinct = nd;
+  uint64_t hsh = 1469598103934665603ull ^ (uint64_t)K;
+  for (int i = 0; i < K3; ++i) hsh = (hsh ^ len[i]) * 1099511628211ull;
+  b->dk_hash = hsh | 1;
   b->serial = ++g_bank_serial;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMalloc(&b->d_len, K3);

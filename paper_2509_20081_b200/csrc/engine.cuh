@@ -24,7 +24,14 @@
 // at half the record size.
 //
 // Distance cache: one byte per voxel, dist[v] >= run length of cells[v] at
-// all times (equal after upload/reset). The sweep reads it (8 voxels per
+// all times (equal after upload/reset).
+//
+// Stamp certificates: one bit per voxel, set by the warp that swept the
+// stamp centred at that voxel (one writer per bit per launch: centres are
+// deduplicated). A set bit means the full K^3 stamp of that centre is already
+// in the grid; the AND being idempotent, a later return centred there needs
+// no sweep (its shadow update still runs). Cleared on reset/upload and when a
+// launch uses a different distance kernel. The sweep reads it (8 voxels per
 // 64-bit load) to find the voxels a return lowers, then applies RED.AND to
 // the word and stores the new distance into the cache. Cache stores race
 // only with other lowering stores, so a cache byte can end up stale-high
@@ -101,7 +108,7 @@ struct ScanCounters {
 struct LaunchCounters {
   unsigned long long n_unique;   // unique centre keys (sweep work items)
   unsigned long long changed;    // mask cells changed (voxels_written)
-  unsigned long long shadow_visits;
+  unsigned long long skipped;    // centres whose stamp was already applied (cache byte 0)
   int error;                     // upload validation etc.
   int pad;
 };
@@ -127,6 +134,7 @@ struct dbt_bank {
   int8_t* d_shadow_xyz = nullptr;    // total_shadow x 4 (dx,dy,dz,0)
   int32_t* d_shadow_start = nullptr; // n_bins + 1
   uint64_t serial = 0;               // identity for per-grid caches
+  uint64_t dk_hash = 0;              // FNV-1a of K and the kernel run lengths
 };
 
 struct dbt_grid {
@@ -136,6 +144,7 @@ struct dbt_grid {
   double vs = 0, org[3] = {0, 0, 0};
   uint32_t* cells = nullptr;                // authoritative voxel words
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
+  uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
   int64_t n_cells = 0;                      // (x1-x0)*ny*nzp
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -185,6 +194,8 @@ struct dbt_grid {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // device_ms of the last call
   cudaEvent_t ev_meta = nullptr;               // pinned metadata consumed by the stream
   int last_first_return = 0;
+  // distance kernel the stamp certificates refer to (0: none yet)
+  uint64_t cert_dk = 0;
   int sweep_ch = 0;                            // cached sweep launch shape
   int64_t sweep_blocks = 0;
   double last_device_ms = 0;

@@ -225,7 +225,9 @@ int check_upload_error(dbt_grid* g) {
   }
   rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
+  g->cert_dk = 0;
   return DBT_OK;
 }
 
@@ -264,6 +266,7 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   // cells past the last row of the slab (never written).
   cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
+  if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cells + 63) / 32) * 4);
   if (e != cudaSuccess) {
     if (g->cells) cudaFree(g->cells);
     delete g;
@@ -303,7 +306,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   dbt::prof_flush(g);
   for (auto e : g->event_pool) cudaEventDestroy(e);
-  void* dev[] = {g->cells,  g->dist,  g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
+  void* dev[] = {g->cells,  g->dist,  g->stamped, g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_scan_off,
                  g->d_lcnt, g->d_stage, g->d_rowoff};
   for (void* p : dev)
@@ -325,7 +328,9 @@ int dbt_grid_reset(dbt_grid* g) {
   fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
   DBT_CHECK_LAUNCH("fill_cells_kernel");
   DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
+  g->cert_dk = 0;
   return DBT_OK;
 }
 

@@ -364,6 +364,8 @@ struct SweepArgs {
   const int32_t* rowoff;  // [rows]
   int K, R, nd;
   int64_t x0, x1, ny, nzp;
+  uint32_t* stamped;  // stamp certificate bits
+  int skip_stamped;   // skip centres whose stamp is certified as applied
 };
 
 // Lower cell p to run length d (generic path, any d in 0..32): CAS on the word.
@@ -410,11 +412,18 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   const int64_t hi = min(lo + per, n_unique);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  unsigned long long changed = 0;
+  unsigned long long changed = 0, skipped = 0;
 
   for (int64_t u = lo + warp; u < hi; u += nwarps) {
     int64_t cx, cy, cz;
     unpack_center(a.uniq[u], cx, cy, cz);
+    // the stamp centred here is certified as applied: nothing to sweep
+    const bool own = cx >= a.x0 && cx < a.x1;
+    const int64_t cidx = ((cx - a.x0) * a.ny + cy) * a.nzp + cz;
+    if (own && a.skip_stamped && ((__ldcg(a.stamped + (cidx >> 5)) >> (cidx & 31)) & 1u)) {
+      if (lane == 0) ++skipped;
+      continue;
+    }
     const int64_t zs = cz - a.R;  // >= 0: boundary discard guarantees it
     const int sh = (int)(zs & 7);
     // chunks this alignment needs per row (3 or 4 for K = 21); j -> row by a
@@ -466,9 +475,13 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
         }
       }
     }
+    // every lane's updates for this centre are issued: certify the stamp
+    __syncwarp();
+    if (own && lane == 0) atomicOr(a.stamped + (cidx >> 5), 1u << (cidx & 31));
   }
   for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
   if (lane == 0 && changed) atomicAdd(a.changed_out, changed);
+  if (lane == 0 && skipped) atomicAdd(a.changed_out + 1, skipped);
 }
 
 typedef void (*SweepFn)(SweepArgs);
@@ -808,6 +821,14 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   wa.x1 = g->x1;
   wa.ny = g->ny;
   wa.nzp = g->nzp;
+  if (g->cert_dk != b->dk_hash) {
+    // certificates of another distance kernel say nothing about this one
+    if (g->cert_dk != 0)
+      DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, st));
+    g->cert_dk = b->dk_hash;
+  }
+  wa.stamped = g->stamped;
+  wa.skip_stamped = (p->flags & DBT_FLAG_NO_SKIP) ? 0 : 1;
   unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 7) / 8));
   prof_begin(g, "sweep_kernel", st, &tok);
   fn<<<blocks, 256, smem, st>>>(wa);
@@ -834,6 +855,7 @@ void fill_stats(dbt_grid* g, const dbt_params* p, dbt_stats* out, int S) {
     if (s == 0) {
       o.voxels_written = (int64_t)g->h_lcnt->changed;
       o.unique_centers = (int64_t)g->h_lcnt->n_unique;
+      o.centers_skipped = (int64_t)g->h_lcnt->skipped;
     }
   }
 }

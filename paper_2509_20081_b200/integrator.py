@@ -114,6 +114,7 @@ class FrameStats:
     # device counters (not part of equality, absent from the reference)
     points_applied: int = field(default=0, compare=False)
     unique_centers: int = field(default=0, compare=False)
+    centers_skipped: int = field(default=0, compare=False)
     bin_fallbacks: int = field(default=0, compare=False)
     device_ms: float = field(default=0.0, compare=False)
 
@@ -121,7 +122,7 @@ class FrameStats:
     def from_native(cls, s: _native.Stats, elapsed_ms: float | None = None) -> "FrameStats":
         return cls(int(s.points_in), int(s.points_discarded), int(s.voxels_written),
                    float(s.elapsed_ms if elapsed_ms is None else elapsed_ms), int(s.points_applied),
-                   int(s.unique_centers), int(s.bin_fallbacks), float(s.device_ms))
+                   int(s.unique_centers), int(s.centers_skipped), int(s.bin_fallbacks), float(s.device_ms))
 
 
 def _scan_times(scan: ScanFrame) -> np.ndarray:

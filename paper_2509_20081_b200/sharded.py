@@ -91,7 +91,7 @@ def reduce_stats(stats: list, dist, group=None, device=None) -> list:
     out = []
     for s, w in zip(stats, t.cpu().tolist()):
         out.append(FrameStats(s.points_in, s.points_discarded, int(w), s.elapsed_ms, s.points_applied,
-                              s.unique_centers, s.bin_fallbacks, s.device_ms))
+                              s.unique_centers, s.centers_skipped, s.bin_fallbacks, s.device_ms))
     return out
 
 

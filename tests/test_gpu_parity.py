@@ -279,6 +279,53 @@ class TestReferenceBehaviours:
         assert np.array_equal(g.sign, og.sign)
 
 
+class TestStampCertificate:
+    """Skipping a centre whose own stamp is already applied (cache byte 0)
+    must never change the grid."""
+
+    def _oracle_after(self, bank, frames, init=None, dims=(48, 48, 48)):
+        og = oracle.OracleGrid(dims, 0.1, (0, 0, 0))
+        if init is not None:
+            og.mask[...], og.sign[...], og.hits[...] = init
+        for bk, pts in frames:
+            oracle.integrate_frame(og, oracle.OracleBank.from_bank(bk), pts, np.eye(4))
+        return og
+
+    def test_repeat_scans_skip_and_match(self):
+        bank = build_kernel_bank(shadow_radius=2)
+        rng = np.random.default_rng(3)
+        pts = rng.uniform(1.15, 3.6, size=(400, 3))
+        g = new_grid((48, 48, 48), 0.1)
+        s1 = integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        s2 = integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        assert s1.centers_skipped == 0 and s2.centers_skipped == s2.unique_centers > 0
+        og = self._oracle_after(bank, [(bank, pts), (bank, pts)])
+        assert np.array_equal(g.mask, og.mask) and np.array_equal(g.hits, og.hits) and np.array_equal(g.sign, og.sign)
+
+    def test_bank_change_voids_certificate(self):
+        small = build_kernel_bank(size=9, shadow_radius=1)
+        big = build_kernel_bank(size=21, shadow_radius=1)
+        rng = np.random.default_rng(4)
+        pts = rng.uniform(1.15, 3.6, size=(300, 3))
+        g = new_grid((48, 48, 48), 0.1)
+        integrate_frame(g, small, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        st = integrate_frame(g, big, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        assert st.centers_skipped == 0
+        og = self._oracle_after(big, [(small, pts), (big, pts)])
+        assert np.array_equal(g.mask, og.mask)
+
+    def test_uploaded_zero_is_not_a_certificate(self):
+        bank = build_kernel_bank(shadow_radius=1)
+        g = new_grid((48, 48, 48), 0.1)
+        g.mask[24, 24, 24] = 0  # distance 0 written by the host, no stamp applied
+        init = (g.mask.copy(), g.sign.copy(), g.hits.copy())
+        p = np.array([[2.45, 2.45, 2.45]])  # centre voxel (24, 24, 24)
+        st = integrate_frame(g, bank, ScanFrame(points=p, pose=np.eye(4)), IntegrationParams())
+        assert st.centers_skipped == 0
+        og = self._oracle_after(bank, [(bank, p)], init=init)
+        assert np.array_equal(g.mask, og.mask)
+
+
 class TestGridSemantics:
     def test_host_mirror_in_place_and_injected_fault(self):
         bank = build_kernel_bank(shadow_radius=3)

@@ -22,4 +22,4 @@ passes = 2 if "--repeat" in sys.argv else 1
 for p in range(passes):
     for k, s in enumerate(scans):
         st = integrate_frame(g, bank, s, IntegrationParams())
-        print(p, k, st.device_ms, st.voxels_written, st.unique_centers, flush=True)
+        print(p, k, round(st.device_ms, 3), st.voxels_written, st.unique_centers, st.centers_skipped, flush=True)
