@@ -6,7 +6,7 @@
 //  * the sweep table: for each of the 8 possible z-alignments of a centre,
 //    each DISTINCT kernel z-row (identical rows are shared; 66 of the 441
 //    rows of the standard 21^3 kernel are distinct) and each 8-voxel chunk of
-//    that row, the 8 run lengths packed into a uint2 (0xFF marks a voxel
+//    that row, the 8 run lengths + 1 packed into a uint2 (64 marks a voxel
 //    outside the kernel, which can never lower a distance <= 32), plus the
 //    row -> distinct-row map;
 //  * the shadow table in CSR form, offsets as int8 (|o| <= R <= 15).
@@ -66,7 +66,8 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
         uint32_t v[2] = {0, 0};
         for (int i = 0; i < 8; ++i) {
           int zk = 8 * c + i - s;
-          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)distinct[q] * K + zk] : 0xFFu;
+          // d + 1, 64 outside the kernel (see the sweep's byte test)
+          uint32_t d = (zk >= 0 && zk < K) ? len[(size_t)distinct[q] * K + zk] + 1u : 64u;
           v[i >> 2] |= d << (8 * (i & 3));
         }
         dtab[((size_t)s * nd + q) * CH + c] = make_uint2(v[0], v[1]);

@@ -397,13 +397,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   const int rows = a.K * a.K;
   const int ntab = 8 * a.nd * CH;
   uint2* dtab = reinterpret_cast<uint2*>(smem_raw);
-  int32_t* rowoff = reinterpret_cast<int32_t*>(dtab + ntab);
-  uint16_t* rowd = reinterpret_cast<uint16_t*>(rowoff + rows);
+  // per kernel row: {voxel offset of the row, index of its d-row in the table}
+  int2* rowinfo = reinterpret_cast<int2*>(dtab + ntab);
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) dtab[i] = a.dtab[i];
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-    rowoff[i] = a.rowoff[i];
-    rowd[i] = a.rowd[i];
-  }
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) rowinfo[i] = make_int2(a.rowoff[i], a.rowd[i]);
   __syncthreads();
 
   const int64_t n_unique = (int64_t)a.lc_in->n_unique;
@@ -449,20 +446,24 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
         const int jj = v ? j : jlo;
         const int row = (int)(((uint32_t)jj * magic) >> 16);
         const int ch = jj - row * nch;
-        off[k] = base + rowoff[row] + 8 * ch;
-        d8[k] = v ? dt[rowd[row] + ch] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+        const int2 ri = rowinfo[row];
+        off[k] = base + ri.x + 8 * ch;
+        d8[k] = v ? dt[ri.y + ch] : make_uint2(0x40404040u, 0x40404040u);
         w[k] = *reinterpret_cast<const uint2*>(a.dist + off[k]);
       }
 #pragma unroll
       for (int k = 0; k < kSweepUnroll; ++k) {
-        const uint32_t lt0 = __vcmpltu4(d8[k].x, w[k].x);
-        const uint32_t lt1 = __vcmpltu4(d8[k].y, w[k].y);
+        // per byte: cached distance L <= 32, table holds d + 1 <= 64, so
+        // (L | 0x80) - (d + 1) never borrows across bytes and its bit 7 is
+        // set exactly when d < L (the return lowers this voxel)
+        const uint32_t lt0 = ((w[k].x | 0x80808080u) - d8[k].x) & 0x80808080u;
+        const uint32_t lt1 = ((w[k].y | 0x80808080u) - d8[k].y) & 0x80808080u;
         if (lt0 | lt1) {
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             const uint32_t lt = b < 4 ? lt0 : lt1;
-            if (!((lt >> (8 * (b & 3))) & 0xFF)) continue;
-            const uint32_t d = ((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF;
+            if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
+            const uint32_t d = (((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF) - 1u;
             uint32_t* cp = a.cells + off[k] + b;
             if (FAST) {
               atomicAnd(cp, kKeepSignHits | ((1u << d) - 1u));
@@ -505,7 +506,7 @@ SweepFn sweep_fn_t(int CH) {
 SweepFn sweep_fn(int CH, bool fast) { return fast ? sweep_fn_t<true>(CH) : sweep_fn_t<false>(CH); }
 
 size_t sweep_smem_bytes(int K, int CH, int nd) {
-  return (size_t)8 * nd * CH * sizeof(uint2) + (size_t)K * K * (4 + 2);
+  return (size_t)8 * nd * CH * sizeof(uint2) + (size_t)K * K * sizeof(int2);
 }
 
 __global__ void bin_kernel(const double* __restrict__ dirs, int64_t n, int b_az, int b_el,
@@ -693,7 +694,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
   ++g->hash_epoch;
   if (p->first_return) DBT_CUDA(cudaMemsetAsync(g->d_hmin, 0xFF, hcap * sizeof(uint32_t), st));
-  const bool fuse_shadow = !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8;
+  const bool fuse_shadow =
+      !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && !(p->flags & DBT_FLAG_NO_FUSE);
 
   PrepArgs pa;
   pa.pts = d_pts;
