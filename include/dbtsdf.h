@@ -76,9 +76,10 @@ typedef struct dbt_stats {
   int64_t points_discarded; /* points_in - #(degenerate or out-of-bounds) */
   int64_t voxels_written;   /* mask cells changed (concurrent count) */
   int64_t points_applied;   /* stamped returns (after first-return dedup) */
-  int64_t unique_centers;   /* distinct centre voxels of the launch */
-  int64_t centers_skipped;  /* of those, centres whose stamp an earlier launch already
-                               applied (AND idempotent: no sweep needed) */
+  int64_t unique_centers;   /* centre voxels swept by this launch */
+  int64_t centers_skipped;  /* applied returns whose centre needed no sweep: its K^3 stamp
+                               was applied by an earlier launch or claimed by another
+                               return of this launch (AND idempotent) */
   int64_t bin_fallbacks;    /* returns binned outside the SVML restatement (a nonzero ray
                                component below 2^-1020 or above 2^993); 0 in practice */
   double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */

@@ -81,6 +81,10 @@ struct PrepArgs {
   const int32_t* sstart;
   int64_t x0, x1, nzp;
   int h_max, t_occ;
+  // claim mode (no first-return): dedup + cross-launch skip through the stamp
+  // certificate bits instead of the hash table
+  int claim;
+  uint32_t* stamped;
 };
 
 constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
   int s = 0;
   int ok = 0, fallback = 0;
   bool append = false;  // this lane owns a new sweep work item (unique centre)
+  bool claimed = false; // centre stamp already applied / claimed: no sweep
   uint64_t packed = kEmptyKey;
   if (live) {
     int64_t src;
@@ -221,13 +226,27 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
       bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
       a.bin[i] = (uint16_t)(ba * a.b_el + be);
       packed = pack_center(cx, cy, cz);
+      if (a.claim) {
+        // claim the stamp certificate of the centre (one atomicOr): a bit
+        // already set means the stamp is in the grid from an earlier launch
+        // or owned by an earlier return of this launch; either way no sweep.
+        // A centre outside this rank's slab has no bit here: always swept.
+        if (cx >= a.x0 && cx < a.x1) {
+          const int64_t cidx = ((cx - a.x0) * a.ny + cy) * a.nzp + cz;
+          const uint32_t bit = 1u << (cidx & 31);
+          claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
+          append = !claimed;
+        } else {
+          append = true;
+        }
+      }
       uint64_t key = (uint64_t)((cx * a.ny + cy) * a.nz + cz);
       if (a.key_scan_bits) key |= (uint64_t)s << 40;
       uint64_t h = mix64(key) & a.hmask;
       key |= a.epoch;
-      append = a.no_dedup != 0;
-      unsigned long long cur = __ldcg(&a.hkey[h]);
-      while (true) {
+      if (!a.claim) append = a.no_dedup != 0;
+      unsigned long long cur = a.claim ? 0ull : __ldcg(&a.hkey[h]);
+      while (!a.claim) {
         if (cur == key) break;  // centre already inserted this launch
         if ((cur & ~kKeyMask) != a.epoch) {
           // slot is empty for this launch (older epoch): claim it
@@ -287,6 +306,8 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
     base = __shfl_sync(0xffffffffu, base, leader);
     if (append) a.uniq[base + __popc(app & ((1u << lane) - 1u))] = packed;
   }
+  const unsigned clm = __ballot_sync(0xffffffffu, claimed);
+  if (clm && lane == __ffs(clm) - 1) atomicAdd(&a.lc->skipped, (unsigned long long)__popc(clm));
   // per-scan counters, warp-aggregated when the warp lies inside one scan
   unsigned act = __ballot_sync(0xffffffffu, live);
   if (!act) return;
@@ -365,7 +386,8 @@ struct SweepArgs {
   int K, R, nd;
   int64_t x0, x1, ny, nzp;
   uint32_t* stamped;  // stamp certificate bits
-  int skip_stamped;   // skip centres whose stamp is certified as applied
+  int skip_stamped;   // hash mode: skip centres whose stamp is certified as applied
+  int certify;        // hash mode: set the certificate after sweeping (claim mode set it)
 };
 
 // Lower cell p to run length d (generic path, any d in 0..32): CAS on the word.
@@ -478,7 +500,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     }
     // every lane's updates for this centre are issued: certify the stamp
     __syncwarp();
-    if (own && lane == 0) atomicOr(a.stamped + (cidx >> 5), 1u << (cidx & 31));
+    if (own && a.certify && lane == 0) atomicOr(a.stamped + (cidx >> 5), 1u << (cidx & 31));
   }
   for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
   if (lane == 0 && changed) atomicAdd(a.changed_out, changed);
@@ -694,6 +716,14 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
   ++g->hash_epoch;
   if (p->first_return) DBT_CUDA(cudaMemsetAsync(g->d_hmin, 0xFF, hcap * sizeof(uint32_t), st));
+  if (g->cert_dk != b->dk_hash) {
+    // certificates of another distance kernel say nothing about this one
+    if (g->cert_dk != 0)
+      DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, st));
+    g->cert_dk = b->dk_hash;
+  }
+  // claim mode: centre dedup and cross-launch skip through the certificates
+  const bool claim = !p->first_return && !(p->flags & (DBT_FLAG_NO_SKIP | DBT_FLAG_NO_DEDUP));
   const bool fuse_shadow =
       !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && !(p->flags & DBT_FLAG_NO_FUSE);
 
@@ -726,6 +756,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.nzp = g->nzp;
   pa.h_max = p->h_max;
   pa.t_occ = p->t_occ;
+  pa.claim = claim ? 1 : 0;
+  pa.stamped = g->stamped;
   pa.nx = g->nx;
   pa.ny = g->ny;
   pa.nz = g->nz;
@@ -823,14 +855,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   wa.x1 = g->x1;
   wa.ny = g->ny;
   wa.nzp = g->nzp;
-  if (g->cert_dk != b->dk_hash) {
-    // certificates of another distance kernel say nothing about this one
-    if (g->cert_dk != 0)
-      DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, st));
-    g->cert_dk = b->dk_hash;
-  }
   wa.stamped = g->stamped;
-  wa.skip_stamped = (p->flags & DBT_FLAG_NO_SKIP) ? 0 : 1;
+  wa.skip_stamped = (p->flags & DBT_FLAG_NO_SKIP) || claim ? 0 : 1;
+  wa.certify = claim ? 0 : 1;
   unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 7) / 8));
   prof_begin(g, "sweep_kernel", st, &tok);
   fn<<<blocks, 256, smem, st>>>(wa);

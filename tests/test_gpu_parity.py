@@ -298,7 +298,9 @@ class TestStampCertificate:
         g = new_grid((48, 48, 48), 0.1)
         s1 = integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
         s2 = integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
-        assert s1.centers_skipped == 0 and s2.centers_skipped == s2.unique_centers > 0
+        assert s1.unique_centers + s1.centers_skipped == s1.points_applied == 400
+        assert s1.unique_centers > 300
+        assert s2.unique_centers == 0 and s2.centers_skipped == 400  # every stamp already applied
         og = self._oracle_after(bank, [(bank, pts), (bank, pts)])
         assert np.array_equal(g.mask, og.mask) and np.array_equal(g.hits, og.hits) and np.array_equal(g.sign, og.sign)
 
@@ -308,9 +310,10 @@ class TestStampCertificate:
         rng = np.random.default_rng(4)
         pts = rng.uniform(1.15, 3.6, size=(300, 3))
         g = new_grid((48, 48, 48), 0.1)
-        integrate_frame(g, small, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        s1 = integrate_frame(g, small, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
         st = integrate_frame(g, big, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
-        assert st.centers_skipped == 0
+        # every distinct centre is swept again: the small kernel's stamps certify nothing
+        assert st.unique_centers == s1.unique_centers > 250
         og = self._oracle_after(big, [(small, pts), (big, pts)])
         assert np.array_equal(g.mask, og.mask)
 
