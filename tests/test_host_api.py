@@ -135,6 +135,32 @@ class TestParamsAndFrames:
         with pytest.raises(ConfigurationError):
             motion_compensate(ScanFrame(points=np.zeros((2, 3)), pose=np.eye(4)), "se3")
 
+    def test_check_rotation_decisions_match_numpy_formulation(self):
+        """The float fast path decides exactly like np.allclose/np.isclose
+        (transforms.py:30-37) on random near-rotations, reflections and
+        non-finite input."""
+        from paper_2509_20081_b200.transforms import _check_rotation_numpy, check_rotation
+
+        rng = np.random.default_rng(0)
+
+        def decide(f):
+            try:
+                f()
+                return "ok"
+            except ConfigurationError as e:
+                return str(e)
+
+        mats = []
+        for k in range(3000):
+            R = Rotation.random(random_state=k).as_matrix()
+            R = R + rng.normal(size=(3, 3)) * 10.0 ** rng.uniform(-16, -3) * (rng.random() < 0.7)
+            mats.append(-R if rng.random() < 0.1 else R)
+        mats += [np.full((3, 3), np.nan), np.diag([np.inf, 1, 1]), np.eye(3) * (1 + 1e-5)]
+        for R in mats:
+            T = np.eye(4)
+            T[:3, :3] = R
+            assert decide(lambda: check_rotation(T)) == decide(lambda: _check_rotation_numpy(R, 1e-9))
+
     def test_yaw_interpolation(self):
         a = make_pose(Rotation.from_euler("z", 0.1), (0, 0, 0))
         b = make_pose(Rotation.from_euler("z", 0.5), (2, 0, 0))
