@@ -54,8 +54,8 @@ extern "C" {
                                         measurement only, the grid result is identical */
 #define DBT_FLAG_NO_SKIP 8u          /* sweep centres whose stamp is already applied too
                                         (measurement only; identical grid) */
-#define DBT_FLAG_NO_FUSE 16u         /* shadow update in its own kernel instead of fused
-                                        into preprocessing (measurement only) */
+#define DBT_FLAG_FUSE_SHADOW 16u     /* shadow update fused into preprocessing instead of
+                                        a kernel concurrent with the sweep (measurement) */
 
 typedef struct dbt_grid dbt_grid; /* device-resident VoxelGrid (grid.py:39-58) */
 typedef struct dbt_bank dbt_bank; /* device copy of a KernelBank (kernels.py:122-141) */

@@ -193,6 +193,8 @@ struct dbt_grid {
   std::vector<int64_t> prof_launches;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // device_ms of the last call
   cudaEvent_t ev_meta = nullptr;               // pinned metadata consumed by the stream
+  cudaStream_t aux = nullptr;                  // shadow kernel, concurrent with the sweep
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int last_first_return = 0;
   // distance kernel the stamp certificates refer to (0: none yet)
   uint64_t cert_dk = 0;

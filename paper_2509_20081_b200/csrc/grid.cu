@@ -276,6 +276,9 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   cudaEventCreate(&g->ev_a);
   cudaEventCreate(&g->ev_b);
   cudaEventCreateWithFlags(&g->ev_meta, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming);
   static_assert(sizeof(LaunchCounters) % 32 == 0, "counter block alignment");
   const size_t cnt_bytes = sizeof(LaunchCounters) + sizeof(ScanCounters) * kMaxScansPerLaunch;
   e = cudaMalloc(&g->d_lcnt, cnt_bytes);
@@ -317,6 +320,9 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->ev_a) cudaEventDestroy(g->ev_a);
   if (g->ev_b) cudaEventDestroy(g->ev_b);
   if (g->ev_meta) cudaEventDestroy(g->ev_meta);
+  if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+  if (g->ev_join) cudaEventDestroy(g->ev_join);
+  if (g->aux) cudaStreamDestroy(g->aux);
   if (g->stream && g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
   return DBT_OK;

@@ -724,8 +724,11 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
   // claim mode: centre dedup and cross-launch skip through the certificates
   const bool claim = !p->first_return && !(p->flags & (DBT_FLAG_NO_SKIP | DBT_FLAG_NO_DEDUP));
+  // the shadow update runs as its own kernel on the aux stream, concurrent
+  // with the sweep (one is atomic-latency bound, the other L1 bound); fusing
+  // it into preprocessing is kept as a measurement option
   const bool fuse_shadow =
-      !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && !(p->flags & DBT_FLAG_NO_FUSE);
+      !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && (p->flags & DBT_FLAG_FUSE_SHADOW);
 
   PrepArgs pa;
   pa.pts = d_pts;
@@ -790,6 +793,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("prep_kernel");
 
+  bool joined = false;
   if (b->max_shadow > 0 && !fuse_shadow) {
     ShadowArgs sa;
     sa.cells = g->cells;
@@ -816,10 +820,16 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sa.lc = g->d_lcnt;
     int64_t total = n << l2;
     unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
-    prof_begin(g, "shadow_kernel", st, &tok);
-    shadow_kernel<<<blocks, 256, 0, st>>>(sa);
-    prof_end(g, st, tok);
+    // fork: aux waits for prep, runs the shadow kernel; joined before the
+    // counters are read back
+    DBT_CUDA(cudaEventRecord(g->ev_fork, st));
+    DBT_CUDA(cudaStreamWaitEvent(g->aux, g->ev_fork, 0));
+    prof_begin(g, "shadow_kernel", g->aux, &tok);
+    shadow_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+    prof_end(g, g->aux, tok);
     DBT_CHECK_LAUNCH("shadow_kernel");
+    DBT_CUDA(cudaEventRecord(g->ev_join, g->aux));
+    joined = true;
   }
 
   const int CH = b->chunks_per_row;
@@ -863,6 +873,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   fn<<<blocks, 256, smem, st>>>(wa);
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("sweep_kernel");
+  if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
   return DBT_OK;
 }
 

@@ -15,7 +15,7 @@ w = workloads.get(2)
 scans = [torch.from_numpy(w.scan(k)).cuda() for k in range(30)]
 bank = build_kernel_bank(shadow_radius=w.shadow_radius)
 L = _native.lib()
-variants = {"default": 0, "no_fuse": _native.FLAG_NO_FUSE, "no_skip": _native.FLAG_NO_SKIP,
+variants = {"default": 0, "fused": _native.FLAG_FUSE_SHADOW, "no_skip": _native.FLAG_NO_SKIP,
             "no_dedup": _native.FLAG_NO_DEDUP}
 for name, flags in variants.items():
     g = VoxelGrid(w.dims, w.voxel_size, w.origin)
