@@ -1,24 +1,28 @@
 """Benchmark: LiDAR points integrated per second (BASELINE.json metric).
 
-Workload (configs[1] of BASELINE.json, the largest single-GPU config the
+Default workload (configs[1] of BASELINE.json, the single-GPU config the
 metric is quoted on): config 2 — 100-scan trajectory in the synthetic box
 room, 64 beams x 1024 azimuths (65 536 float32 returns per scan), 0.05 m
 voxels on the 400x400x100 room padded by 11 voxels (422x422x122; the literal
 grid discards every wall return), K=21 kernel, 40x40 bins, shadow radius 1.
+`--config N` selects another BASELINE config (3: street 2000x2000x100 @ 0.1 m,
+4: 4000x4000x400 @ 0.02 m, 5: config-3 scans, `--batch S` per launch).
 
-A step integrates the next scan of the trajectory into the grid that holds
-all previous scans (the grid is reset when the trajectory wraps, outside the
-timed region). L2 is flushed (256 MB write) between timed steps.
+A step integrates the next scan (or the next S scans, one launch) of the
+trajectory into the grid that holds all previous scans (the grid is reset
+when the trajectory wraps, outside the timed region). L2 is flushed (256 MB
+write) between timed steps.
 
   value : applied returns / device seconds, scans resident in HBM, CUDA
-          events on the launch stream around each step (prep + shadow + sweep
-          + counter copy), summed over K steps, max over ranks.
-  e2e   : same metric through the public API (integrate_frame with a
-          ScanFrame over PINNED host float32 points): H2D of the scan, the
-          launch sequence and the D2H of the FrameStats counters are inside
-          the timed region (host wall clock per call).
+          events on the launch stream around each step (launch sequence incl.
+          the concurrent shadow stream and the counter copy), summed over K
+          steps, max over ranks.
+  e2e   : same metric through the public API (integrate_frame /
+          integrate_frames over PINNED host float32 scans): validation, H2D,
+          launches, D2H of the FrameStats counters, host wall clock per call.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--config 2] [--batch 1]
 Under torchrun (N>1) every rank owns an x-slab of the grid; rank 0 holds the
 scans and broadcasts each step's points over NCCL inside the timed region.
 """
@@ -33,6 +37,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ProcessPoolExecutor
 
 import numpy as np
 
@@ -41,7 +46,6 @@ sys.path.insert(0, ROOT)
 
 import workloads  # noqa: E402
 
-CONFIG = 2
 METRIC = "LiDAR points integrated/sec (device-timed)"
 UNIT = "points/s"
 K_EDGE = 21
@@ -108,11 +112,13 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
         def num(v):
             try:
                 return float(v)
             except ValueError:
                 return None
+
         sm = [x for x in (num(r[0]) for r in self.rows) if x is not None]
         mx = [x for x in (num(r[1]) for r in self.rows) if x is not None]
         reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
@@ -120,8 +126,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _scan_job(args):
+    config, k = args
+    return workloads.get(config).scan(k)
+
+
 def gen_scans(w, n):
-    return [w.scan(k) for k in range(n)]
+    """Scans 0..n-1 of the trajectory (ray casting in a process pool for the
+    street scenes, ~2.6 s per config-3 scan)."""
+    if w.config <= 2 or n <= 2:
+        return [w.scan(k) for k in range(n)]
+    with ProcessPoolExecutor(max_workers=min(n, os.cpu_count() or 1)) as ex:
+        return list(ex.map(_scan_job, [(w.config, k) for k in range(n)]))
+
+
+def cpu_grid_for(w):
+    """Grid the CPU samples run on. Config 4's 6.4e9-voxel grid needs 38 GB
+    of reference host arrays; per-scan CPU cost does not depend on grid size
+    (BASELINE.md §2), so its sample uses the config-4 window
+    of tests/cases.py (1000x1000x400 at the same origin offset)."""
+    if w.config == 4:
+        return (1000, 1000, 400), (0.0, 90.0, -0.22), "config-4 scene on its 1000x1000x400 window grid"
+    return w.dims, w.origin, "same grid"
 
 
 def cpu_baseline(w, scans, budget_s=12.0, threads=None):
@@ -132,7 +158,8 @@ def cpu_baseline(w, scans, budget_s=12.0, threads=None):
 
     threads = threads or oracle.os_threads()
     ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
-    g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+    dims, origin, note = cpu_grid_for(w)
+    g = oracle.OracleGrid(dims, w.voxel_size, origin)
     applied = 0
     t0 = time.perf_counter()
     k = 0
@@ -144,8 +171,8 @@ def cpu_baseline(w, scans, budget_s=12.0, threads=None):
             break
     el = time.perf_counter() - t0
     return {"value": applied / el, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"config-2 scans 0..{k - 1} ({k} scans, {applied} applied returns) in {el:.1f} s, "
-                      f"oracle C port (libm transcendentals), {threads} threads (x-slab stamping)"}
+            "sample": f"config-{w.config} scans 0..{k - 1} ({k} scans, {applied} applied returns) in {el:.1f} s, "
+                      f"{note}, oracle C port (libm transcendentals), {threads} threads (x-slab stamping)"}
 
 
 def run_reference(args, rank, world):
@@ -156,19 +183,20 @@ def run_reference(args, rank, world):
         return
     import oracle
 
-    w = workloads.get(CONFIG)
+    w = workloads.get(args.config)
     n = args.warmup + args.steps
     scans = gen_scans(w, min(n, w.n_scans))
     threads = oracle.os_threads()
     ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
-    g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+    dims, origin, note = cpu_grid_for(w)
+    g = oracle.OracleGrid(dims, w.voxel_size, origin)
     applied, el = 0, 0.0
     for s in range(n):
-        k = s % w.n_scans
+        k = s % len(scans)
         if k == 0 and s > 0:
-            g = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+            g = oracle.OracleGrid(dims, w.voxel_size, origin)
         t0 = time.perf_counter()
-        st = oracle.integrate_frame(g, ob, scans[k % len(scans)], w.poses[k], threads=threads, c_prep=True)
+        st = oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             applied += st.points_in - st.points_discarded
@@ -178,21 +206,24 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w),
+        "config": config_desc(w, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} timed scans of config 2 (full scans), oracle C port of the "
-                                   f"reference integrate_frame, {threads} threads"},
+                         "sample": f"{args.steps} timed scans of config {args.config} (full scans, {note}), oracle "
+                                   f"C port of the reference integrate_frame, {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_desc(w):
-    return {"workload": f"config {CONFIG}: synthetic room, 100-scan trajectory, 64x1024 float32 returns/scan, "
-                        f"{w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]} "
-                        "(400x400x100 padded by 11)",
+def config_desc(w, batch):
+    scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
+    return {"workload": f"config {w.config}: {scene}, {w.n_scans}-scan trajectory, {w.beams}x{w.n_az} float32 "
+                        f"returns/scan, {w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]}"
+                        + (" (literal room grid padded by 11)" if w.config <= 2 else ""),
             "kernel": f"{K_EDGE}^3", "bins": "40x40", "shadow_radius": w.shadow_radius, "t_occ": 2, "h_max": 255,
-            "step": "one scan integrated into the trajectory grid", "l2": "flushed between steps (256 MB write)",
+            "scans_per_step": batch,
+            "step": f"{batch} scan(s) integrated into the trajectory grid in one launch",
+            "l2": "flushed between steps (256 MB write)",
             "parallelism": "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU"}
 
 
@@ -202,6 +233,9 @@ def main():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--batch", type=int, default=1, help="scans per launch (config 5: 1/8/32/128)")
+    ap.add_argument("--max-scans", type=int, default=None, help="distinct scans to generate (default: all needed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -215,7 +249,8 @@ def main():
     import torch
 
     from paper_2509_20081_b200 import _native
-    from paper_2509_20081_b200 import (IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame, new_grid)
+    from paper_2509_20081_b200 import (IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame,
+                                       integrate_frames, new_grid)
     from paper_2509_20081_b200.sharded import ShardedGrid
 
     torch.cuda.set_device(local)
@@ -224,34 +259,44 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = workloads.get(CONFIG)
-    n_total = args.warmup + args.steps
-    scans = gen_scans(w, min(n_total, w.n_scans))
+    w = workloads.get(args.config)
+    B = max(1, args.batch)
+    need = (args.warmup + args.steps) * B
+    n_avail = min(w.n_scans, need if args.max_scans is None else min(need, args.max_scans))
+    n_avail = max(B, n_avail - n_avail % B)  # whole batches; the trajectory wraps with a grid reset
+    scans = gen_scans(w, n_avail)
+    steps_per_pass = n_avail // B
     bank = build_kernel_bank(size=K_EDGE, shadow_radius=w.shadow_radius)
     shadow_cells = float(np.mean([len(o) for o in bank.shadow_offsets]))
     params = IntegrationParams()
     L = _native.lib()
+    dev = f"cuda:{local}"
 
     # ---------------- device-resident value --------------------------------
     sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local)
-    dev_scans = [torch.from_numpy(s).to(f"cuda:{local}") for s in scans] if rank == 0 else None
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+    # one device buffer per step-batch (concatenated scans), built before timing
+    batches = []
+    for j in range(steps_per_pass):
+        idx = list(range(j * B, (j + 1) * B))
+        counts = [len(scans[k]) for k in idx]
+        poses = np.stack([w.poses[k] for k in idx])
+        pts = torch.from_numpy(np.concatenate([scans[k] for k in idx])).to(dev) if rank == 0 else None
+        batches.append((pts, counts, poses))
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
     torch.cuda.set_stream(stream)
     L.dbt_profile_enable(sg.local.handle, 1)
 
     def do_step(s):
-        k = s % w.n_scans
-        if rank == 0:
-            pts = dev_scans[k % len(dev_scans)]
-        else:
-            pts = torch.empty((len(scans[k % len(scans)]), 3), dtype=torch.float32, device=f"cuda:{local}")
+        pts, counts, poses = batches[s % steps_per_pass]
+        if rank != 0:
+            pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
         if dist is not None:
             dist.broadcast(pts, 0)
-        sg.integrate_device(bank, pts, [pts.shape[0]], w.poses[k][None], params, stream=stream)
+        sg.integrate_device(bank, pts, counts, poses, params, stream=stream)
 
     for s in range(args.warmup):
-        if s % w.n_scans == 0:
+        if s % steps_per_pass == 0:
             L.dbt_grid_reset(sg.local.handle)
         do_step(s)
     torch.cuda.synchronize()
@@ -265,30 +310,28 @@ def main():
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             s = args.warmup + i
-            if s % w.n_scans == 0:
+            if s % steps_per_pass == 0:
                 L.dbt_grid_reset(sg.local.handle)
             flush.zero_()
             ev[i][0].record(stream)
             do_step(s)
             ev[i][1].record(stream)
-            if (i + 1) % 16 == 0 or i == args.steps - 1:
-                torch.cuda.synchronize()
-            st = sg.stats()[0]
-            applied += st.points_in - st.points_discarded
-            swept += st.unique_centers
-            written += st.voxels_written
-            skipped += st.centers_skipped
+            sts = sg.stats()
+            applied += sum(x.points_in - x.points_discarded for x in sts)
+            swept += sts[0].unique_centers
+            written += sts[0].voxels_written
+            skipped += sts[0].centers_skipped
         torch.cuda.synchronize()
     launches = L.dbt_launch_count() - launches0
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
     if dist is not None:
-        t = torch.tensor([dev_ms], device=f"cuda:{local}")
+        t = torch.tensor([dev_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
         dist.barrier()
     value = applied / (dev_ms / 1e3)
 
-    # per-kernel device time (CUDA events on the launch stream, same region)
+    # per-kernel device time (CUDA events on each kernel's stream, same region)
     names = ctypes.create_string_buffer(32 * 16)
     ms = (ctypes.c_double * 16)()
     cnt = (ctypes.c_int64 * 16)()
@@ -307,18 +350,17 @@ def main():
     achieved = alg_bytes / (sweep["avg_us"] * 1e-6) / 1e9
     # bytes the sweep actually touches (device counters): the 1-byte distance
     # cache over the K^3 cube of every swept centre + word RED.AND and cache
-    # store per lowered voxel; the shadow kernel runs concurrently (8 B RMW
-    # per shadow visit)
+    # store per lowered voxel (the shadow kernel runs concurrently)
     touched = (swept * K_EDGE ** 3 + written * 5) / max(args.steps, 1)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_per_launch.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.config == 2 and B == 1:
         traffic = json.load(open(tpath)).get("sweep_kernel")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w),
+        "config": config_desc(w, B),
         "gpu_launches": int(launches),
         "kernels": kernels,
         "clocks": clk.summary(),
@@ -326,8 +368,9 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes,
                      "alg_bytes_def": f"4*21^3 + 4*|S| = {b_alg(shadow_cells):.0f} B per applied return "
-                                      "(SURVEY.md 8(d)) x applied returns per scan",
-                     "traffic_source": "ncu dram__bytes_read+write per sweep launch, profiles/dram_per_launch.json",
+                                      "(SURVEY.md 8(d)) x applied returns per launch",
+                     "traffic_source": "ncu dram__bytes_read+write per sweep launch (config 2), "
+                                       "profiles/dram_per_launch.json",
                      "touched_bytes_per_launch": touched,
                      "touched_gbs": touched / (sweep["avg_us"] * 1e-6) / 1e9,
                      "why_frac_above_1": "B_alg is the reference's per-return traffic; the engine sweeps each "
@@ -338,9 +381,9 @@ def main():
                      "returns_skipped_per_launch": skipped / max(args.steps, 1)},
     }
 
-    # ---------------- e2e through the public API (rank 0, N=1) --------------
+    # ---------------- e2e through the public API (N=1) ----------------------
     if world == 1:
-        g = new_grid(w.dims, w.voxel_size, w.origin, device=local)
+        g = new_grid(w.dims, w.voxel_size, w.origin, memory_cap=1 << 42, device=local)
         pinned = []
         for s in scans:
             buf = ctypes.c_void_p()
@@ -350,38 +393,31 @@ def main():
             pinned.append((buf, arr))
         e_el, e_pts, h2d = 0.0, 0, 0
         for s in range(args.warmup + args.steps):
-            k = s % w.n_scans
-            if k == 0:
+            j = s % steps_per_pass
+            if j == 0:
                 L.dbt_grid_reset(g.handle)
-            arr = pinned[k % len(pinned)][1]
+            ks = range(j * B, (j + 1) * B)
             if s >= args.warmup:
                 flush.zero_()
                 torch.cuda.synchronize()
             t0 = time.perf_counter()
-            st = integrate_frame(g, bank, ScanFrame(points=arr, pose=w.poses[k]), params)
+            if B == 1:
+                sts = [integrate_frame(g, bank, ScanFrame(points=pinned[j][1], pose=w.poses[j]), params)]
+            else:
+                sts = integrate_frames(g, bank, [ScanFrame(points=pinned[k][1], pose=w.poses[k]) for k in ks],
+                                       params)
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 e_el += dt
-                e_pts += st.points_in - st.points_discarded
-                h2d += arr.nbytes
+                e_pts += sum(x.points_in - x.points_discarded for x in sts)
+                h2d += sum(pinned[k][1].nbytes for k in ks)
         line["e2e"] = {"value": e_pts / e_el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
-                       "d2h_bytes_per_step": 64, "ms_per_step": e_el / args.steps * 1e3,
-                       "api": "paper_2509_20081_b200.integrate_frame (dbt_integrate_frame), pinned float32 scans"}
+                       "d2h_bytes_per_step": 32 + 32 * B, "ms_per_step": e_el / args.steps * 1e3,
+                       "api": ("paper_2509_20081_b200.integrate_frame (dbt_integrate_frame)" if B == 1 else
+                               "paper_2509_20081_b200.integrate_frames (dbt_integrate_batch)")
+                              + ", pinned float32 scans"}
         for buf, _ in pinned:
             L.dbt_host_free(buf)
-        # L2 read bandwidth microbenchmark (context for the L2-resident grid)
-        x = torch.ones(16 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 64 MB, L2 resident
-        x.sum()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(50):
-            x.sum()
-        e1.record()
-        torch.cuda.synchronize()
-        l2 = 50 * x.numel() * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9
-        line["roofline"]["l2_read_gbs_torch_sum"] = l2
-        line["roofline"]["frac_of_l2_read"] = achieved / l2
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, scans)

@@ -100,8 +100,8 @@ DBT_API int dbt_grid_destroy(dbt_grid* g);
 DBT_API int dbt_grid_reset(dbt_grid* g);
 DBT_API int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* device_bytes);
 /* Host C-order (nx,ny,nz) field arrays restricted to the slab, i.e. shape
- * (x1-x0, ny, nz). Masks must be low-bit runs and signs 0/1 (else
- * DBT_ERR_CORRUPTION: the device word stores the run length). */
+ * (x1-x0, ny, nz). Any mask / sign / hits values are stored as is (the device
+ * record is the reference's 8-byte record). */
 DBT_API int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits);
 DBT_API int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits);
 /* Same for the global x-planes [x_begin, x_end) (inside the slab): arrays of

@@ -1,45 +1,37 @@
 // engine.cuh — internal definitions shared by the libdbtsdf CUDA sources.
 //
-// Device voxel word (32 bits, one per voxel, the "single aligned word" every
-// per-voxel update is applied to):
+// Device voxel record (8 bytes, one per voxel): exactly the reference's
+// serialized record (grid.py:30-34) — .x = the 32-bit distance mask,
+// .y = sign (byte 0) | hits (byte 1) << 8 | 0 (2 reserved bytes). The two
+// halves are the single aligned words the two update kinds touch:
+//   * mask update (integrator.py:145-149): one native atomicAnd (RED.AND) of
+//     the kernel's run mask into .x — AND is commutative and idempotent, so
+//     no CAS and no retries;
+//   * shadow update (integrator.py:151-159): a 32-bit CAS on .y applying
+//     h += (h < h_max) and sign = 0 when h >= T.
+// They never touch the same 32-bit word, so concurrent sweeps and shadow
+// updates do not invalidate each other's CAS. Any mask and sign byte the
+// reference can hold is represented (no run-mask assumption).
 //
-//   bits  0..18  T: the low 19 bits of the reference's 32-bit distance mask.
-//                Masks are low-bit runs (grid.py:118-136), so T is a run of
-//                min(L, 19) ones where L = popcount(mask) is the distance.
-//   bits 19..22  E: L - 19 when L >= 19 (0..13), else 0.
-//   bit  23      1 = SIGN_FREE, 0 = SIGN_OCCUPIED (grid.py SIGN_*)
-//   bits 24..31  saturating hit counter (u8)
+// Distance cache: one byte per voxel, dist[v] >= bitlen(mask[v]) at all times
+// (equal after upload/reset), where bitlen = 32 - clz (the popcount for the
+// low-bit run masks integration produces). ANDing run_mask(d) changes a mask
+// exactly when d < bitlen(mask), so the sweep reads the cache (8 voxels per
+// 64-bit load) to find the voxels a return lowers, applies RED.AND to their
+// records and stores d into the cache. Cache stores race only with other
+// lowering stores, so a cache byte can end up stale-high (a later redundant
+// AND) but never below the record: no update is ever lost.
 //
-// Every distance the K<=21 kernel can write is <= ceil(sqrt(3)*10) = 18, so
-// "this return lowers the stored distance to d" is the single bit test
-// (w >> d) & 1, and the update is one native atomicAnd (RED.AND) with
-// 0xFF800000 | ((1 << d) - 1): T becomes the run of min(L, d) ones and E is
-// cleared, exactly the reference's mask AND (integrator.py:145-149) on the
-// encoded word. AND is commutative and idempotent, so no CAS loop and no
-// retries. Hits/sign (|S| cells per return) use a 32-bit CAS.
-//
-// The reference stores mask u32 + sign u8 + hits u8 as three C-order arrays
-// (grid.py:47-49) and serialises 8-byte records (grid.py:30-34); the device
-// word is lossless for every grid the reference can produce (runs; sign 0/1)
-// at half the record size.
-//
-// Distance cache: one byte per voxel, dist[v] >= run length of cells[v] at
-// all times (equal after upload/reset).
-//
-// Stamp certificates: one bit per voxel, set by the warp that swept the
-// stamp centred at that voxel (one writer per bit per launch: centres are
-// deduplicated). A set bit means the full K^3 stamp of that centre is already
-// in the grid; the AND being idempotent, a later return centred there needs
-// no sweep (its shadow update still runs). Cleared on reset/upload and when a
-// launch uses a different distance kernel. The sweep reads it (8 voxels per
-// 64-bit load) to find the voxels a return lowers, then applies RED.AND to
-// the word and stores the new distance into the cache. Cache stores race
-// only with other lowering stores, so a cache byte can end up stale-high
-// (a later redundant AND) but never below the word: no update is ever lost.
+// Stamp certificates: one bit per voxel, set when the full K^3 stamp centred
+// at that voxel is in the grid; the AND being idempotent, a later return
+// centred there needs no sweep (its shadow update still runs). Returns claim
+// the bit with one atomicOr in preprocessing (claim mode) or the sweep sets it
+// after stamping (first-return mode). Cleared on reset/upload and when a
+// launch uses a different distance kernel.
 //
 // Layout in HBM: C-order (x, y, z) like the reference arrays, x restricted to
 // the owned slab [x0, x1), z stride padded to a multiple of 8 voxels so every
-// z-row of the cache starts 8-byte aligned (and of the words 32-byte aligned).
+// z-row of the cache starts 8-byte aligned.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -52,39 +44,20 @@
 
 namespace dbt {
 
-typedef uint32_t cell_t;
-constexpr uint32_t kTMask = 0x7FFFFu;        // run bits 0..18
-constexpr int kTBits = 19;
-constexpr int kEShift = 19;
-constexpr uint32_t kEMask = 0xFu << kEShift;
-constexpr uint32_t kFreeBit = 1u << 23;
-constexpr int kHitsShift = 24;
-constexpr uint32_t kKeepSignHits = 0xFF800000u;  // AND mask bits that a mask update keeps
-constexpr uint32_t kFreshCell = kTMask | (13u << kEShift) | kFreeBit;  // L=32, free, 0 hits
-constexpr int kMaxFastD = 18;                 // kernel distances the RED.AND path handles
+constexpr uint32_t kFullMask = 0xFFFFFFFFu;
+constexpr uint32_t kFreshMeta = 1u;   // sign free (1), 0 hits
+constexpr uint32_t kSignByte = 0xFFu;
+constexpr uint32_t kHitsByte = 0xFF00u;
 constexpr int kCenterBits = 21;                 // packed centre: 3 x 21 bits
 constexpr int64_t kMaxDim = (1 << kCenterBits) - 1;
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kMaxK = 31;          // kernel edge supported by the sweep templates
 constexpr int kMaxScansPerLaunch = 4096;
 
-__host__ __device__ inline int cell_len(uint32_t c) {
-  const uint32_t t = c & kTMask;
-#ifdef __CUDA_ARCH__
-  return t == kTMask ? kTBits + (int)((c >> kEShift) & 0xF) : __popc(t);
-#else
-  return t == kTMask ? kTBits + (int)((c >> kEShift) & 0xF) : __builtin_popcount(t);
-#endif
-}
-// distance run length L (0..32), sign (0/1), hits (0..255) -> word
-__host__ __device__ inline uint32_t make_cell(int len, int free_, uint32_t hits) {
-  const uint32_t t = len >= kTBits ? kTMask : ((1u << len) - 1u);
-  const uint32_t e = len >= kTBits ? (uint32_t)(len - kTBits) : 0u;
-  return t | (e << kEShift) | (free_ ? kFreeBit : 0u) | (hits << kHitsShift);
-}
-__host__ __device__ inline uint32_t cell_with_len(uint32_t c, int len) {
-  return make_cell(len, (c & kFreeBit) ? 1 : 0, c >> kHitsShift);
-}
+__host__ __device__ inline uint32_t make_meta(uint32_t sign, uint32_t hits) { return (sign & 0xFFu) | ((hits & 0xFFu) << 8); }
+__host__ __device__ inline uint8_t meta_sign(uint32_t m) { return (uint8_t)(m & 0xFFu); }
+__host__ __device__ inline uint8_t meta_hits(uint32_t m) { return (uint8_t)((m >> 8) & 0xFFu); }
+__device__ inline int mask_bitlen(uint32_t m) { return 32 - __clz(m); }
 __host__ __device__ inline uint32_t run_mask_of(int len) { return len ? (0xFFFFFFFFu >> (32 - len)) : 0u; }
 
 __host__ __device__ inline uint64_t pack_center(int64_t x, int64_t y, int64_t z) {
@@ -130,7 +103,7 @@ struct dbt_bank {
   uint16_t* d_rowd = nullptr;        // K*K: distinct-row id * CH
   int n_distinct = 0;
   int chunks_per_row = 0;            // CH = ceil((K+7)/8) 8-voxel chunks per kernel row
-  int max_d = 0;                     // largest kernel run length (fast path needs <= 18)
+  int max_d = 0;                     // largest kernel run length
   int8_t* d_shadow_xyz = nullptr;    // total_shadow x 4 (dx,dy,dz,0)
   int32_t* d_shadow_start = nullptr; // n_bins + 1
   uint64_t serial = 0;               // identity for per-grid caches
@@ -142,7 +115,7 @@ struct dbt_grid {
   int64_t nx = 0, ny = 0, nz = 0, nzp = 0;  // global dims, padded z stride
   int64_t x0 = 0, x1 = 0;                   // owned slab
   double vs = 0, org[3] = {0, 0, 0};
-  uint32_t* cells = nullptr;                // authoritative voxel words
+  uint2* cells = nullptr;                   // authoritative voxel records
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
   int64_t n_cells = 0;                      // (x1-x0)*ny*nzp

@@ -30,94 +30,83 @@ namespace {
 
 constexpr int64_t kStageBytes = 256ll << 20;
 
-__global__ void fill_cells_kernel(uint32_t* __restrict__ cells, int64_t n) {
-  // n is a multiple of 4 (allocation is padded); 128-bit stores
-  const uint4 v = make_uint4(kFreshCell, kFreshCell, kFreshCell, kFreshCell);
+__global__ void fill_cells_kernel(uint2* __restrict__ cells, int64_t n) {
+  // n is even (allocation is padded); 128-bit stores of two fresh records
+  const uint4 v = make_uint4(kFullMask, kFreshMeta, kFullMask, kFreshMeta);
   uint4* p = reinterpret_cast<uint4*>(cells);
-  int64_t n4 = n / 4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+  int64_t n2 = n / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
 
-// Host C-order slice (xs, ny, nz) of mask/sign/hits -> device words.
-// Validates the run-mask invariant (grid.py:118-121: (m & (m+1)) == 0, i.e.
-// popc(m) + clz(m) == 32) and sign in {0,1}.
-__global__ void encode_kernel(uint32_t* __restrict__ cells, const uint32_t* __restrict__ mask,
+// Host C-order slice (xs, ny, nz) of mask/sign/hits -> device records. Any
+// mask and sign byte the reference can hold is stored as is.
+__global__ void encode_kernel(uint2* __restrict__ cells, const uint32_t* __restrict__ mask,
                               const uint8_t* __restrict__ sign, const uint8_t* __restrict__ hits,
-                              int64_t n, int64_t nz, int64_t nzp, int* __restrict__ err) {
+                              int64_t n, int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t m = mask[i];
-    int pc = __popc(m);
-    uint8_t s = sign[i];
-    if (pc + __clz(m) != 32 || s > 1) {
-      atomicOr(err, pc + __clz(m) != 32 ? 1 : 2);
-      continue;
-    }
     int64_t row = i / nz, z = i - row * nz;
-    cells[row * nzp + z] = make_cell(pc, s, hits[i]);
+    cells[row * nzp + z] = make_uint2(mask[i], make_meta(sign[i], hits[i]));
   }
 }
 
-
-// dist[v] = run length of cells[v] over the whole slab (after host writes)
-__global__ void rebuild_dist_kernel(const uint32_t* __restrict__ cells, uint8_t* __restrict__ dist, int64_t n) {
+// dist[v] = bit length of the mask of cells[v] over the whole slab (after host writes)
+__global__ void rebuild_dist_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ dist, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    dist[i] = (uint8_t)cell_len(cells[i]);
+    dist[i] = (uint8_t)mask_bitlen(cells[i].x);
 }
 
-__global__ void decode_kernel(const uint32_t* __restrict__ cells, uint32_t* __restrict__ mask,
+__global__ void decode_kernel(const uint2* __restrict__ cells, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits, int64_t n,
                               int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    uint32_t c = cells[row * nzp + z];
-    mask[i] = run_mask_of(cell_len(c));
-    sign[i] = (c & kFreeBit) ? 1 : 0;
-    hits[i] = (uint8_t)(c >> kHitsShift);
+    const uint2 c = cells[row * nzp + z];
+    mask[i] = c.x;
+    sign[i] = meta_sign(c.y);
+    hits[i] = meta_hits(c.y);
   }
 }
 
 // Readout (grid.py:161-175). mode 0: popcount int32; 1: observed u8;
-// 2: signed distance f64 (+ observed u8).
-__global__ void readout_kernel(const uint32_t* __restrict__ cells, int mode, int32_t* __restrict__ pop,
+// 2: signed distance f64 (+ observed u8). Decode = __popc of the mask
+// (grid.py:124-129, 166-167).
+__global__ void readout_kernel(const uint2* __restrict__ cells, int mode, int32_t* __restrict__ pop,
                                uint8_t* __restrict__ obs, double* __restrict__ sdf, double vs,
                                int64_t n, int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    uint32_t c = cells[row * nzp + z];
-    // decode = popcount of the run mask; the run check is popc + clz == 32
-    uint32_t m = run_mask_of(cell_len(c));
-    int len = __popc(m);
-    int hits = c >> kHitsShift;
+    const uint2 c = cells[row * nzp + z];
+    const int len = __popc(c.x);
     if (mode == 0) {
       pop[i] = len;
     } else {
-      uint8_t observed = !(m == 0xFFFFFFFFu && hits == 0);
-      obs[i] = observed;
+      obs[i] = !(c.x == kFullMask && meta_hits(c.y) == 0);
       if (mode == 2) {
-        // sigma * (popcount * voxel_size), sigma = -1 for occupied: keeps -0.0
+        // sigma * (popcount * voxel_size), sigma = -1 where sign == occupied:
+        // keeps -0.0 like numpy
         double dist = __dmul_rn((double)len, vs);
-        double sigma = (c & kFreeBit) ? 1.0 : -1.0;
+        double sigma = meta_sign(c.y) == 0 ? -1.0 : 1.0;
         sdf[i] = __dmul_rn(sigma, dist);
       }
     }
   }
 }
 
-__global__ void count_kernel(const uint32_t* __restrict__ cells, int64_t n, int64_t nz, int64_t nzp,
+__global__ void count_kernel(const uint2* __restrict__ cells, int64_t n, int64_t nz, int64_t nzp,
                              unsigned long long* __restrict__ out) {
   unsigned long long obs = 0, occ = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    uint32_t c = cells[row * nzp + z];
-    obs += !(cell_len(c) == 32 && (c >> kHitsShift) == 0);
-    occ += !(c & kFreeBit);
+    const uint2 c = cells[row * nzp + z];
+    obs += !(c.x == kFullMask && meta_hits(c.y) == 0);
+    occ += meta_sign(c.y) == 0;
   }
   for (int o = 16; o; o >>= 1) {
     obs += __shfl_xor_sync(0xffffffffu, obs, o);
@@ -130,51 +119,41 @@ __global__ void count_kernel(const uint32_t* __restrict__ cells, int64_t n, int6
 }
 
 // F-order record transpose (grid.py:178-185): records of iz slab [z0, z0+zc)
-// rec[(iz-z0)*nx*ny + iy*nx + ix] <- cell(ix, iy, iz). Tile 32 (x) x 32 (z)
-// per block at fixed iy so both the cell reads (along z) and the record
-// writes (along x) are coalesced.
-__global__ void to_records_kernel(const uint32_t* __restrict__ cells, uint64_t* __restrict__ rec,
-                                  int64_t nx, int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
-  __shared__ uint32_t tile[32][33];
+// rec[(iz-z0)*nx*ny + iy*nx + ix] <- cell(ix, iy, iz). The device record IS
+// the serialized record (reserved bytes 0); tile 32 (x) x 32 (z) per block at
+// fixed iy so both the cell reads (along z) and the record writes (along x)
+// are coalesced.
+__global__ void to_records_kernel(const uint2* __restrict__ cells, uint2* __restrict__ rec, int64_t nx,
+                                  int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
+  __shared__ uint2 tile[32][33];
   int64_t iy = blockIdx.y;
   int64_t xb = blockIdx.x * 32, zb = blockIdx.z * 32;
   int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int k = ty; k < 32; k += 8) {
     int64_t ix = xb + k, iz = zb + tx;
-    uint32_t v = 0;
+    uint2 v = make_uint2(0, 0);
     if (ix < nx && iz < zc) v = cells[(ix * ny + iy) * nzp + z0 + iz];
     tile[k][tx] = v;
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     int64_t iz = zb + k, ix = xb + tx;
-    if (ix < nx && iz < zc) {
-      uint32_t c = tile[tx][k];
-      uint64_t r = (uint64_t)run_mask_of(cell_len(c)) | ((uint64_t)((c & kFreeBit) ? 1 : 0) << 32) |
-                   ((uint64_t)(c >> kHitsShift) << 40);
-      rec[iz * nx * ny + iy * nx + ix] = r;
-    }
+    if (ix < nx && iz < zc) rec[iz * nx * ny + iy * nx + ix] = tile[tx][k];
   }
 }
 
-__global__ void from_records_kernel(uint32_t* __restrict__ cells, const uint64_t* __restrict__ rec,
-                                    int64_t nx, int64_t ny, int64_t nzp, int64_t z0, int64_t zc,
-                                    int* __restrict__ err) {
-  __shared__ uint32_t tile[32][33];
+__global__ void from_records_kernel(uint2* __restrict__ cells, const uint2* __restrict__ rec, int64_t nx,
+                                    int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
+  __shared__ uint2 tile[32][33];
   int64_t iy = blockIdx.y;
   int64_t xb = blockIdx.x * 32, zb = blockIdx.z * 32;
   int tx = threadIdx.x, ty = threadIdx.y;
   for (int k = ty; k < 32; k += 8) {
     int64_t iz = zb + k, ix = xb + tx;
-    uint32_t v = 0;
+    uint2 v = make_uint2(0, 0);
     if (ix < nx && iz < zc) {
-      uint64_t r = rec[iz * nx * ny + iy * nx + ix];
-      uint32_t m = (uint32_t)r;
-      uint32_t s = (uint32_t)(r >> 32) & 0xFF;
-      uint32_t h = (uint32_t)(r >> 40) & 0xFF;
-      int pc = __popc(m);
-      if (pc + __clz(m) != 32 || s > 1) atomicOr(err, pc + __clz(m) != 32 ? 1 : 2);
-      v = make_cell(pc, s ? 1 : 0, h);
+      v = rec[iz * nx * ny + iy * nx + ix];
+      v.y &= 0xFFFFu;  // reserved bytes are ignored (grid.py:188-202)
     }
     tile[tx][k] = v;
   }
@@ -185,15 +164,15 @@ __global__ void from_records_kernel(uint32_t* __restrict__ cells, const uint64_t
   }
 }
 
-__global__ void gather_kernel(const uint32_t* __restrict__ cells, const int64_t* __restrict__ xyz, int64_t n,
+__global__ void gather_kernel(const uint2* __restrict__ cells, const int64_t* __restrict__ xyz, int64_t n,
                               int64_t x0, int64_t ny, int64_t nzp, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t c = cells[((xyz[3 * i] - x0) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
-    mask[i] = run_mask_of(cell_len(c));
-    sign[i] = (c & kFreeBit) ? 1 : 0;
-    hits[i] = (uint8_t)(c >> kHitsShift);
+    const uint2 c = cells[((xyz[3 * i] - x0) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
+    mask[i] = c.x;
+    sign[i] = meta_sign(c.y);
+    hits[i] = meta_hits(c.y);
   }
 }
 
@@ -207,22 +186,9 @@ int check_grid(const dbt_grid* g) {
   return grid_set_device(g);
 }
 
-int check_upload_error(dbt_grid* g) {
-  int err = 0;
-  DBT_CUDA(cudaMemcpyAsync(&err, &g->d_lcnt->error, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
-  DBT_CUDA(cudaStreamSynchronize(g->stream));
-  if (err) {
-    // leave the grid fresh rather than half-written
-    fill_cells_kernel<<<grid_blocks(g->n_cells / 4), 256, 0, g->stream>>>(g->cells, g->n_cells);
-    DBT_CHECK_LAUNCH("fill_cells_kernel");
-    DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)g->n_cells, g->stream));
-    DBT_CUDA(cudaStreamSynchronize(g->stream));
-    if (err & 1)
-      return set_error(DBT_ERR_CORRUPTION,
-                       "distance mask is not a low-bit run (grid.py:118-129); the device word "
-                       "stores the run length");
-    return set_error(DBT_ERR_CORRUPTION, "sign byte outside {0 (occupied), 1 (free)}");
-  }
+// after host data replaced the records: rebuild the distance cache, drop
+// every stamp certificate (host writes carry no stamp history)
+int finish_host_write(dbt_grid* g) {
   rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
@@ -264,7 +230,7 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   }
   // +64 cells of slack: the sweep's aligned 4-cell chunks may read up to 3
   // cells past the last row of the slab (never written).
-  cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint32_t));
+  cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint2));
   if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
   if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cells + 63) / 32) * 4);
   if (e != cudaSuccess) {
@@ -331,7 +297,7 @@ int dbt_grid_destroy(dbt_grid* g) {
 int dbt_grid_reset(dbt_grid* g) {
   int rc = check_grid(g);
   if (rc) return rc;
-  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
+  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 2), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
   DBT_CHECK_LAUNCH("fill_cells_kernel");
   DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
@@ -347,7 +313,7 @@ int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* 
   dims[2] = g->nz;
   slab[0] = g->x0;
   slab[1] = g->x1;
-  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint32_t) + 1);
+  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint2) + 1) + (g->n_cells + 63) / 32 * 4;
   return DBT_OK;
 }
 
@@ -358,7 +324,6 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
-  DBT_CUDA(cudaMemsetAsync(&g->d_lcnt->error, 0, sizeof(int), g->stream));
   uint8_t* st = (uint8_t*)g->d_stage;
   for (int64_t x = 0; x < lx; x += xs) {
     int64_t cx = std::min(xs, lx - x), n = cx * plane;
@@ -369,10 +334,10 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
     DBT_CUDA(cudaMemcpyAsync(ds, sign + x * plane, n, cudaMemcpyHostToDevice, g->stream));
     DBT_CUDA(cudaMemcpyAsync(dh, hits + x * plane, n, cudaMemcpyHostToDevice, g->stream));
     encode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, dm, ds, dh, n,
-                                                         g->nz, g->nzp, &g->d_lcnt->error);
+                                                         g->nz, g->nzp);
     DBT_CHECK_LAUNCH("encode_kernel");
   }
-  return check_upload_error(g);
+  return finish_host_write(g);
 }
 
 int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
@@ -497,7 +462,7 @@ int dbt_grid_to_records(dbt_grid* g, void* out_records) {
   int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
   if (rc) return rc;
-  uint64_t* st = (uint64_t*)g->d_stage;
+  uint2* st = (uint2*)g->d_stage;
   for (int64_t z = 0; z < g->nz; z += zs) {
     int64_t zc = std::min(zs, g->nz - z);
     dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
@@ -520,19 +485,17 @@ int dbt_grid_from_records(dbt_grid* g, const void* records) {
   int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
   if (rc) return rc;
-  DBT_CUDA(cudaMemsetAsync(&g->d_lcnt->error, 0, sizeof(int), g->stream));
-  uint64_t* st = (uint64_t*)g->d_stage;
+  uint2* st = (uint2*)g->d_stage;
   for (int64_t z = 0; z < g->nz; z += zs) {
     int64_t zc = std::min(zs, g->nz - z);
     DBT_CUDA(cudaMemcpyAsync(st, (const uint64_t*)records + z * plane, zc * plane * 8,
                              cudaMemcpyHostToDevice, g->stream));
     dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
-    from_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc,
-                                                             &g->d_lcnt->error);
+    from_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc);
     DBT_CHECK_LAUNCH("from_records_kernel");
     DBT_CUDA(cudaStreamSynchronize(g->stream));
   }
-  return check_upload_error(g);
+  return finish_host_write(g);
 }
 
 }  // extern "C"

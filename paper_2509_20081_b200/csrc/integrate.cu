@@ -9,10 +9,11 @@
 //                  (integrator.py:256-262), per-scan counters.
 //   shadow_kernel  one thread per (applied return, shadow offset): saturating
 //                  hit increment + occupied sign (integrator.py:151-159) as a
-//                  16-bit CAS on the voxel word.
-//   sweep_kernel   one warp per unique centre voxel: the K^3 AND sweep
-//                  (integrator.py:145-149) as min(run length, d) with 64-bit
-//                  (4-voxel) loads, skip-if-unchanged, CAS only on change.
+//                  32-bit CAS on the record's sign/hits word; runs on a second
+//                  stream, concurrent with the sweep.
+//   sweep_kernel   one warp per centre to sweep: the K^3 AND (integrator.py:
+//                  145-149) over the 1-byte distance cache, RED.AND of the
+//                  kernel run mask into the record's mask word on change.
 //
 // Order independence: every voxel update is an atomic application of a
 // monotone function (min on the run length; h -> h + (h < h_max) with the
@@ -76,7 +77,7 @@ struct PrepArgs {
   uint64_t epoch;      // hash-key epoch tag (bits 52..63); stale slots count as empty
   // fused shadow update (no first-return, small shadow sets)
   int fuse_shadow;
-  uint32_t* cells;
+  uint2* cells;
   const int8_t* sxyz;
   const int32_t* sstart;
   int64_t x0, x1, nzp;
@@ -91,15 +92,20 @@ constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
 constexpr int kEpochShift = 52;
 constexpr uint32_t kMaxEpoch = 4095;
 
-// h += (h < h_max); sign <- occupied when h >= T (integrator.py:154-159) as a
-// 32-bit CAS on the voxel word
+// one shadow visit on a record's sign/hits word (integrator.py:154-159):
+// h += (h < h_max); sign byte <- 0 (occupied) when the new h >= T
+__device__ __forceinline__ uint32_t shadow_step(uint32_t old, uint32_t h_max, uint32_t t_occ) {
+  const uint32_t h = (old >> 8) & 0xFFu;
+  const uint32_t hn = h + (h < h_max ? 1u : 0u);
+  uint32_t nw = (old & ~kHitsByte) | (hn << 8);
+  if (hn >= t_occ) nw &= ~kSignByte;
+  return nw;
+}
+
 __device__ __forceinline__ void shadow_update(uint32_t* p, uint32_t h_max, uint32_t t_occ) {
   uint32_t old = *p;
   while (true) {
-    uint32_t h = old >> kHitsShift;
-    uint32_t hn = h + (h < h_max ? 1u : 0u);
-    uint32_t nw = (old & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
-    if (hn >= t_occ) nw &= ~kFreeBit;
+    const uint32_t nw = shadow_step(old, h_max, t_occ);
     if (nw == old) break;
     uint32_t prev = atomicCAS(p, old, nw);
     if (prev == old) break;
@@ -273,7 +279,8 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
           if (k < nsh) {
             const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
             const int64_t gx = cx + o.x;
-            if (gx >= a.x0 && gx < a.x1) ptr[k] = a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z);
+            if (gx >= a.x0 && gx < a.x1)
+              ptr[k] = &a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y;
           }
           old[k] = ptr[k] ? __ldcg(ptr[k]) : 0u;
         }
@@ -281,10 +288,7 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
         for (int k = 0; k < 8; ++k) {
           prev[k] = old[k];
           if (!ptr[k]) continue;
-          const uint32_t h = old[k] >> kHitsShift;
-          const uint32_t hn = h + (h < (uint32_t)a.h_max ? 1u : 0u);
-          uint32_t nw = (old[k] & ~(0xFFu << kHitsShift)) | (hn << kHitsShift);
-          if (hn >= (uint32_t)a.t_occ) nw &= ~kFreeBit;
+          const uint32_t nw = shadow_step(old[k], (uint32_t)a.h_max, (uint32_t)a.t_occ);
           if (nw != old[k]) prev[k] = atomicCAS(ptr[k], old[k], nw);
         }
 #pragma unroll
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
 }
 
 struct ShadowArgs {
-  uint32_t* cells;
+  uint2* cells;
   const uint64_t* center;
   const uint16_t* bin;
   const uint32_t* slot;
@@ -369,13 +373,13 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     unpack_center(c, cx, cy, cz);
     int64_t gx = cx + o.x;
     if (gx < a.x0 || gx >= a.x1) continue;
-    shadow_update(a.cells + ((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z), (uint32_t)a.h_max,
+    shadow_update(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
                   (uint32_t)a.t_occ);
   }
 }
 
 struct SweepArgs {
-  uint32_t* cells;
+  uint2* cells;
   uint8_t* dist;
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
@@ -390,17 +394,6 @@ struct SweepArgs {
   int certify;        // hash mode: set the certificate after sweeping (claim mode set it)
 };
 
-// Lower cell p to run length d (generic path, any d in 0..32): CAS on the word.
-__device__ __forceinline__ int lower_cas(uint32_t* p, int d) {
-  uint32_t old = *p;
-  while (cell_len(old) > d) {
-    uint32_t prev = atomicCAS(p, old, cell_with_len(old, d));
-    if (prev == old) return 1;
-    old = prev;
-  }
-  return 0;
-}
-
 constexpr int kSweepUnroll = 4;
 
 // Warp per unique centre. Chunks of 8 voxels along z, row-major over the
@@ -408,12 +401,11 @@ constexpr int kSweepUnroll = 4;
 // loads of the distance cache depending on the centre's z alignment. Each
 // lane issues kSweepUnroll independent loads before testing any of them (the
 // updates below could alias later loads, so the compiler would not hoist
-// them). A byte lane with d < cached distance marks a voxel this return
-// lowers: RED.AND on its word (FAST: every kernel distance <= 18, where the
-// update is the AND with 0xFF800000 | ((1 << d) - 1); otherwise a CAS), then
-// the new distance goes to the cache. Stale cache reads (L1) only cause
-// redundant updates, never missed ones (cache >= word, see engine.cuh).
-template <int CH, bool FAST>
+// them). A byte lane with d < cached bit length marks a voxel this return
+// lowers: RED.AND of run_mask(d) into its record's mask word, then d goes to
+// the cache. Stale cache reads (L1) only cause redundant ANDs, never missed
+// ones (cache >= bit length of the mask, see engine.cuh).
+template <int CH>
 __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int rows = a.K * a.K;
@@ -486,13 +478,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
             const uint32_t lt = b < 4 ? lt0 : lt1;
             if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
             const uint32_t d = (((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-            uint32_t* cp = a.cells + off[k] + b;
-            if (FAST) {
-              atomicAnd(cp, kKeepSignHits | ((1u << d) - 1u));
-              ++changed;
-            } else {
-              changed += lower_cas(cp, (int)d);
-            }
+            atomicAnd(&a.cells[off[k] + b].x, run_mask_of((int)d));  // RED.AND, fire and forget
+            ++changed;
             a.dist[off[k] + b] = (uint8_t)d;
           }
         }
@@ -509,23 +496,17 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 
 typedef void (*SweepFn)(SweepArgs);
 
-template <bool FAST>
-SweepFn sweep_fn_t(int CH) {
+SweepFn sweep_fn(int CH) {
   switch (CH) {
-    case 1: return sweep_kernel<1, FAST>;
-    case 2: return sweep_kernel<2, FAST>;
-    case 3: return sweep_kernel<3, FAST>;
-    case 4: return sweep_kernel<4, FAST>;
-    case 5: return sweep_kernel<5, FAST>;
-    case 6: return sweep_kernel<6, FAST>;
-    case 7: return sweep_kernel<7, FAST>;
-    case 8: return sweep_kernel<8, FAST>;
-    case 9: return sweep_kernel<9, FAST>;
+    case 1: return sweep_kernel<1>;
+    case 2: return sweep_kernel<2>;
+    case 3: return sweep_kernel<3>;
+    case 4: return sweep_kernel<4>;
+    case 5: return sweep_kernel<5>;
+    case 6: return sweep_kernel<6>;
   }
   return nullptr;
 }
-
-SweepFn sweep_fn(int CH, bool fast) { return fast ? sweep_fn_t<true>(CH) : sweep_fn_t<false>(CH); }
 
 size_t sweep_smem_bytes(int K, int CH, int nd) {
   return (size_t)8 * nd * CH * sizeof(uint2) + (size_t)K * K * sizeof(int2);
@@ -833,11 +814,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
 
   const int CH = b->chunks_per_row;
-  const bool fast = b->max_d <= kMaxFastD;
-  SweepFn fn = sweep_fn(CH, fast);
+  SweepFn fn = sweep_fn(CH);
   if (!fn) return set_error(DBT_ERR_CONFIG, "unsupported kernel size for the sweep");
   const size_t smem = sweep_smem_bytes(b->K, CH, b->n_distinct);
-  const int shape_key = CH * 2 + (fast ? 1 : 0);
+  const int shape_key = CH;
   if (g->sweep_ch != shape_key) {
     DBT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // keep shared memory to what 8 resident blocks need; the rest stays L1

@@ -115,6 +115,15 @@ def small_cases() -> list:
         cases.append(Case(f"nonfresh_{model}_h{hm}_t{t}", dims, 0.1, (0, 0, 0),
                           dict(size=21, shadow_radius=3 if model == "cone" else 2, shadow_model=model,
                                cone_half_angle_deg=40.0), {"h_max": hm, "t_occ": t}, frames, init=init))
+    # arbitrary state the reference accepts: any 32-bit mask (not only low-bit
+    # runs), any sign byte, any hit count
+    rng = np.random.default_rng(77)
+    dims = (48, 48, 48)
+    init = (rng.integers(0, 2**32, size=dims, dtype=np.uint64).astype(np.uint32),
+            rng.integers(0, 256, size=dims).astype(np.uint8), rng.integers(0, 256, size=dims).astype(np.uint8))
+    frames = [(rng.uniform(1.15, 3.6, size=(300, 3)), yaw_pose(0.2 * k, (0.03 * k, 0.0, 0.0))) for k in range(2)]
+    cases.append(Case("arbitrary_state", dims, 0.1, (0, 0, 0), dict(size=21, shadow_radius=2), {"h_max": 250, "t_occ": 4},
+                      frames, init=init))
     # other kernel sizes
     rng = np.random.default_rng(41)
     p = rng.uniform(0.45, 2.75, size=(300, 3))
