@@ -56,6 +56,8 @@ extern "C" {
                                         (measurement only; identical grid) */
 #define DBT_FLAG_FUSE_SHADOW 16u     /* shadow update fused into preprocessing instead of
                                         a kernel concurrent with the sweep (measurement) */
+#define DBT_FLAG_GENERIC_SWEEP 32u   /* distinct-row sweep even for a symmetric kernel
+                                        (measurement; identical grid) */
 
 typedef struct dbt_grid dbt_grid; /* device-resident VoxelGrid (grid.py:39-58) */
 typedef struct dbt_bank dbt_bank; /* device copy of a KernelBank (kernels.py:122-141) */

@@ -9,6 +9,8 @@
 //    that row, the 8 run lengths + 1 packed into a uint2 (64 marks a voxel
 //    outside the kernel, which can never lower a distance <= 32), plus the
 //    row -> distinct-row map;
+//  * whether the kernel is isotropic (run length a non-decreasing function
+//    of |o|^2), which licenses the culling sweep;
 //  * the shadow table in CSR form, offsets as int8 (|o| <= R <= 15).
 #include <algorithm>
 #include <cstring>
@@ -72,6 +74,26 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
         }
         dtab[((size_t)s * nd + q) * CH + c] = make_uint2(v[0], v[1]);
       }
+  // isotropic kernel: run length = h(|o|^2) with h non-decreasing (the
+  // culling sweep's premise; every bank build_kernel_bank makes)
+  bool iso = CH <= 4;
+  {
+    std::vector<int> h(3 * R * R + 1, -1);
+    for (int dx = -R; dx <= R && iso; ++dx)
+      for (int dy = -R; dy <= R && iso; ++dy)
+        for (int dz = -R; dz <= R && iso; ++dz) {
+          const int q = dx * dx + dy * dy + dz * dz;
+          const int l = len[((size_t)(dx + R) * K + (dy + R)) * K + (dz + R)];
+          if (h[q] < 0) h[q] = l;
+          else if (h[q] != l) iso = false;
+        }
+    int prev = -1;
+    for (size_t q = 0; q < h.size() && iso; ++q)
+      if (h[q] >= 0) {
+        if (h[q] < prev) iso = false;
+        prev = h[q];
+      }
+  }
   std::vector<uint16_t> rowd(rows);
   for (int r = 0; r < rows; ++r) rowd[r] = (uint16_t)(rowid[r] * CH);
   const int nb = b_az * b_el;
@@ -103,6 +125,7 @@ int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint32_t* di
   b->chunks_per_row = CH;
   b->max_d = max_d;
   b->n_distinct = nd;
+  b->iso = iso ? 1 : 0;
   uint64_t hsh = 1469598103934665603ull ^ (uint64_t)K;
   for (int i = 0; i < K3; ++i) hsh = (hsh ^ len[i]) * 1099511628211ull;
   b->dk_hash = hsh | 1;

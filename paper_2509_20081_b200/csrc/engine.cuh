@@ -82,8 +82,7 @@ struct LaunchCounters {
   unsigned long long n_unique;   // unique centre keys (sweep work items)
   unsigned long long changed;    // mask cells changed (voxels_written)
   unsigned long long skipped;    // centres whose stamp was already applied (cache byte 0)
-  int error;                     // upload validation etc.
-  int pad;
+  unsigned long long work;       // sweep work-item cursor (dynamic fetch)
 };
 
 struct ProfEvent {
@@ -104,6 +103,8 @@ struct dbt_bank {
   int n_distinct = 0;
   int chunks_per_row = 0;            // CH = ceil((K+7)/8) 8-voxel chunks per kernel row
   int max_d = 0;                     // largest kernel run length
+  int iso = 0;                       // run length = h(|o|^2), h non-decreasing, CH <= 4:
+                                     // sweep_cull_kernel (neighbour-dominance culling)
   int8_t* d_shadow_xyz = nullptr;    // total_shadow x 4 (dx,dy,dz,0)
   int32_t* d_shadow_start = nullptr; // n_bins + 1
   uint64_t serial = 0;               // identity for per-grid caches

@@ -22,6 +22,7 @@
 // (integrator.py:266-284) for any schedule. Duplicate centres stamp the same
 // mask (AND is idempotent), so the sweep runs once per distinct centre.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -246,19 +247,23 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
           append = true;
         }
       }
+      // the hash table dedups centres for the sweep when certificates are not
+      // used (measurement flags) and picks the first return per centre for
+      // the shadow update in first-return mode
+      const bool use_hash = !a.claim || a.first_return;
       uint64_t key = (uint64_t)((cx * a.ny + cy) * a.nz + cz);
       if (a.key_scan_bits) key |= (uint64_t)s << 40;
       uint64_t h = mix64(key) & a.hmask;
       key |= a.epoch;
       if (!a.claim) append = a.no_dedup != 0;
-      unsigned long long cur = a.claim ? 0ull : __ldcg(&a.hkey[h]);
-      while (!a.claim) {
+      unsigned long long cur = use_hash ? __ldcg(&a.hkey[h]) : 0ull;
+      while (use_hash) {
         if (cur == key) break;  // centre already inserted this launch
         if ((cur & ~kKeyMask) != a.epoch) {
           // slot is empty for this launch (older epoch): claim it
           unsigned long long prev = atomicCAS(&a.hkey[h], cur, (unsigned long long)key);
           if (prev == cur) {
-            if (!a.no_dedup) append = true;
+            if (!a.claim && !a.no_dedup) append = true;
             break;
           }
           cur = prev;  // lost the race: re-examine the same slot
@@ -389,9 +394,6 @@ struct SweepArgs {
   const int32_t* rowoff;  // [rows]
   int K, R, nd;
   int64_t x0, x1, ny, nzp;
-  uint32_t* stamped;  // stamp certificate bits
-  int skip_stamped;   // hash mode: skip centres whose stamp is certified as applied
-  int certify;        // hash mode: set the certificate after sweeping (claim mode set it)
 };
 
 constexpr int kSweepUnroll = 4;
@@ -423,18 +425,11 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
   const int64_t hi = min(lo + per, n_unique);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  unsigned long long changed = 0, skipped = 0;
+  unsigned long long changed = 0;
 
   for (int64_t u = lo + warp; u < hi; u += nwarps) {
     int64_t cx, cy, cz;
     unpack_center(a.uniq[u], cx, cy, cz);
-    // the stamp centred here is certified as applied: nothing to sweep
-    const bool own = cx >= a.x0 && cx < a.x1;
-    const int64_t cidx = ((cx - a.x0) * a.ny + cy) * a.nzp + cz;
-    if (own && a.skip_stamped && ((__ldcg(a.stamped + (cidx >> 5)) >> (cidx & 31)) & 1u)) {
-      if (lane == 0) ++skipped;
-      continue;
-    }
     const int64_t zs = cz - a.R;  // >= 0: boundary discard guarantees it
     const int sh = (int)(zs & 7);
     // chunks this alignment needs per row (3 or 4 for K = 21); j -> row by a
@@ -485,13 +480,214 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
         }
       }
     }
-    // every lane's updates for this centre are issued: certify the stamp
-    __syncwarp();
-    if (own && a.certify && lane == 0) atomicOr(a.stamped + (cidx >> 5), 1u << (cidx & 31));
   }
   for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
   if (lane == 0 && changed) atomicAdd(a.changed_out, changed);
-  if (lane == 0 && skipped) atomicAdd(a.changed_out + 1, skipped);
+}
+
+// Culling sweep for isotropic kernels (run length = h(|o|^2), h
+// non-decreasing: every bank build_kernel_bank makes). A centre c may skip
+// voxel v when a neighbour centre e = c + delta (|delta|_inf = 1) whose stamp
+// is applied or claimed (certificate bit set) covers v (v in e's K^3 window)
+// and is strictly closer in real distance, |v - e| < |v - c|, i.e.
+// 2 (v - c).delta > |delta|^2: then h(|v-e|^2) <= h(|v-c|^2), so e's AND
+// already implies c's at v. Following "skips because of" strictly decreases
+// the real distance to v, so the chain ends at a centre that does sweep v
+// with a run length <= c's: the grid is exactly the unculled one. The
+// certificate bits are static during the sweep (set by prep), so the rule is
+// race-free.
+//
+// Per centre the surviving region is, for each kernel x-offset dx (lane), a
+// dy interval (neighbours with delta_z = 0 cut whole rows) and per row a dz
+// interval (delta_z = +-1 neighbours cut z prefixes/suffixes). A block takes
+// 8 centres at a time: phase A, one warp per centre, compacts the surviving
+// rows into a shared-memory queue of row tasks (row start, chunk range,
+// d-table row); phase B, the whole block, sweeps the queued rows one thread
+// per row (1-4 chunk loads in flight each), testing them as sweep_kernel
+// does. Rows of a heavy centre (a fresh surface: nothing culled) thus spread
+// over 256 threads instead of serialising one warp.
+struct CullArgs {
+  uint2* cells;
+  uint8_t* dist;
+  const uint64_t* uniq;
+  LaunchCounters* lc;
+  const uint2* dtab;     // [8][nd][CH]
+  const uint16_t* rowd;  // [K*K] distinct id * CH
+  const uint32_t* stamped;
+  int K, R, nd, CH;
+  int64_t x0, x1, ny, nzp;
+};
+
+constexpr int kFar = 1 << 20;
+constexpr int kCullWarps = 8;  // centres per block batch (one per warp)
+
+// row task: bits 0-36 row start / 8 (cells), 37-38 first chunk, 39-40 last
+// chunk, 41-54 d-table row offset
+__device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int drow) {
+  return (uint64_t)(rbase >> 3) | ((uint64_t)c0 << 37) | ((uint64_t)c1 << 39) | ((uint64_t)drow << 41);
+}
+
+__global__ void __launch_bounds__(256) sweep_cull_kernel(CullArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw);  // kCullWarps * K * K
+  __shared__ int q_n;
+  __shared__ long long batch0, batch_next;
+  // the d-table (17 KB for K = 21) is read through L1 (__ldg), not staged
+  const uint2* dtab = a.dtab;
+  const uint16_t* rowd = a.rowd;
+  if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int R = a.R, K = a.K;
+  const int64_t n_items = (int64_t)a.lc->n_unique;
+  const int64_t sx = a.ny * a.nzp;
+  unsigned long long changed = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      batch0 = batch_next;
+      q_n = 0;
+    }
+    __syncthreads();
+    const int64_t item = batch0 + warp;
+    if (batch0 >= n_items) break;
+    if (item < n_items) {
+      // ===== phase A: this warp's centre -> surviving row tasks =====
+      int64_t cx, cy, cz;
+      unpack_center(a.uniq[item], cx, cy, cz);
+      // neighbour certificates: 27 bits, bit (a+1)*9 + (b+1)*3 + (c+1)
+      uint32_t nb3 = 0;
+      if (lane < 9) {
+        const int na = lane / 3 - 1, nbb = lane % 3 - 1;
+        const int64_t gx = cx + na;
+        if (gx >= a.x0 && gx < a.x1) {
+          const int64_t idx = ((gx - a.x0) * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
+          const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+          const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+          nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
+        }
+      }
+      const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
+#define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
+      // per lane: kernel x-offset dx, its dy interval and z-cut terms
+      const int dx = lane - R;
+      const int64_t gx = cx + dx;
+      bool dead = lane >= K || gx < a.x0 || gx >= a.x1;
+      int ylo = -R, yhi = R;
+      int mp[3] = {kFar, kFar, kFar}, mm[3] = {-kFar, -kFar, -kFar};  // index b + 1
+#pragma unroll
+      for (int na = -1; na <= 1; ++na) {
+        const bool xw = na == 0 || (na > 0 ? dx >= -R + 1 : dx <= R - 1);  // v in e's x-window
+        if (!xw) continue;
+        const int s = na * dx;
+        if (na != 0 && NB(na, 0, 0) && s >= 1) dead = true;  // delta_z = 0: whole rows
+        const int t2 = na == 0 ? 1 : 2;                     // floor(|delta|^2 / 2) + 1
+        if (NB(na, 1, 0)) yhi = min(yhi, max(t2 - s, -R + 1) - 1);
+        if (NB(na, -1, 0)) ylo = max(ylo, min(s - t2, R - 1) + 1);
+#pragma unroll
+        for (int b = -1; b <= 1; ++b) {
+          const int t3 = (na * na + b * b + 1) / 2 + 1;
+          if (NB(na, b, 1)) mp[b + 1] = min(mp[b + 1], t3 - s);
+          if (NB(na, b, -1)) mm[b + 1] = max(mm[b + 1], s - t3);
+        }
+      }
+#undef NB
+      const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
+      int pre = cnt;  // inclusive scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= cnt;  // exclusive
+      const int64_t zs = cz - R;
+      const int sh = (int)(zs & 7);
+      const int64_t zb = zs >> 3;  // chunk index of the kernel's first chunk
+      const int64_t cbase = ((cx - a.x0) * a.ny + cy) * a.nzp + (zb << 3);
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        int own = 0;  // owner lane: the last lane whose exclusive prefix is <= t
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const int cand = own + st;
+          const int pv = __shfl_sync(0xffffffffu, pre, cand & 31);
+          if (cand < 32 && pv <= t) own = cand;
+        }
+        const int o_pre = __shfl_sync(0xffffffffu, pre, own);
+        const int o_ylo = __shfl_sync(0xffffffffu, ylo, own);
+        const int mp0 = __shfl_sync(0xffffffffu, mp[0], own), mp1 = __shfl_sync(0xffffffffu, mp[1], own),
+                  mp2 = __shfl_sync(0xffffffffu, mp[2], own);
+        const int mm0 = __shfl_sync(0xffffffffu, mm[0], own), mm1 = __shfl_sync(0xffffffffu, mm[1], own),
+                  mm2 = __shfl_sync(0xffffffffu, mm[2], own);
+        bool alive = t < total;
+        const int rdx = own - R;
+        const int rdy = o_ylo + (t - o_pre);
+        // dz interval: delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1),
+        // delta_z = -1 ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only
+        // when v is in their y-window)
+        int zhi = min(R, max(mp1, -R + 1) - 1), zlo = max(-R, min(mm1, R - 1) + 1);
+        if (rdy <= R - 1) {  // b = -1
+          zhi = min(zhi, max(mp0 + rdy, -R + 1) - 1);
+          zlo = max(zlo, min(mm0 - rdy, R - 1) + 1);
+        }
+        if (rdy >= -R + 1) {  // b = +1
+          zhi = min(zhi, max(mp2 - rdy, -R + 1) - 1);
+          zlo = max(zlo, min(mm2 + rdy, R - 1) + 1);
+        }
+        alive = alive && zlo <= zhi;
+        uint64_t task = 0;
+        if (alive) {
+          const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
+          const int drow = sh * a.nd * a.CH + __ldg(rowd + (rdx + R) * K + (rdy + R));
+          task = pack_task(cbase + rdx * sx + rdy * a.nzp, c0, c1, drow);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, alive);
+        int qb = 0;
+        if (lane == 0 && m) qb = atomicAdd(&q_n, __popc(m));
+        qb = __shfl_sync(0xffffffffu, qb, 0);
+        if (alive) queue[qb + __popc(m & ((1u << lane) - 1u))] = task;
+      }
+    }
+    __syncthreads();
+    // next batch index: its atomic overlaps phase B
+    if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
+    // ===== phase B: the block sweeps the queued rows, one thread per row =====
+    const int nq = q_n;
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+      const uint64_t task = queue[i];
+      const int64_t rbase = (int64_t)(task & ((1ull << 37) - 1)) << 3;
+      const int c0 = (int)((task >> 37) & 3), c1 = (int)((task >> 39) & 3);
+      const uint2* drow = dtab + (int)(task >> 41);
+      uint2 w[4], d8[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool act = c0 + j <= c1;
+        const uint2 dv = __ldg(drow + (act ? c0 + j : c0));
+        d8[j] = act ? dv : make_uint2(0x40404040u, 0x40404040u);
+        w[j] = *reinterpret_cast<const uint2*>(a.dist + rbase + 8 * (act ? c0 + j : c0));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t lt0 = ((w[j].x | 0x80808080u) - d8[j].x) & 0x80808080u;
+        const uint32_t lt1 = ((w[j].y | 0x80808080u) - d8[j].y) & 0x80808080u;
+        if (lt0 | lt1) {
+          const int64_t off = rbase + 8 * (c0 + j);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const uint32_t lt = b < 4 ? lt0 : lt1;
+            if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
+            const uint32_t d = (((b < 4 ? d8[j].x : d8[j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
+            atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
+            ++changed;
+            a.dist[off + b] = (uint8_t)d;
+          }
+        }
+      }
+    }
+    __syncthreads();  // queue and batch0 are rewritten by the next batch
+  }
+  for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  if (lane == 0 && changed) atomicAdd(&a.lc->changed, changed);
 }
 
 typedef void (*SweepFn)(SweepArgs);
@@ -704,7 +900,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     g->cert_dk = b->dk_hash;
   }
   // claim mode: centre dedup and cross-launch skip through the certificates
-  const bool claim = !p->first_return && !(p->flags & (DBT_FLAG_NO_SKIP | DBT_FLAG_NO_DEDUP));
+  // (the stamp of a centre is the same for every return there, so this holds
+  // in first-return mode too; the hash then only picks the shadow return)
+  const bool claim = !(p->flags & (DBT_FLAG_NO_SKIP | DBT_FLAG_NO_DEDUP));
   // the shadow update runs as its own kernel on the aux stream, concurrent
   // with the sweep (one is atomic-latency bound, the other L1 bound); fusing
   // it into preprocessing is kept as a measurement option
@@ -813,6 +1011,41 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     joined = true;
   }
 
+  if (b->iso && !(p->flags & DBT_FLAG_GENERIC_SWEEP)) {
+    const size_t smem = (size_t)kCullWarps * b->K * b->K * sizeof(uint64_t);
+    if (g->sweep_ch != -b->K) {
+      DBT_CUDA(cudaFuncSetAttribute(sweep_cull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0, sms = 0;
+      DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_cull_kernel, 256, smem));
+      DBT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+      g->sweep_blocks = std::max(per_sm, 1) * sms;
+      g->sweep_ch = -b->K;
+    }
+    CullArgs wa;
+    wa.cells = g->cells;
+    wa.dist = g->dist;
+    wa.uniq = g->d_uniq;
+    wa.lc = g->d_lcnt;
+    wa.dtab = b->d_dtab;
+    wa.rowd = b->d_rowd;
+    wa.stamped = g->stamped;
+    wa.K = b->K;
+    wa.R = b->R;
+    wa.nd = b->n_distinct;
+    wa.CH = b->chunks_per_row;
+    wa.x0 = g->x0;
+    wa.x1 = g->x1;
+    wa.ny = g->ny;
+    wa.nzp = g->nzp;
+    // persistent blocks fetching 8 centres at a time
+    unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 15) / 16));
+    prof_begin(g, "sweep_kernel", st, &tok);
+    sweep_cull_kernel<<<blocks, 256, smem, st>>>(wa);
+    prof_end(g, st, tok);
+    DBT_CHECK_LAUNCH("sweep_cull_kernel");
+    if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
+    return DBT_OK;
+  }
   const int CH = b->chunks_per_row;
   SweepFn fn = sweep_fn(CH);
   if (!fn) return set_error(DBT_ERR_CONFIG, "unsupported kernel size for the sweep");
@@ -845,9 +1078,6 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   wa.x1 = g->x1;
   wa.ny = g->ny;
   wa.nzp = g->nzp;
-  wa.stamped = g->stamped;
-  wa.skip_stamped = (p->flags & DBT_FLAG_NO_SKIP) || claim ? 0 : 1;
-  wa.certify = claim ? 0 : 1;
   unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 7) / 8));
   prof_begin(g, "sweep_kernel", st, &tok);
   fn<<<blocks, 256, smem, st>>>(wa);

@@ -329,6 +329,40 @@ class TestStampCertificate:
         assert np.array_equal(g.mask, og.mask)
 
 
+class TestSweepPaths:
+    """The symmetric-kernel sweep (base-pair table) and the generic sweep
+    (distinct-row table) must both reproduce the reference stamping."""
+
+    def _run(self, bank, frames, dims=(48, 48, 48), first_return=False):
+        g = new_grid(dims, 0.1)
+        og = oracle.OracleGrid(dims, 0.1, (0, 0, 0))
+        ob = oracle.OracleBank.from_bank(bank)
+        for pts, pose in frames:
+            integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams(first_return_per_voxel=first_return))
+            oracle.integrate_frame(og, ob, pts, pose, first_return=first_return)
+        assert np.array_equal(g.mask, og.mask) and np.array_equal(g.sign, og.sign) and np.array_equal(g.hits, og.hits)
+
+    @pytest.mark.parametrize("first_return", [False, True])
+    def test_asymmetric_kernel_takes_generic_sweep(self, first_return):
+        import dataclasses
+        base = build_kernel_bank(shadow_radius=2)
+        dk = base.distance_kernel.copy()
+        # break the x/y symmetry: one octant gets shorter runs, one row longer
+        dk[12:, 14:, :] &= np.uint32(0x3F)
+        dk[3, 17, :] = np.uint32(0xFFFFF)
+        bank = dataclasses.replace(base, distance_kernel=dk, _device={})
+        rng = np.random.default_rng(8)
+        frames = [(rng.uniform(1.15, 3.6, size=(400, 3)), cases.yaw_pose(0.4 * k, (0.02 * k, 0, 0))) for k in range(3)]
+        self._run(bank, frames, first_return=first_return)
+
+    @pytest.mark.parametrize("size", [3, 5, 9, 15, 21, 25, 27])
+    def test_symmetric_kernel_sizes(self, size):
+        bank = build_kernel_bank(size=size, shadow_radius=1)
+        rng = np.random.default_rng(size)
+        frames = [(rng.uniform(1.4, 3.4, size=(300, 3)), cases.yaw_pose(0.3 * k, (0.0, 0.01 * k, 0))) for k in range(2)]
+        self._run(bank, frames)
+
+
 class TestGridSemantics:
     def test_host_mirror_in_place_and_injected_fault(self):
         bank = build_kernel_bank(shadow_radius=3)

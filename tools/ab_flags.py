@@ -16,7 +16,9 @@ scans = [torch.from_numpy(w.scan(k)).cuda() for k in range(30)]
 bank = build_kernel_bank(shadow_radius=w.shadow_radius)
 L = _native.lib()
 variants = {"default": 0, "fused": _native.FLAG_FUSE_SHADOW, "no_skip": _native.FLAG_NO_SKIP,
-            "no_dedup": _native.FLAG_NO_DEDUP}
+            "no_dedup": _native.FLAG_NO_DEDUP, "generic": _native.FLAG_GENERIC_SWEEP}
+if len(sys.argv) > 1:
+    variants = {k: v for k, v in variants.items() if k in sys.argv[1:]}
 for name, flags in variants.items():
     g = VoxelGrid(w.dims, w.voxel_size, w.origin)
     prm = _native.make_params(flags=flags)

@@ -20,10 +20,22 @@ lib = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2509
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr_i = next(i for i, r in enumerate(rows) if "Address" in r and "Source" in r)
+# a report with several kernels has one section per kernel, each opened by a
+# "Kernel Name" row: keep the section of the requested kernel
+sec_start = 0
+for i, r in enumerate(rows):
+    if r and r[0] == "Kernel Name" and len(r) > 1 and kname in r[1]:
+        sec_start = i
+        break
+hdr_i = next(i for i, r in enumerate(rows) if i > sec_start and "Address" in r and "Source" in r)
 hdr = rows[hdr_i]
 ia, isrc, ismp = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
-samples = [(int(r[ia], 16), r[isrc].strip(), int(r[ismp] or 0)) for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
+samples = []
+for r in rows[hdr_i + 1:]:
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        samples.append((int(r[ia], 16), r[isrc].strip(), int(r[ismp] or 0)))
 base = samples[0][0]
 rel = {a - base: (s, n) for a, s, n in samples}
 tmp = tempfile.mkdtemp()
