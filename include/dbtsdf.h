@@ -56,8 +56,10 @@ extern "C" {
                                         (measurement only; identical grid) */
 #define DBT_FLAG_FUSE_SHADOW 16u     /* shadow update fused into preprocessing instead of
                                         a kernel concurrent with the sweep (measurement) */
-#define DBT_FLAG_GENERIC_SWEEP 32u   /* distinct-row sweep even for a symmetric kernel
+#define DBT_FLAG_GENERIC_SWEEP 32u   /* distinct-row sweep even for an isotropic kernel
                                         (measurement; identical grid) */
+#define DBT_FLAG_STAGE_COPY 64u      /* stage pinned host scans with an H2D copy instead of
+                                        reading them zero-copy in preprocessing (measurement) */
 
 typedef struct dbt_grid dbt_grid; /* device-resident VoxelGrid (grid.py:39-58) */
 typedef struct dbt_bank dbt_bank; /* device copy of a KernelBank (kernels.py:122-141) */
@@ -136,9 +138,10 @@ DBT_API int dbt_bank_create(int32_t size, int32_t b_az, int32_t b_el, const uint
 DBT_API int dbt_bank_destroy(dbt_bank* b);
 
 /* ---- integration (integrator.py:163-287) ------------------------------- */
-/* One scan, sensor-frame points from HOST memory (pinned or pageable):
- * H2D copy, transform pts@R.T+t, discard, bin, stamp, stats D2H; returns
- * when the grid is updated. pose: 4x4 row-major float64. */
+/* One scan, sensor-frame points from HOST memory: pageable memory is staged
+ * with one H2D copy, pinned (device-mapped) memory is read zero-copy by the
+ * preprocessing kernel; then transform pts@R.T+t, discard, bin, stamp, stats
+ * D2H; returns when the grid is updated. pose: 4x4 row-major float64. */
 DBT_API int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
                         int64_t n, const double pose[16], const dbt_params* p, dbt_stats* out);
 /* S scans in one launch sequence (config 5): points concatenated, counts[S],

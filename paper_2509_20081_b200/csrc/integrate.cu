@@ -1137,12 +1137,28 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
     return DBT_OK;
   }
   const size_t esz = dtype == DBT_F32 ? 12 : 24;
-  rc = stage_raw(g, total * (int64_t)esz);
-  if (rc) return rc;
   cudaStream_t st = g->stream;
+  // Pinned (page-locked, device-mapped) host scans are read by the prep
+  // kernel straight over the host link (zero-copy): the transfer overlaps
+  // preprocessing instead of preceding it. Pageable memory is staged with
+  // one H2D copy.
+  const void* d_src = nullptr;
+  if (!(p->flags & DBT_FLAG_STAGE_COPY)) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, points) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer != nullptr)
+      d_src = at.devicePointer;
+    else
+      cudaGetLastError();  // pageable pointers report an error on some drivers
+  }
   DBT_CUDA(cudaEventRecord(g->ev_a, st));
-  DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
-  rc = launch_integrate(g, b, g->d_raw, dtype, counts, S, poses, p, nullptr, nullptr, st);
+  if (!d_src) {
+    rc = stage_raw(g, total * (int64_t)esz);
+    if (rc) return rc;
+    DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
+    d_src = g->d_raw;
+  }
+  rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st);
   if (rc) return rc;
   rc = fetch_counters(g, st);
   if (rc) return rc;
