@@ -237,6 +237,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1, help="scans per launch (config 5: 1/8/32/128)")
     ap.add_argument("--max-scans", type=int, default=None, help="distinct scans to generate (default: all needed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -285,7 +286,6 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
     torch.cuda.set_stream(stream)
-    L.dbt_profile_enable(sg.local.handle, 1)
 
     def do_step(s):
         pts, counts, poses = batches[s % steps_per_pass]
@@ -295,52 +295,76 @@ def main():
             dist.broadcast(pts, 0)
         sg.integrate_device(bank, pts, counts, poses, params, stream=stream)
 
-    for s in range(args.warmup):
-        if s % steps_per_pass == 0:
+    # applied returns of every distinct batch (discards do not depend on the
+    # grid state), so the timed pass needs no per-step read-back
+    applied_of = []
+    for j in range(steps_per_pass):
+        if j == 0:
             L.dbt_grid_reset(sg.local.handle)
-        do_step(s)
-    torch.cuda.synchronize()
-    L.dbt_profile_reset(sg.local.handle)
-    applied = swept = written = skipped = 0
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = L.dbt_launch_count()
-    with ClockSampler(local) as clk:
+        do_step(j)
+        applied_of.append(sum(x.points_in - x.points_discarded for x in sg.stats()))
+
+    def run_pass(timed):
+        """warmup + steps from a reset grid; timed: no host sync or profiling
+        inside the region (launches queue ahead), else per-step stats and
+        per-kernel CUDA events."""
+        L.dbt_profile_enable(sg.local.handle, 0 if timed else 1)
+        L.dbt_grid_reset(sg.local.handle)
+        for s in range(args.warmup):
+            if s and s % steps_per_pass == 0:
+                L.dbt_grid_reset(sg.local.handle)
+            do_step(s)
+        torch.cuda.synchronize()
+        L.dbt_profile_reset(sg.local.handle)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        cnt = {"applied": 0, "swept": 0, "written": 0, "skipped": 0}
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = L.dbt_launch_count()
         for i in range(args.steps):
             s = args.warmup + i
             if s % steps_per_pass == 0:
                 L.dbt_grid_reset(sg.local.handle)
-            flush.zero_()
+            if not args.no_flush:
+                flush.zero_()
             ev[i][0].record(stream)
             do_step(s)
             ev[i][1].record(stream)
-            sts = sg.stats()
-            applied += sum(x.points_in - x.points_discarded for x in sts)
-            swept += sts[0].unique_centers
-            written += sts[0].voxels_written
-            skipped += sts[0].centers_skipped
+            cnt["applied"] += applied_of[s % steps_per_pass]
+            if not timed:
+                sts = sg.stats()
+                cnt["swept"] += sts[0].unique_centers
+                cnt["written"] += sts[0].voxels_written
+                cnt["skipped"] += sts[0].centers_skipped
         torch.cuda.synchronize()
-    launches = L.dbt_launch_count() - launches0
-    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+        launches = L.dbt_launch_count() - launches0
+        dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+        return dev_ms, launches, cnt
+
+    with ClockSampler(local) as clk:
+        dev_ms, launches, cnt = run_pass(timed=True)
     if dist is not None:
         t = torch.tensor([dev_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
         dist.barrier()
+    applied = cnt["applied"]
     value = applied / (dev_ms / 1e3)
 
-    # per-kernel device time (CUDA events on each kernel's stream, same region)
+    # per-kernel device time: a second, identical pass with CUDA events around
+    # every kernel on its own stream (not inside the timed region above)
+    prof_ms, _, pc = run_pass(timed=False)
+    swept, written, skipped = pc["swept"], pc["written"], pc["skipped"]
     names = ctypes.create_string_buffer(32 * 16)
     ms = (ctypes.c_double * 16)()
-    cnt = (ctypes.c_int64 * 16)()
+    cnt_ = (ctypes.c_int64 * 16)()
     nk = ctypes.c_int32()
-    L.dbt_profile_read(sg.local.handle, names, ms, cnt, 16, ctypes.byref(nk))
+    L.dbt_profile_read(sg.local.handle, names, ms, cnt_, 16, ctypes.byref(nk))
     kernels = {}
     for i in range(nk.value):
         nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
-        kernels[nm] = {"ms_total": ms[i], "launches": int(cnt[i]), "avg_us": ms[i] / max(cnt[i], 1) * 1e3}
+        kernels[nm] = {"ms_total": ms[i], "launches": int(cnt_[i]), "avg_us": ms[i] / max(cnt_[i], 1) * 1e3}
     L.dbt_profile_enable(sg.local.handle, 0)
 
     sweep = kernels.get("sweep_kernel", {"avg_us": float("nan"), "launches": 0})
@@ -363,6 +387,10 @@ def main():
         "config": config_desc(w, B),
         "gpu_launches": int(launches),
         "kernels": kernels,
+        "profiled_step_ms": prof_ms / args.steps,
+        "timing": "timed pass: launches queue ahead (no per-step host sync, no per-kernel events); "
+                  "applied returns per scan from an untimed counting pass; kernel times from a second "
+                  "identical pass with per-kernel CUDA events",
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -500,12 +500,12 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 // Per centre the surviving region is, for each kernel x-offset dx (lane), a
 // dy interval (neighbours with delta_z = 0 cut whole rows) and per row a dz
 // interval (delta_z = +-1 neighbours cut z prefixes/suffixes). A block takes
-// 8 centres at a time: phase A, one warp per centre, compacts the surviving
+// kCullWarps centres at a time: phase A, one warp per centre, compacts the surviving
 // rows into a shared-memory queue of row tasks (row start, chunk range,
 // d-table row); phase B, the whole block, sweeps the queued rows one thread
 // per row (1-4 chunk loads in flight each), testing them as sweep_kernel
 // does. Rows of a heavy centre (a fresh surface: nothing culled) thus spread
-// over 256 threads instead of serialising one warp.
+// over the block instead of serialising one warp.
 struct CullArgs {
   uint2* cells;
   uint8_t* dist;
@@ -519,7 +519,7 @@ struct CullArgs {
 };
 
 constexpr int kFar = 1 << 20;
-constexpr int kCullWarps = 8;  // centres per block batch (one per warp)
+constexpr int kCullWarps = 4;  // centres per block batch (one per warp; 4 measured best of 1/2/4/8)
 
 // row task: bits 0-36 row start / 8 (cells), 37-38 first chunk, 39-40 last
 // chunk, 41-54 d-table row offset
@@ -527,7 +527,7 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
   return (uint64_t)(rbase >> 3) | ((uint64_t)c0 << 37) | ((uint64_t)c1 << 39) | ((uint64_t)drow << 41);
 }
 
-__global__ void __launch_bounds__(256) sweep_cull_kernel(CullArgs a) {
+__global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw);  // kCullWarps * K * K
   __shared__ int q_n;
@@ -1016,7 +1016,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     if (g->sweep_ch != -b->K) {
       DBT_CUDA(cudaFuncSetAttribute(sweep_cull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0, sms = 0;
-      DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_cull_kernel, 256, smem));
+      DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_cull_kernel, kCullWarps * 32, smem));
       DBT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
       g->sweep_blocks = std::max(per_sm, 1) * sms;
       g->sweep_ch = -b->K;
@@ -1037,10 +1037,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     wa.x1 = g->x1;
     wa.ny = g->ny;
     wa.nzp = g->nzp;
-    // persistent blocks fetching 8 centres at a time
-    unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 15) / 16));
+    // persistent blocks fetching kCullWarps centres at a time
+    unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 2 * kCullWarps - 1) / (2 * kCullWarps)));
     prof_begin(g, "sweep_kernel", st, &tok);
-    sweep_cull_kernel<<<blocks, 256, smem, st>>>(wa);
+    sweep_cull_kernel<<<blocks, kCullWarps * 32, smem, st>>>(wa);
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");
     if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
