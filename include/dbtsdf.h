@@ -117,6 +117,11 @@ DBT_API int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end,
  * Whole grid only (slab == full grid). */
 DBT_API int dbt_grid_to_records(dbt_grid* g, void* out_records);
 DBT_API int dbt_grid_from_records(dbt_grid* g, const void* records);
+/* The records of the z-planes [z_begin, z_end): a contiguous block of
+ * (z_end-z_begin)*nx*ny records of the F-order stream (io.py:449-486 writes
+ * them in this order), so DBTSDF01 snapshots stream in pieces. */
+DBT_API int dbt_grid_to_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, void* out_records);
+DBT_API int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, const void* records);
 /* Point query: n voxels given as global (ix,iy,iz) int64 triples inside the
  * slab (signed_distance / is_observed, grid.py:138-158); outputs nullable. */
 DBT_API int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, uint8_t* sign,

@@ -37,6 +37,7 @@ from .integrator import (
     integrate_points,
 )
 from .kernels import KernelBank, build_kernel_bank
+from .snapshot import SNAPSHOT_MAGIC, load_grid, save_grid
 
 __version__ = "0.1.0"
 
@@ -60,6 +61,9 @@ __all__ = [
     "integrate_frames",
     "integrate_point",
     "integrate_points",
+    "SNAPSHOT_MAGIC",
+    "save_grid",
+    "load_grid",
     "BitsdfError",
     "ConfigurationError",
     "ResourceError",

@@ -59,6 +59,17 @@ __global__ void rebuild_dist_kernel(const uint2* __restrict__ cells, uint8_t* __
     dist[i] = (uint8_t)mask_bitlen(cells[i].x);
 }
 
+// distance cache of the z-range [z0, z1) only (chunked record loads)
+__global__ void rebuild_dist_range_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ dist, int64_t rows,
+                                          int64_t nzp, int64_t z0, int64_t z1) {
+  const int64_t zc = z1 - z0, n = rows * zc;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / zc, off = row * nzp + z0 + (i - row * zc);
+    dist[off] = (uint8_t)mask_bitlen(cells[off].x);
+  }
+}
+
 __global__ void decode_kernel(const uint2* __restrict__ cells, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits, int64_t n,
                               int64_t nz, int64_t nzp) {
@@ -452,50 +463,73 @@ int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, 
   return DBT_OK;
 }
 
-int dbt_grid_to_records(dbt_grid* g, void* out_records) {
+int dbt_grid_to_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, void* out_records) {
   int rc = check_grid(g);
   if (rc) return rc;
   if (g->x0 != 0 || g->x1 != g->nx)
     return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
   if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
+  if (z_begin < 0 || z_end > g->nz || z_begin > z_end) return set_error(DBT_ERR_CONFIG, "z range outside the grid");
   const int64_t plane = g->nx * g->ny;
-  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
+  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(z_end - z_begin, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
   if (rc) return rc;
   uint2* st = (uint2*)g->d_stage;
-  for (int64_t z = 0; z < g->nz; z += zs) {
-    int64_t zc = std::min(zs, g->nz - z);
+  for (int64_t z = z_begin; z < z_end; z += zs) {
+    int64_t zc = std::min(zs, z_end - z);
     dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
     to_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc);
     DBT_CHECK_LAUNCH("to_records_kernel");
-    DBT_CUDA(cudaMemcpyAsync((uint64_t*)out_records + z * plane, st, zc * plane * 8,
+    DBT_CUDA(cudaMemcpyAsync((uint64_t*)out_records + (z - z_begin) * plane, st, zc * plane * 8,
                              cudaMemcpyDeviceToHost, g->stream));
     DBT_CUDA(cudaStreamSynchronize(g->stream));
   }
   return DBT_OK;
 }
 
-int dbt_grid_from_records(dbt_grid* g, const void* records) {
+int dbt_grid_to_records(dbt_grid* g, void* out_records) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  return dbt_grid_to_records_range(g, 0, g->nz, out_records);
+}
+
+int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, const void* records) {
   int rc = check_grid(g);
   if (rc) return rc;
   if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
   if (g->x0 != 0 || g->x1 != g->nx)
     return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
+  if (z_begin < 0 || z_end > g->nz || z_begin > z_end) return set_error(DBT_ERR_CONFIG, "z range outside the grid");
   const int64_t plane = g->nx * g->ny;
-  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(g->nz, kStageBytes / (plane * 8)));
+  int64_t zs = std::max<int64_t>(1, std::min<int64_t>(z_end - z_begin, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
   if (rc) return rc;
   uint2* st = (uint2*)g->d_stage;
-  for (int64_t z = 0; z < g->nz; z += zs) {
-    int64_t zc = std::min(zs, g->nz - z);
-    DBT_CUDA(cudaMemcpyAsync(st, (const uint64_t*)records + z * plane, zc * plane * 8,
+  for (int64_t z = z_begin; z < z_end; z += zs) {
+    int64_t zc = std::min(zs, z_end - z);
+    DBT_CUDA(cudaMemcpyAsync(st, (const uint64_t*)records + (z - z_begin) * plane, zc * plane * 8,
                              cudaMemcpyHostToDevice, g->stream));
     dim3 grid((unsigned)((g->nx + 31) / 32), (unsigned)g->ny, (unsigned)((zc + 31) / 32));
     from_records_kernel<<<grid, dim3(32, 8), 0, g->stream>>>(g->cells, st, g->nx, g->ny, g->nzp, z, zc);
     DBT_CHECK_LAUNCH("from_records_kernel");
     DBT_CUDA(cudaStreamSynchronize(g->stream));
   }
-  return finish_host_write(g);
+  // distance cache of the written range; every stamp certificate dropped
+  if (z_end > z_begin) {
+    rebuild_dist_range_kernel<<<grid_blocks(plane * (z_end - z_begin)), 256, 0, g->stream>>>(
+        g->cells, g->dist, plane, g->nzp, z_begin, z_end);
+    DBT_CHECK_LAUNCH("rebuild_dist_range_kernel");
+  }
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
+  DBT_CUDA(cudaStreamSynchronize(g->stream));
+  g->cert_dk = 0;
+  return DBT_OK;
+}
+
+int dbt_grid_from_records(dbt_grid* g, const void* records) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  return dbt_grid_from_records_range(g, 0, g->nz, records);
 }
 
 }  // extern "C"

@@ -29,6 +29,7 @@ import cases  # noqa: E402
 from bitsdf.grid import new_grid  # noqa: E402  (reference)
 from bitsdf.integrator import IntegrationParams, ScanFrame, integrate_frame, integrate_point  # noqa: E402
 from bitsdf.kernels import bin_index_array, build_kernel_bank  # noqa: E402
+from bitsdf import io as bio  # noqa: E402
 
 
 def run_case(c: cases.Case) -> dict:
@@ -61,6 +62,17 @@ def run_case(c: cases.Case) -> dict:
         "occupied": int(np.count_nonzero(g.sign == 0)),
         "ref_seconds": round(el, 2),
     }
+    if not c.slow:
+        # the reference's own DBTSDF01 snapshot of the final grid (io.py:449-459)
+        # with the case's h_max / t_occ in the header
+        import hashlib
+        import tempfile
+        g.h_max, g.t_occ = params.h_max, params.t_occ
+        with tempfile.TemporaryDirectory() as td:
+            fp = Path(td) / "g.dbtsdf"
+            bio.save_grid(g, fp)
+            raw = fp.read_bytes()
+        out["snapshot"] = {"bytes": len(raw), "sha": hashlib.sha256(raw).hexdigest()[:32]}
     print(f"{c.name}: {el:.1f}s stats={stats} applied={applied}", flush=True)
     return out
 
@@ -84,6 +96,18 @@ def main():
         gold["bins"][name] = {"input": cases.sha(dirs), "b_a": cases.sha(b_a.astype(np.int64)),
                               "b_e": cases.sha(b_e.astype(np.int64))}
     gold.setdefault("cases", {})
+    if "--only-snapshots" in sys.argv:
+        # add the snapshot hashes of the small cases; every other stored value
+        # must come out unchanged
+        for c in cases.small_cases():
+            r = run_case(c)
+            old = gold["cases"][c.name]
+            for k in ("input", "mask", "sign", "hits", "stats", "applied"):
+                assert old[k] == r[k], (c.name, k)
+            old["snapshot"] = r["snapshot"]
+        out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))
+        print("wrote", out_path)
+        return
     all_cases = cases.small_cases() + cases.config_cases(include_slow=not fast)
     for c in all_cases:
         gold["cases"][c.name] = run_case(c)

@@ -329,6 +329,64 @@ class TestStampCertificate:
         assert np.array_equal(g.mask, og.mask)
 
 
+SNAP = [c for c in SMALL if c.name in ("frame500_default", "arbitrary_state", "nonfresh_cone_h200_t2", "k9_bins8")]
+
+
+class TestSnapshot:
+    """DBTSDF01 snapshots from the device layout (io.py:449-486): the bytes are
+    the reference's own save_grid bytes for the same final grid."""
+
+    @pytest.mark.parametrize("c", SNAP, ids=[c.name for c in SNAP])
+    def test_save_matches_reference_bytes(self, c, golden, tmp_path, monkeypatch):
+        import hashlib
+
+        from paper_2509_20081_b200 import snapshot
+        from paper_2509_20081_b200 import load_grid, save_grid
+
+        g, _, _ = engine_run(c)
+        params = IntegrationParams(**c.params)
+        g.h_max, g.t_occ = params.h_max, params.t_occ
+        p = tmp_path / "g.dbtsdf"
+        save_grid(g, p)
+        raw = p.read_bytes()
+        ref = golden["cases"][c.name]["snapshot"]
+        assert len(raw) == ref["bytes"] and hashlib.sha256(raw).hexdigest()[:32] == ref["sha"]
+        # streamed in 1-plane chunks: same bytes
+        monkeypatch.setattr(snapshot, "_CHUNK_BYTES", 1)
+        p2 = tmp_path / "g2.dbtsdf"
+        save_grid(g, p2)
+        assert p2.read_bytes() == raw
+        # load (chunked) -> identical grid, h_max/t_occ restored, byte-identical re-save
+        g2 = load_grid(p2)
+        assert (g2.h_max, g2.t_occ) == (params.h_max, params.t_occ)
+        m, s_, h = g.download_range(0, c.dims[0])
+        m2, s2, h2 = g2.download_range(0, c.dims[0])
+        assert np.array_equal(m, m2) and np.array_equal(s_, s2) and np.array_equal(h, h2)
+        p3 = tmp_path / "g3.dbtsdf"
+        save_grid(g2, p3)
+        assert p3.read_bytes() == raw
+
+    def test_loaded_grid_integrates_like_reference(self, tmp_path):
+        """A grid loaded from a snapshot carries no stamp certificates: the
+        next scan must still match the oracle exactly."""
+        from paper_2509_20081_b200 import load_grid, save_grid
+
+        bank = build_kernel_bank(shadow_radius=2)
+        rng = np.random.default_rng(5)
+        pts1, pts2 = rng.uniform(1.15, 3.6, size=(300, 3)), rng.uniform(1.15, 3.6, size=(300, 3))
+        g = new_grid((48, 48, 48), 0.1)
+        integrate_frame(g, bank, ScanFrame(points=pts1, pose=np.eye(4)), IntegrationParams())
+        save_grid(g, tmp_path / "a.dbtsdf")
+        g2 = load_grid(tmp_path / "a.dbtsdf")
+        integrate_frame(g2, bank, ScanFrame(points=pts1, pose=np.eye(4)), IntegrationParams())
+        integrate_frame(g2, bank, ScanFrame(points=pts2, pose=np.eye(4)), IntegrationParams())
+        og = oracle.OracleGrid((48, 48, 48), 0.1, (0, 0, 0))
+        ob = oracle.OracleBank.from_bank(bank)
+        for pts in (pts1, pts1, pts2):
+            oracle.integrate_frame(og, ob, pts, np.eye(4))
+        assert np.array_equal(g2.mask, og.mask) and np.array_equal(g2.sign, og.sign) and np.array_equal(g2.hits, og.hits)
+
+
 class TestSweepPaths:
     """The symmetric-kernel sweep (base-pair table) and the generic sweep
     (distinct-row table) must both reproduce the reference stamping."""

@@ -201,3 +201,39 @@ class TestGridHelpers:
         assert errors.CODE_TO_ERROR[4] is CorruptionError
         assert errors.CODE_TO_ERROR[5] is errors.EvaluationError
         assert errors.CODE_TO_ERROR[6] is ResourceError
+
+
+class TestSnapshotHeader:
+    """DBTSDF01 validation happens on the host before any device work
+    (io.py:462-477; reference test_io.py snapshot cases)."""
+
+    def _write(self, p, body):
+        p.write_bytes(body)
+        return p
+
+    def test_header_layout(self):
+        from paper_2509_20081_b200 import snapshot
+
+        assert snapshot.SNAPSHOT_MAGIC == b"DBTSDF01" and snapshot._HEADER.size == 52
+
+    def test_wrong_magic(self, tmp_path):
+        from paper_2509_20081_b200 import load_grid
+
+        with pytest.raises(CorruptionError):
+            load_grid(self._write(tmp_path / "bad.dbtsdf", b"NOTADUMP" + b"\x00" * 64))
+
+    def test_truncated_header(self, tmp_path):
+        from paper_2509_20081_b200 import load_grid
+
+        with pytest.raises(CorruptionError):
+            load_grid(self._write(tmp_path / "t.dbtsdf", b"DBTSDF01" + b"\x00" * 20))
+
+    def test_zero_dims_and_short_payload(self, tmp_path):
+        from paper_2509_20081_b200 import load_grid, snapshot
+
+        head = snapshot._HEADER.pack(0, 2, 2, 0.1, 0.0, 0.0, 0.0, 255, 2)
+        with pytest.raises(CorruptionError):
+            load_grid(self._write(tmp_path / "z.dbtsdf", b"DBTSDF01" + head + b"\x00" * 64))
+        head = snapshot._HEADER.pack(4, 4, 4, 0.1, 0.0, 0.0, 0.0, 255, 2)
+        with pytest.raises(CorruptionError):
+            load_grid(self._write(tmp_path / "s.dbtsdf", b"DBTSDF01" + head + b"\x00" * (64 * 8 - 16)))
