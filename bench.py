@@ -376,10 +376,21 @@ def main():
     # cache over the K^3 cube of every swept centre + word RED.AND and cache
     # store per lowered voxel (the shadow kernel runs concurrently)
     touched = (swept * K_EDGE ** 3 + written * 5) / max(args.steps, 1)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "dram_per_launch.json")
+    traffic, lts = None, None
+    tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
     if os.path.exists(tpath) and args.config == 2 and B == 1:
-        traffic = json.load(open(tpath)).get("sweep_kernel")
+        tr = json.load(open(tpath)).get("kernels", {})
+        sw = tr.get("sweep_kernel", {})
+        if "dram_bytes" in sw:
+            traffic = sw["dram_bytes"]
+        lts = {k: v for k, v in tr.items()}
+    # the roof of a launch whose mask footprint fits L2 is the
+    # measured L2 atomic (4-byte RED.AND) throughput, HBM otherwise
+    l2 = (ctypes.c_double * 3)()
+    _native.check(L.dbt_probe_l2(local, 48 << 20, l2))
+    mask_bytes = 4 * w.dims[0] * w.dims[1] * w.dims[2]
+    l2_size = torch.cuda.get_device_properties(local).L2_cache_size
+    survey_roof = ("l2_red", l2[1]) if mask_bytes <= l2_size else ("hbm", peak)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -406,7 +417,16 @@ def main():
                                          "(certificates) and reads a 1-byte cache: touched/traffic are the bytes "
                                          "actually moved",
                      "centres_swept_per_launch": swept / max(args.steps, 1),
-                     "returns_skipped_per_launch": skipped / max(args.steps, 1)},
+                     "returns_skipped_per_launch": skipped / max(args.steps, 1),
+                     "l2_probe": {"red_and_gops": l2[0], "red_and_gbs": l2[1], "ldcg_gbs": l2[2],
+                                  "buffer_bytes": 48 << 20,
+                                  "how": "dbt_probe_l2: coalesced 4-byte RED.AND / 8-byte ld.cg over an "
+                                         "L2-resident 48 MB buffer, best of 4 (CUDA events)"},
+                     "survey_roof": {"kind": survey_roof[0], "peak_gbs": survey_roof[1],
+                                     "achieved_gbs": achieved, "frac": achieved / survey_roof[1],
+                                     "why": f"SURVEY.md 8(d): reference mask array {mask_bytes / 1e6:.0f} MB "
+                                            f"vs L2 {l2_size / 1e6:.0f} MB"},
+                     "ncu_per_launch": lts},
     }
 
     # ---------------- e2e through the public API (N=1) ----------------------

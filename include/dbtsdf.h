@@ -186,6 +186,10 @@ DBT_API int dbt_profile_read(dbt_grid* g, char* names, double* ms, int64_t* laun
 DBT_API int dbt_profile_reset(dbt_grid* g);
 /* Kernel launches issued by the engine since load (all handles). */
 DBT_API int64_t dbt_launch_count(void);
+/* Roofline probes: on an L2-resident buffer of `bytes`,
+ * out[0] RED.AND Gop/s on 4-byte words, out[1] the same in GB/s, out[2]
+ * 8-byte ld.cg GB/s. Best of 4 timed runs after a warm-up. */
+DBT_API int dbt_probe_l2(int device, int64_t bytes, double* out);
 
 /* pinned host buffers for callers without a CUDA runtime of their own */
 DBT_API int dbt_host_alloc(int64_t bytes, void** out);

@@ -71,6 +71,7 @@ SIGNATURES = {
     "dbt_grid_download_range": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp]),
     "dbt_grid_to_records": (ctypes.c_int, [_vp, _vp]),
     "dbt_grid_from_records": (ctypes.c_int, [_vp, _vp]),
+    "dbt_probe_l2": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]),
     "dbt_grid_to_records_range": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
     "dbt_grid_from_records_range": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
     "dbt_grid_gather": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
