@@ -1,17 +1,21 @@
 // engine.cuh — internal definitions shared by the libdbtsdf CUDA sources.
 //
-// Device voxel record (8 bytes, one per voxel): exactly the reference's
-// serialized record (grid.py:30-34) — .x = the 32-bit distance mask,
-// .y = sign (byte 0) | hits (byte 1) << 8 | 0 (2 reserved bytes). The two
-// halves are the single aligned words the two update kinds touch:
+// Device voxel record (8 bytes, one per voxel): the reference's serialized
+// record (grid.py:30-34) — .x = the 32-bit distance mask, .y = sign (byte 0)
+// | hits (byte 1) << 8 | pending shadow visits (bytes 2-3, 0 in every record
+// that leaves the device). The two halves are the single aligned words the
+// two update kinds touch:
 //   * mask update (integrator.py:145-149): one native atomicAnd (RED.AND) of
 //     the kernel's run mask into .x — AND is commutative and idempotent, so
 //     no CAS and no retries;
-//   * shadow update (integrator.py:151-159): a 32-bit CAS on .y applying
-//     h += (h < h_max) and sign = 0 when h >= T.
-// They never touch the same 32-bit word, so concurrent sweeps and shadow
-// updates do not invalidate each other's CAS. Any mask and sign byte the
-// reference can hold is represented (no run-mask assumption).
+//   * shadow update (integrator.py:151-159): one atomicAdd of 1 << 16 on .y
+//     counts the visit. n visits of the step h += (h < h_max), sign = 0 when
+//     h >= T, compose to h' = h >= h_max ? h : min(h + n, h_max) and sign = 0
+//     when h' >= T (fold_meta), so counts are folded lazily: before any read
+//     of the grid, before a launch with other (h_max, T), and by the visit
+//     that takes a count to 2^15 (no 16-bit overflow).
+// Any mask and sign byte the reference can hold is represented (no run-mask
+// assumption).
 //
 // Distance cache: one byte per voxel, dist[v] >= bitlen(mask[v]) at all times
 // (equal after upload/reset), where bitlen = 32 - clz (the popcount for the
@@ -23,11 +27,11 @@
 // AND) but never below the record: no update is ever lost.
 //
 // Stamp certificates: one bit per voxel, set when the full K^3 stamp centred
-// at that voxel is in the grid; the AND being idempotent, a later return
-// centred there needs no sweep (its shadow update still runs). Returns claim
-// the bit with one atomicOr in preprocessing (claim mode) or the sweep sets it
-// after stamping (first-return mode). Cleared on reset/upload and when a
-// launch uses a different distance kernel.
+// at that voxel is in the grid or claimed by a return of the running launch;
+// the AND being idempotent, a later return centred there needs no sweep (its
+// shadow update still runs). Returns claim the bit with one atomicOr in
+// preprocessing. Cleared on reset/upload and when a launch uses a different
+// distance kernel.
 //
 // Layout in HBM: C-order (x, y, z) like the reference arrays, x restricted to
 // the owned slab [x0, x1), z stride padded to a multiple of 8 voxels so every
@@ -59,6 +63,20 @@ __host__ __device__ inline uint8_t meta_sign(uint32_t m) { return (uint8_t)(m & 
 __host__ __device__ inline uint8_t meta_hits(uint32_t m) { return (uint8_t)((m >> 8) & 0xFFu); }
 __device__ inline int mask_bitlen(uint32_t m) { return 32 - __clz(m); }
 __host__ __device__ inline uint32_t run_mask_of(int len) { return len ? (0xFFFFFFFFu >> (32 - len)) : 0u; }
+
+constexpr int kPendShift = 16;        // pending shadow visits in .y bits 16-31
+constexpr uint32_t kPendFold = 0x8000u;
+// n pending visits of h += (h < h_max), sign = 0 when h >= T (integrator.py:
+// 154-159) applied at once; the pending bits are cleared
+__host__ __device__ inline uint32_t fold_meta(uint32_t y, uint32_t h_max, uint32_t t_occ) {
+  const uint32_t n = y >> kPendShift;
+  if (!n) return y;
+  const uint32_t h = (y >> 8) & 0xFFu;
+  uint32_t sign = y & 0xFFu;
+  const uint32_t hn = h >= h_max ? h : (h + n < h_max ? h + n : h_max);
+  if (hn >= t_occ) sign = 0;
+  return sign | (hn << 8);
+}
 
 __host__ __device__ inline uint64_t pack_center(int64_t x, int64_t y, int64_t z) {
   return ((uint64_t)x << (2 * kCenterBits)) | ((uint64_t)y << kCenterBits) | (uint64_t)z;
@@ -172,12 +190,19 @@ struct dbt_grid {
   int last_first_return = 0;
   // distance kernel the stamp certificates refer to (0: none yet)
   uint64_t cert_dk = 0;
+  // shadow visits pending in the records (folded before reads, see above)
+  bool pend = false;
+  int pend_h_max = 0, pend_t_occ = 0;
+  cudaEvent_t ev_done = nullptr;               // last integration launch (any stream)
   int sweep_ch = 0;                            // cached sweep launch shape
   int64_t sweep_blocks = 0;
   double last_device_ms = 0;
 };
 
 namespace dbt {
+
+// pending shadow visits (grid.cu): make the records final before a read
+int fold_pending(dbt_grid* g, cudaStream_t st);
 
 // error plumbing (abi.cu)
 int set_error(int code, const std::string& msg);

@@ -59,6 +59,15 @@ __global__ void rebuild_dist_kernel(const uint2* __restrict__ cells, uint8_t* __
     dist[i] = (uint8_t)mask_bitlen(cells[i].x);
 }
 
+// pending shadow visits -> final sign/hits (no concurrent writers)
+__global__ void fold_kernel(uint2* __restrict__ cells, int64_t n, uint32_t h_max, uint32_t t_occ) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t y = cells[i].y;
+    if (y >> kPendShift) cells[i].y = fold_meta(y, h_max, t_occ);
+  }
+}
+
 // distance cache of the z-range [z0, z1) only (chunked record loads)
 __global__ void rebuild_dist_range_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ dist, int64_t rows,
                                           int64_t nzp, int64_t z0, int64_t z1) {
@@ -197,6 +206,22 @@ int check_grid(const dbt_grid* g) {
   return grid_set_device(g);
 }
 
+}  // namespace
+
+// the records read back are final: order after the last integration launch
+// (it may have run on a caller's stream) and fold pending shadow visits
+int dbt::fold_pending(dbt_grid* g, cudaStream_t st) {
+  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_done, 0));
+  if (!g->pend) return DBT_OK;
+  fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells, g->n_cells, (uint32_t)g->pend_h_max,
+                                                      (uint32_t)g->pend_t_occ);
+  DBT_CHECK_LAUNCH("fold_kernel");
+  g->pend = false;
+  return DBT_OK;
+}
+
+namespace {
+
 // after host data replaced the records: rebuild the distance cache, drop
 // every stamp certificate (host writes carry no stamp history)
 int finish_host_write(dbt_grid* g) {
@@ -256,6 +281,7 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming);
   static_assert(sizeof(LaunchCounters) % 32 == 0, "counter block alignment");
   const size_t cnt_bytes = sizeof(LaunchCounters) + sizeof(ScanCounters) * kMaxScansPerLaunch;
   e = cudaMalloc(&g->d_lcnt, cnt_bytes);
@@ -299,6 +325,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->ev_meta) cudaEventDestroy(g->ev_meta);
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);
   if (g->ev_join) cudaEventDestroy(g->ev_join);
+  if (g->ev_done) cudaEventDestroy(g->ev_done);
   if (g->aux) cudaStreamDestroy(g->aux);
   if (g->stream && g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -308,7 +335,9 @@ int dbt_grid_destroy(dbt_grid* g) {
 int dbt_grid_reset(dbt_grid* g) {
   int rc = check_grid(g);
   if (rc) return rc;
+  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(g->stream, g->ev_done, 0));
   fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 2), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
+  g->pend = false;
   DBT_CHECK_LAUNCH("fill_cells_kernel");
   DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
@@ -335,6 +364,8 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
+  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(g->stream, g->ev_done, 0));
+  g->pend = false;  // every record of the slab is replaced
   uint8_t* st = (uint8_t*)g->d_stage;
   for (int64_t x = 0; x < lx; x += xs) {
     int64_t cx = std::min(xs, lx - x), n = cx * plane;
@@ -359,6 +390,8 @@ int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_
     return set_error(DBT_ERR_CONFIG, "download range outside the grid's slab");
   const int64_t lx = x_end - x_begin, plane = g->ny * g->nz;
   if (lx == 0) return DBT_OK;
+  rc = fold_pending(g, g->stream);
+  if (rc) return rc;
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
@@ -386,6 +419,7 @@ int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits)
 
 static int readout(dbt_grid* g, int mode, int32_t* pop, uint8_t* obs, double* sdf) {
   int rc = check_grid(g);
+  if (!rc) rc = fold_pending(g, g->stream);
   if (rc) return rc;
   const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
   const int64_t per = mode == 0 ? 4 : (mode == 1 ? 1 : 9);
@@ -423,6 +457,7 @@ int dbt_grid_counts(dbt_grid* g, int64_t* observed, int64_t* occupied) {
   int rc = check_grid(g);
   if (rc) return rc;
   rc = ensure_stage(g, 16);
+  if (!rc) rc = fold_pending(g, g->stream);
   if (rc) return rc;
   unsigned long long* d = (unsigned long long*)g->d_stage;
   DBT_CUDA(cudaMemsetAsync(d, 0, 16, g->stream));
@@ -453,6 +488,8 @@ int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, 
   uint32_t* dm = (uint32_t*)(st + 24 * n);
   uint8_t* ds = st + 28 * n;
   uint8_t* dh = ds + n;
+  rc = fold_pending(g, g->stream);
+  if (rc) return rc;
   DBT_CUDA(cudaMemcpyAsync(didx, xyz, 24 * n, cudaMemcpyHostToDevice, g->stream));
   gather_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, didx, n, g->x0, g->ny, g->nzp, dm, ds, dh);
   DBT_CHECK_LAUNCH("gather_kernel");
@@ -473,6 +510,7 @@ int dbt_grid_to_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, void*
   const int64_t plane = g->nx * g->ny;
   int64_t zs = std::max<int64_t>(1, std::min<int64_t>(z_end - z_begin, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
+  if (!rc) rc = fold_pending(g, g->stream);
   if (rc) return rc;
   uint2* st = (uint2*)g->d_stage;
   for (int64_t z = z_begin; z < z_end; z += zs) {
@@ -503,6 +541,7 @@ int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, con
   const int64_t plane = g->nx * g->ny;
   int64_t zs = std::max<int64_t>(1, std::min<int64_t>(z_end - z_begin, kStageBytes / (plane * 8)));
   rc = ensure_stage(g, zs * plane * 8);
+  if (!rc) rc = fold_pending(g, g->stream);  // records outside the range stay
   if (rc) return rc;
   uint2* st = (uint2*)g->d_stage;
   for (int64_t z = z_begin; z < z_end; z += zs) {

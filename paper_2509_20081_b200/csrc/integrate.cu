@@ -93,24 +93,19 @@ constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
 constexpr int kEpochShift = 52;
 constexpr uint32_t kMaxEpoch = 4095;
 
-// one shadow visit on a record's sign/hits word (integrator.py:154-159):
-// h += (h < h_max); sign byte <- 0 (occupied) when the new h >= T
-__device__ __forceinline__ uint32_t shadow_step(uint32_t old, uint32_t h_max, uint32_t t_occ) {
-  const uint32_t h = (old >> 8) & 0xFFu;
-  const uint32_t hn = h + (h < h_max ? 1u : 0u);
-  uint32_t nw = (old & ~kHitsByte) | (hn << 8);
-  if (hn >= t_occ) nw &= ~kSignByte;
-  return nw;
-}
-
-__device__ __forceinline__ void shadow_update(uint32_t* p, uint32_t h_max, uint32_t t_occ) {
-  uint32_t old = *p;
+// one shadow visit: count it in the record's pending field (engine.cuh);
+// the visit that takes the count to 2^15 folds the record right away, so the
+// 16-bit field never overflows
+__device__ __forceinline__ void shadow_add(uint32_t* p, uint32_t h_max, uint32_t t_occ) {
+  const uint32_t old = atomicAdd(p, 1u << kPendShift);
+  if ((old >> kPendShift) + 1 != kPendFold) return;
+  uint32_t cur = __ldcg(p);
   while (true) {
-    const uint32_t nw = shadow_step(old, h_max, t_occ);
-    if (nw == old) break;
-    uint32_t prev = atomicCAS(p, old, nw);
-    if (prev == old) break;
-    old = prev;
+    const uint32_t nw = fold_meta(cur, h_max, t_occ);
+    if (nw == cur) break;
+    const uint32_t prev = atomicCAS(p, cur, nw);
+    if (prev == cur) break;
+    cur = prev;
   }
 }
 
@@ -273,32 +268,17 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
         cur = __ldcg(&a.hkey[h]);
       }
       if (a.fuse_shadow) {
-        // up to 8 shadow cells: independent loads, then independent first CAS
-        // attempts; only a lost race takes the retry loop
+        // up to 8 shadow cells, their visits counted independently
         const int b0 = a.sstart[ba * a.b_el + be], nsh = a.sstart[ba * a.b_el + be + 1] - b0;
-        uint32_t* ptr[8];
-        uint32_t old[8], prev[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          ptr[k] = nullptr;
-          if (k < nsh) {
-            const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
-            const int64_t gx = cx + o.x;
-            if (gx >= a.x0 && gx < a.x1)
-              ptr[k] = &a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y;
-          }
-          old[k] = ptr[k] ? __ldcg(ptr[k]) : 0u;
+          if (k >= nsh) break;
+          const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
+          const int64_t gx = cx + o.x;
+          if (gx >= a.x0 && gx < a.x1)
+            shadow_add(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+                       (uint32_t)a.t_occ);
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          prev[k] = old[k];
-          if (!ptr[k]) continue;
-          const uint32_t nw = shadow_step(old[k], (uint32_t)a.h_max, (uint32_t)a.t_occ);
-          if (nw != old[k]) prev[k] = atomicCAS(ptr[k], old[k], nw);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (ptr[k] && prev[k] != old[k]) shadow_update(ptr[k], (uint32_t)a.h_max, (uint32_t)a.t_occ);
       }
       if (a.first_return) atomicMin(&a.hmin[h], (uint32_t)i);
       a.slot[i] = (uint32_t)h;
@@ -378,8 +358,8 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     unpack_center(c, cx, cy, cz);
     int64_t gx = cx + o.x;
     if (gx < a.x0 || gx >= a.x1) continue;
-    shadow_update(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
-                  (uint32_t)a.t_occ);
+    shadow_add(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+               (uint32_t)a.t_occ);
   }
 }
 
@@ -880,6 +860,16 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   // launch + per-scan counters: one contiguous block, one memset
   DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
   if (n == 0) return DBT_OK;
+  // pending shadow visits were counted under other (h_max, T): fold them first
+  if (g->pend && (g->pend_h_max != p->h_max || g->pend_t_occ != p->t_occ)) {
+    rc = fold_pending(g, st);
+    if (rc) return rc;
+  }
+  if (b->max_shadow > 0) {
+    g->pend = true;
+    g->pend_h_max = p->h_max;
+    g->pend_t_occ = p->t_occ;
+  }
   const int64_t hcap = [&] {
     int64_t w = 1024;
     while (w < 2 * n) w <<= 1;
@@ -1044,6 +1034,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");
     if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
+    DBT_CUDA(cudaEventRecord(g->ev_done, st));
     return DBT_OK;
   }
   const int CH = b->chunks_per_row;
@@ -1084,6 +1075,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("sweep_kernel");
   if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
+  DBT_CUDA(cudaEventRecord(g->ev_done, st));
   return DBT_OK;
 }
 

@@ -387,6 +387,59 @@ class TestSnapshot:
         assert np.array_equal(g2.mask, og.mask) and np.array_equal(g2.sign, og.sign) and np.array_equal(g2.hits, og.hits)
 
 
+class TestPendingShadowVisits:
+    """Shadow visits are counted in the record's spare bytes and folded before
+    reads (engine.cuh): overflow fold, parameter changes, partial reads."""
+
+    def test_count_crossing_fold_threshold(self):
+        bank = build_kernel_bank(shadow_radius=1)
+        p = np.array([[2.45, 2.45, 2.45]])
+        pm = np.repeat(p, 40_000, axis=0)            # 40k visits of the same cells in one launch
+        sens = pm - np.array([1.0, 0.0, 0.0])
+        for h_max, t in ((255, 2), (7, 3)):
+            g = new_grid((48, 48, 48), 0.1)
+            params = IntegrationParams(h_max=h_max, t_occ=t)
+            integrate_points(g, bank, pm, sens, params)
+            integrate_points(g, bank, pm[:3], sens[:3], params)  # more visits after the in-kernel fold
+            og = oracle.OracleGrid((48, 48, 48), 0.1, (0, 0, 0))
+            ob = oracle.OracleBank.from_bank(bank)
+            oracle.integrate_points_map(og, ob, pm, sens, h_max=h_max, t_occ=t)
+            oracle.integrate_points_map(og, ob, pm[:3], sens[:3], h_max=h_max, t_occ=t)
+            assert np.array_equal(g.hits, og.hits) and np.array_equal(g.sign, og.sign)
+            assert np.array_equal(g.mask, og.mask)
+
+    def test_parameter_change_folds_pending_visits_first(self):
+        bank = build_kernel_bank(shadow_radius=2)
+        rng = np.random.default_rng(12)
+        frames = [rng.uniform(1.15, 3.6, size=(400, 3)) for _ in range(4)]
+        plist = [(7, 3), (7, 3), (200, 2), (2, 1)]
+        g = new_grid((48, 48, 48), 0.1)
+        og = oracle.OracleGrid((48, 48, 48), 0.1, (0, 0, 0))
+        ob = oracle.OracleBank.from_bank(bank)
+        for pts, (hm, t) in zip(frames, plist):
+            integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams(h_max=hm, t_occ=t))
+            oracle.integrate_frame(og, ob, pts, np.eye(4), h_max=hm, t_occ=t)
+        assert np.array_equal(g.hits, og.hits) and np.array_equal(g.sign, og.sign)
+
+    def test_every_read_path_sees_folded_records(self):
+        bank = build_kernel_bank(shadow_radius=1)
+        rng = np.random.default_rng(13)
+        pts = rng.uniform(1.15, 3.6, size=(500, 3))
+        og = oracle.OracleGrid((48, 48, 48), 0.1, (0, 0, 0))
+        oracle.integrate_frame(og, oracle.OracleBank.from_bank(bank), pts, np.eye(4))
+        occ = og.sign == 0
+        readers = [
+            lambda g: np.array_equal(g.download_range(5, 30)[2], og.hits[5:30]),
+            lambda g: G.grid_counts(g)[1] == int(occ.sum()),
+            lambda g: np.array_equal(G.observed_array(g), ~((og.mask == G.FULL_MASK) & (og.hits == 0))),
+            lambda g: np.array_equal(G.to_records(g)["hits"], og.hits.ravel(order="F")),
+        ]
+        for read in readers:
+            g = new_grid((48, 48, 48), 0.1)
+            integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+            assert read(g)
+
+
 class TestSweepPaths:
     """The symmetric-kernel sweep (base-pair table) and the generic sweep
     (distinct-row table) must both reproduce the reference stamping."""
