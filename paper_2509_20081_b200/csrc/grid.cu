@@ -211,7 +211,11 @@ int check_grid(const dbt_grid* g) {
 // the records read back are final: order after the last integration launch
 // (it may have run on a caller's stream) and fold pending shadow visits
 int dbt::fold_pending(dbt_grid* g, cudaStream_t st) {
-  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_done, 0));
+  if (g->last_st != st) {
+    // the last launch ran on a caller's stream (which may be gone by now)
+    DBT_CUDA(cudaDeviceSynchronize());
+    g->last_st = st;
+  }
   if (!g->pend) return DBT_OK;
   fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells, g->n_cells, (uint32_t)g->pend_h_max,
                                                       (uint32_t)g->pend_t_occ);
@@ -281,7 +285,7 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming);
+  g->last_st = g->stream;
   static_assert(sizeof(LaunchCounters) % 32 == 0, "counter block alignment");
   const size_t cnt_bytes = sizeof(LaunchCounters) + sizeof(ScanCounters) * kMaxScansPerLaunch;
   e = cudaMalloc(&g->d_lcnt, cnt_bytes);
@@ -325,7 +329,6 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->ev_meta) cudaEventDestroy(g->ev_meta);
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);
   if (g->ev_join) cudaEventDestroy(g->ev_join);
-  if (g->ev_done) cudaEventDestroy(g->ev_done);
   if (g->aux) cudaStreamDestroy(g->aux);
   if (g->stream && g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -335,7 +338,10 @@ int dbt_grid_destroy(dbt_grid* g) {
 int dbt_grid_reset(dbt_grid* g) {
   int rc = check_grid(g);
   if (rc) return rc;
-  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(g->stream, g->ev_done, 0));
+  if (g->last_st != g->stream) {
+    DBT_CUDA(cudaDeviceSynchronize());
+    g->last_st = g->stream;
+  }
   fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 2), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
   g->pend = false;
   DBT_CHECK_LAUNCH("fill_cells_kernel");
@@ -364,7 +370,10 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
-  if (g->ev_done) DBT_CUDA(cudaStreamWaitEvent(g->stream, g->ev_done, 0));
+  if (g->last_st != g->stream) {
+    DBT_CUDA(cudaDeviceSynchronize());
+    g->last_st = g->stream;
+  }
   g->pend = false;  // every record of the slab is replaced
   uint8_t* st = (uint8_t*)g->d_stage;
   for (int64_t x = 0; x < lx; x += xs) {

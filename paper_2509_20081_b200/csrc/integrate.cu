@@ -1034,7 +1034,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");
     if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
-    DBT_CUDA(cudaEventRecord(g->ev_done, st));
+    g->last_st = st;
     return DBT_OK;
   }
   const int CH = b->chunks_per_row;
@@ -1075,7 +1075,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("sweep_kernel");
   if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
-  DBT_CUDA(cudaEventRecord(g->ev_done, st));
+  g->last_st = st;
   return DBT_OK;
 }
 
