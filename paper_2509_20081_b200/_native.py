@@ -82,13 +82,13 @@ SIGNATURES = {
     "dbt_bank_create": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int,
                                        ctypes.POINTER(_vp)]),
     "dbt_bank_destroy": (ctypes.c_int, [_vp]),
-    "dbt_integrate_frame": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _c_dp,
+    "dbt_integrate_frame": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp,
                                            ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
-    "dbt_integrate_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _c_dp,
+    "dbt_integrate_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _vp,
                                            ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
     "dbt_integrate_points_map": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.POINTER(Params),
                                                 ctypes.POINTER(Stats), _vp]),
-    "dbt_integrate_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _c_dp,
+    "dbt_integrate_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _vp,
                                             ctypes.POINTER(Params), _vp]),
     "dbt_stats_read": (ctypes.c_int, [_vp, ctypes.POINTER(Stats), ctypes.c_int32]),
     "dbt_synchronize": (ctypes.c_int, [_vp]),
@@ -146,5 +146,13 @@ def default_device() -> int:
     return int(os.environ.get("DBT_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 
 
+_params_cache: dict = {}
+
+
 def make_params(h_max=255, t_occ=2, downsample=1, first_return=False, flags=0) -> Params:
-    return Params(int(h_max), int(t_occ), int(downsample), int(bool(first_return)), int(flags), 0)
+    """dbt_params for these values (cached: the struct is read-only for the engine)."""
+    key = (int(h_max), int(t_occ), int(downsample), int(bool(first_return)), int(flags))
+    p = _params_cache.get(key)
+    if p is None:
+        p = _params_cache[key] = Params(*key, 0)
+    return p

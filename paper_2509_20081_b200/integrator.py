@@ -160,7 +160,7 @@ def motion_compensate(scan: ScanFrame, mode: str) -> ScanFrame:
 
 def _pose_arg(pose: np.ndarray):
     p = np.ascontiguousarray(pose, dtype=np.float64).reshape(16)
-    return p, p.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    return p, ctypes.c_void_p(p.ctypes.data)
 
 
 def integrate_point(grid: VoxelGrid, bank: KernelBank, p_map, sensor_pos, params: IntegrationParams) -> str:
@@ -265,7 +265,7 @@ def integrate_frames(grid: VoxelGrid, bank: KernelBank, scans, params: Integrati
     _native.check(_native.lib().dbt_integrate_batch(
         grid.handle, bank.device_handle(grid.device), _native.ptr(pts), dtype,
         counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(scans),
-        poses.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(prm), out))
+        ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm), out))
     grid.pull_host()
     el = (time.perf_counter() - t0) * 1e3
     return [FrameStats.from_native(out[i], el if i == 0 else 0.0) for i in range(len(scans))]

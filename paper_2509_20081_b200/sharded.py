@@ -119,7 +119,7 @@ class ShardedGrid:
         _native.check(_native.lib().dbt_integrate_device(
             self.local.handle, bank.device_handle(self.local.device), ctypes.c_void_p(points.data_ptr()), dtype,
             counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
-            poses.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(prm),
+            ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm),
             ctypes.c_void_p(st.cuda_stream)))
 
     def stats(self) -> list:

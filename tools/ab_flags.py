@@ -34,7 +34,7 @@ for name, flags in variants.items():
             a.record()
             _native.check(L.dbt_integrate_device(g.handle, bank.device_handle(0), ctypes.c_void_p(s.data_ptr()), 0,
                                                  cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 1,
-                                                 pose.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                                 ctypes.c_void_p(pose.ctypes.data),
                                                  ctypes.byref(prm), ctypes.c_void_p(0)))
             b.record()
             ev.append((a, b))

@@ -47,7 +47,7 @@ for rep in range(2):
         cst = _native.Stats()
         t3 = time.perf_counter()
         _native.check(L.dbt_integrate_frame(g.handle, bank.device_handle(0), _native.ptr(pts), dt_, pts.shape[0],
-                                            pose.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            ctypes.c_void_p(pose.ctypes.data),
                                             ctypes.byref(prm), ctypes.byref(cst)))
         t4 = time.perf_counter()
         if rep == 1 and k >= 10:
