@@ -154,6 +154,12 @@ DBT_API int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* poin
 DBT_API int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
                         const int64_t* counts, int32_t n_scans, const double* poses,
                         const dbt_params* p, dbt_stats* out);
+/* The same batch with one host pointer per scan (no host concatenation):
+ * pinned scans are read zero-copy by preprocessing through a device table of
+ * scan pointers, pageable ones are staged with one H2D copy each. */
+DBT_API int dbt_integrate_scans(dbt_grid* g, const dbt_bank* b, const void* const* points, int dtype,
+                        const int64_t* counts, int32_t n_scans, const double* poses,
+                        const dbt_params* p, dbt_stats* out);
 /* Map-frame points with per-point sensor positions (integrate_point,
  * integrator.py:163-189); outcome[i] = 1 applied, 0 discarded (nullable). */
 DBT_API int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map,

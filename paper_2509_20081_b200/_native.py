@@ -86,6 +86,8 @@ SIGNATURES = {
                                            ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
     "dbt_integrate_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _vp,
                                            ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
+    "dbt_integrate_scans": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _vp,
+                                           ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
     "dbt_integrate_points_map": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.POINTER(Params),
                                                 ctypes.POINTER(Stats), _vp]),
     "dbt_integrate_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _c_i64p, ctypes.c_int32, _vp,

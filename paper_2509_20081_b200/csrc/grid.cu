@@ -291,7 +291,8 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
   e = cudaMalloc(&g->d_lcnt, cnt_bytes);
   if (e == cudaSuccess) g->d_scnt = reinterpret_cast<ScanCounters*>(g->d_lcnt + 1);
   // per-launch metadata, packed: scan_off (S+1) | src_off (S+1) | poses (12 S)
-  const size_t meta_bytes = sizeof(int64_t) * (2 * (kMaxScansPerLaunch + 1) + 12 * kMaxScansPerLaunch);
+  // scan_off (S+1) | src_off (S+1) | poses (12 S) | scan pointers (S)
+  const size_t meta_bytes = sizeof(int64_t) * (2 * (kMaxScansPerLaunch + 1) + 13 * kMaxScansPerLaunch);
   if (e == cudaSuccess) e = cudaMalloc(&g->d_scan_off, meta_bytes);
   if (e == cudaSuccess) e = cudaHostAlloc(&g->h_lcnt, cnt_bytes, cudaHostAllocDefault);
   if (e == cudaSuccess) g->h_scnt = reinterpret_cast<ScanCounters*>(g->h_lcnt + 1);

@@ -55,6 +55,7 @@ struct PrepArgs {
   const int64_t* scan_off;
   const int64_t* src_off;
   const double* poses;  // S x 12 : R row-major (9), t (3)
+  const uint64_t* scan_ptr;  // S device pointers, one per scan (nullptr: pts + src_off)
   int64_t nx, ny, nz;
   double vs, ox, oy, oz;
   int R, b_az, b_el;
@@ -180,16 +181,17 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
       src = i * a.ds;
     } else {
       s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
-      src = a.src_off[s] + (i - a.scan_off[s]) * a.ds;
+      src = (a.scan_ptr ? 0 : a.src_off[s]) + (i - a.scan_off[s]) * a.ds;
     }
+    const void* pts = a.scan_ptr && !a.inline_meta ? (const void*)a.scan_ptr[s] : a.pts;
     double p0, p1, p2;
     if (a.dtype == DBT_F32) {
-      const float* q = (const float*)a.pts + 3 * src;
+      const float* q = (const float*)pts + 3 * src;
       p0 = q[0];
       p1 = q[1];
       p2 = q[2];
     } else {
-      const double* q = (const double*)a.pts + 3 * src;
+      const double* q = (const double*)pts + 3 * src;
       p0 = q[0];
       p1 = q[1];
       p2 = q[2];
@@ -807,7 +809,8 @@ int validate_params(const dbt_params* p) {
 // poses are host arrays. map_sensor (device) selects the map-frame mode.
 int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtype,
                      const int64_t* counts, int S, const double* poses, const dbt_params* p,
-                     const double* d_map_sensor, int8_t* d_outcome, cudaStream_t st) {
+                     const double* d_map_sensor, int8_t* d_outcome, cudaStream_t st,
+                     const void* const* scan_ptrs) {
   if (S < 1 || S > kMaxScansPerLaunch) return set_error(DBT_ERR_CONFIG, "scan count per launch out of range");
   if (b->device != g->device) return set_error(DBT_ERR_CONFIG, "bank and grid live on different devices");
   if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
@@ -832,8 +835,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   if (rc) return rc;
   const bool inline_meta = (S == 1);
   if (!inline_meta) {
-    // one H2D copy of [scan_off (S+1) | src_off (S+1) | poses (12 S)] from
-    // pinned staging; wait until the previous launch consumed it
+    // one H2D copy of [scan_off (S+1) | src_off (S+1) | poses (12 S) |
+    // scan pointers (S)] from pinned staging; wait until the previous launch
+    // consumed it
     DBT_CUDA(cudaEventSynchronize(g->ev_meta));
     int64_t* h_scan = g->h_meta;
     int64_t* h_src = h_scan + (S + 1);
@@ -853,7 +857,11 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
         D[11] = P[11];
       }
     }
-    const size_t bytes = (size_t)(2 * (S + 1) + (d_map_sensor ? 0 : 12 * S)) * 8;
+    if (scan_ptrs) {
+      uint64_t* h_ptr = reinterpret_cast<uint64_t*>(h_pose + 12 * S);
+      for (int s = 0; s < S; ++s) h_ptr[s] = (uint64_t)(uintptr_t)scan_ptrs[s];
+    }
+    const size_t bytes = (size_t)(2 * (S + 1) + (d_map_sensor ? 0 : 12 * S) + (scan_ptrs ? S : 0)) * 8;
     DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, bytes, cudaMemcpyHostToDevice, st));
     DBT_CUDA(cudaEventRecord(g->ev_meta, st));
   }
@@ -910,6 +918,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.scan_off = g->d_scan_off;
   pa.src_off = g->d_scan_off + (S + 1);
   pa.poses = reinterpret_cast<const double*>(g->d_scan_off + 2 * (S + 1));
+  pa.scan_ptr = scan_ptrs ? reinterpret_cast<const uint64_t*>(g->d_scan_off + 2 * (S + 1) + 12 * S) : nullptr;
   pa.inline_meta = inline_meta ? 1 : 0;
   if (inline_meta && !d_map_sensor) {
     for (int r = 0; r < 3; ++r)
@@ -1150,7 +1159,72 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
     DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
     d_src = g->d_raw;
   }
-  rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st);
+  rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st, nullptr);
+  if (rc) return rc;
+  rc = fetch_counters(g, st);
+  if (rc) return rc;
+  DBT_CUDA(cudaEventRecord(g->ev_b, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  fill_stats(g, p, out, S);
+  float dms = 0.f;
+  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
+  out[0].device_ms = dms;
+  out[0].elapsed_ms = now_ms() - t0;
+  return DBT_OK;
+}
+
+// S scans given as S host pointers (no concatenation on the host): pinned
+// scans are read zero-copy by the prep kernel through a device table of scan
+// pointers, pageable ones are staged each with one H2D copy.
+int integrate_scans_host(dbt_grid* g, const dbt_bank* b, const void* const* points, int dtype,
+                         const int64_t* counts, int S, const double* poses, const dbt_params* p, dbt_stats* out) {
+  double t0 = now_ms();
+  int rc = check(g, b);
+  if (!rc) rc = validate_params(p);
+  if (rc) return rc;
+  if (S < 1 || S > kMaxScansPerLaunch) return set_error(DBT_ERR_CONFIG, "scan count per launch out of range");
+  int64_t total = 0;
+  for (int s = 0; s < S; ++s) {
+    if (counts[s] < 0) return set_error(DBT_ERR_CONFIG, "negative point count");
+    total += counts[s];
+  }
+  if (total == 0) {
+    for (int s = 0; s < S; ++s) std::memset(&out[s], 0, sizeof(dbt_stats));
+    out[0].elapsed_ms = now_ms() - t0;
+    return DBT_OK;
+  }
+  const size_t esz = dtype == DBT_F32 ? 12 : 24;
+  cudaStream_t st = g->stream;
+  std::vector<const void*> dptr(S, nullptr);
+  int64_t staged = 0;
+  for (int s = 0; s < S; ++s) {
+    if (counts[s] == 0 || (p->flags & DBT_FLAG_STAGE_COPY)) continue;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, points[s]) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer != nullptr)
+      dptr[s] = at.devicePointer;
+    else
+      cudaGetLastError();
+  }
+  for (int s = 0; s < S; ++s)
+    if (!dptr[s]) staged += counts[s];
+  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  if (staged) {
+    rc = stage_raw(g, staged * (int64_t)esz);
+    if (rc) return rc;
+    int64_t off = 0;
+    for (int s = 0; s < S; ++s) {
+      if (dptr[s]) continue;
+      char* d = (char*)g->d_raw + off * esz;
+      if (counts[s]) DBT_CUDA(cudaMemcpyAsync(d, points[s], counts[s] * esz, cudaMemcpyHostToDevice, st));
+      dptr[s] = d;
+      off += counts[s];
+    }
+  }
+  if (S == 1)
+    rc = launch_integrate(g, b, dptr[0], dtype, counts, 1, poses, p, nullptr, nullptr, st, nullptr);
+  else
+    rc = launch_integrate(g, b, nullptr, dtype, counts, S, poses, p, nullptr, nullptr, st, dptr.data());
   if (rc) return rc;
   rc = fetch_counters(g, st);
   if (rc) return rc;
@@ -1167,6 +1241,12 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
 }  // namespace
 
 extern "C" {
+
+int dbt_integrate_scans(dbt_grid* g, const dbt_bank* b, const void* const* points, int dtype,
+                        const int64_t* counts, int32_t n_scans, const double* poses, const dbt_params* p,
+                        dbt_stats* out) {
+  return integrate_scans_host(g, b, points, dtype, counts, n_scans, poses, p, out);
+}
 
 int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
                         const double pose[16], const dbt_params* p, dbt_stats* out) {
@@ -1199,7 +1279,7 @@ int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map
   DBT_CUDA(cudaMemcpyAsync(g->d_raw, p_map, n * 24, cudaMemcpyHostToDevice, st));
   DBT_CUDA(cudaMemcpyAsync(g->d_sensor, sensor, n * 24, cudaMemcpyHostToDevice, st));
   rc = launch_integrate(g, b, g->d_raw, DBT_F64, &n, 1, nullptr, &q, g->d_sensor,
-                        outcome ? g->d_outcome : nullptr, st);
+                        outcome ? g->d_outcome : nullptr, st, nullptr);
   if (rc) return rc;
   rc = fetch_counters(g, st);
   if (rc) return rc;
@@ -1221,7 +1301,7 @@ int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, i
   if (!rc) rc = validate_params(p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
-  rc = launch_integrate(g, b, d_points, dtype, counts, n_scans, poses, p, nullptr, nullptr, st);
+  rc = launch_integrate(g, b, d_points, dtype, counts, n_scans, poses, p, nullptr, nullptr, st, nullptr);
   if (rc) return rc;
   return fetch_counters(g, st);
 }

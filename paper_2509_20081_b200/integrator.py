@@ -254,16 +254,19 @@ def integrate_frames(grid: VoxelGrid, bank: KernelBank, scans, params: Integrati
     payloads = [s.device_payload() for s in scans]
     dtype = _native.DBT_F32 if all(d == _native.DBT_F32 for _, d in payloads) else _native.DBT_F64
     np_dt = np.float32 if dtype == _native.DBT_F32 else np.float64
-    pts = np.ascontiguousarray(np.concatenate([p.astype(np_dt, copy=False) for p, _ in payloads]))
-    counts = np.array([p.shape[0] for p, _ in payloads], dtype=np.int64)
+    # one pointer per scan: no host concatenation (pinned scans are read
+    # zero-copy by the device, pageable ones staged scan by scan)
+    arrays = [p if p.dtype == np_dt else p.astype(np_dt) for p, _ in payloads]
+    ptrs = (ctypes.c_void_p * len(arrays))(*[a.ctypes.data for a in arrays])
+    counts = np.array([a.shape[0] for a in arrays], dtype=np.int64)
     poses = np.ascontiguousarray(np.stack([s.pose for s in scans]).reshape(-1))
     grid.h_max = params.h_max
     grid.t_occ = params.t_occ
     prm = params.native(downsample=downsample)
     out = (_native.Stats * len(scans))()
     grid.push_host()
-    _native.check(_native.lib().dbt_integrate_batch(
-        grid.handle, bank.device_handle(grid.device), _native.ptr(pts), dtype,
+    _native.check(_native.lib().dbt_integrate_scans(
+        grid.handle, bank.device_handle(grid.device), ptrs, dtype,
         counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(scans),
         ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm), out))
     grid.pull_host()

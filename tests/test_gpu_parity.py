@@ -440,6 +440,41 @@ class TestPendingShadowVisits:
             assert read(g)
 
 
+class TestPinnedScans:
+    """Scans in pinned host memory are read zero-copy by preprocessing, one
+    device pointer per scan for batches (dbt_integrate_scans): same grid as
+    the pageable path and the reference."""
+
+    def test_pinned_batch_and_single_match_golden(self, golden):
+        import ctypes
+
+        c = next(c for c in CONFIG if c.name == "cfg2_scans0-2")
+        L = _native.lib()
+        bufs, pinned = [], []
+        for p, _ in c.frames:
+            p = np.ascontiguousarray(p, dtype=np.float32)
+            buf = ctypes.c_void_p()
+            _native.check(L.dbt_host_alloc(p.nbytes, ctypes.byref(buf)))
+            arr = np.ctypeslib.as_array((ctypes.c_float * p.size).from_address(buf.value)).reshape(p.shape)
+            arr[...] = p
+            bufs.append(buf)
+            pinned.append(arr)
+        try:
+            bank = build_kernel_bank(**c.bank)
+            for batch in (True, False):
+                g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 42)
+                frames = [ScanFrame(points=a, pose=pose) for a, (_, pose) in zip(pinned, c.frames)]
+                if batch:
+                    sts = integrate_frames(g, bank, frames, IntegrationParams())
+                else:
+                    sts = [integrate_frame(g, bank, f, IntegrationParams()) for f in frames]
+                stats = [[x.points_in, x.points_discarded, x.voxels_written] for x in sts]
+                check(c, golden, g, stats, None, batch=batch)
+        finally:
+            for b in bufs:
+                L.dbt_host_free(b)
+
+
 class TestSweepPaths:
     """The symmetric-kernel sweep (base-pair table) and the generic sweep
     (distinct-row table) must both reproduce the reference stamping."""
