@@ -633,38 +633,48 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
     __syncthreads();
     // next batch index: its atomic overlaps phase B
     if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
-    // ===== phase B: the block sweeps the queued rows, one thread per row =====
+    // ===== phase B: the block sweeps the queued rows, one thread per row,
+    // two rows' chunk loads in flight per thread =====
     const int nq = q_n;
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-      const uint64_t task = queue[i];
-      const int64_t rbase = (int64_t)(task & ((1ull << 37) - 1)) << 3;
-      const int c0 = (int)((task >> 37) & 3), c1 = (int)((task >> 39) & 3);
-      const uint2* drow = dtab + (int)(task >> 41);
-      uint2 w[4], d8[4];
+    for (int i = threadIdx.x; i < nq; i += 2 * blockDim.x) {
+      uint2 w[2][4], d8[2][4];
+      int64_t rb[2];
+      int cb[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool act = c0 + j <= c1;
-        const uint2 dv = __ldg(drow + (act ? c0 + j : c0));
-        d8[j] = act ? dv : make_uint2(0x40404040u, 0x40404040u);
-        w[j] = *reinterpret_cast<const uint2*>(a.dist + rbase + 8 * (act ? c0 + j : c0));
-      }
+      for (int r = 0; r < 2; ++r) {
+        const int qi = i + r * blockDim.x;
+        const uint64_t task = qi < nq ? queue[qi] : 0ull;
+        rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
+        const int c0 = (int)((task >> 37) & 3), c1 = qi < nq ? (int)((task >> 39) & 3) : -1;
+        cb[r] = c0;
+        const uint2* drow = dtab + (int)(task >> 41);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t lt0 = ((w[j].x | 0x80808080u) - d8[j].x) & 0x80808080u;
-        const uint32_t lt1 = ((w[j].y | 0x80808080u) - d8[j].y) & 0x80808080u;
-        if (lt0 | lt1) {
-          const int64_t off = rbase + 8 * (c0 + j);
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            const uint32_t lt = b < 4 ? lt0 : lt1;
-            if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
-            const uint32_t d = (((b < 4 ? d8[j].x : d8[j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-            atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
-            ++changed;
-            a.dist[off + b] = (uint8_t)d;
-          }
+        for (int j = 0; j < 4; ++j) {
+          const bool act = c0 + j <= c1;
+          d8[r][j] = act ? __ldg(drow + c0 + j) : make_uint2(0x40404040u, 0x40404040u);
+          // inactive chunks read one shared dummy sector
+          w[r][j] = *reinterpret_cast<const uint2*>(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
         }
       }
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t lt0 = ((w[r][j].x | 0x80808080u) - d8[r][j].x) & 0x80808080u;
+          const uint32_t lt1 = ((w[r][j].y | 0x80808080u) - d8[r][j].y) & 0x80808080u;
+          if (lt0 | lt1) {
+            const int64_t off = rb[r] + 8 * (cb[r] + j);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              const uint32_t lt = b < 4 ? lt0 : lt1;
+              if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
+              const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
+              atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
+              ++changed;
+              a.dist[off + b] = (uint8_t)d;
+            }
+          }
+        }
     }
     __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
