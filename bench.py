@@ -215,7 +215,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(w, batch):
+def config_desc(w, batch, interleave=0):
     scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
     return {"workload": f"config {w.config}: {scene}, {w.n_scans}-scan trajectory, {w.beams}x{w.n_az} float32 "
                         f"returns/scan, {w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]}"
@@ -224,7 +224,9 @@ def config_desc(w, batch):
             "scans_per_step": batch,
             "step": f"{batch} scan(s) integrated into the trajectory grid in one launch",
             "l2": "flushed between steps (256 MB write)",
-            "parallelism": "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU"}
+            "parallelism": (f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks)"
+                            if interleave else
+                            "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU")}
 
 
 def main():
@@ -238,6 +240,8 @@ def main():
     ap.add_argument("--max-scans", type=int, default=None, help="distinct scans to generate (default: all needed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
+    ap.add_argument("--interleave", type=int, default=None,
+                    help="x-block width of interleaved sharding (default 64 when N > 1, contiguous at N = 1)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -274,7 +278,8 @@ def main():
     dev = f"cuda:{local}"
 
     # ---------------- device-resident value --------------------------------
-    sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local)
+    ilv = args.interleave if args.interleave is not None else (64 if world > 1 else 0)
+    sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local, interleave=ilv or None)
     # one device buffer per step-batch (concatenated scans), built before timing
     batches = []
     for j in range(steps_per_pass):
@@ -395,7 +400,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w, B),
+        "config": config_desc(w, B, ilv),
         "gpu_launches": int(launches),
         "kernels": kernels,
         "profiled_step_ms": prof_ms / args.steps,

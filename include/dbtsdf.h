@@ -100,6 +100,16 @@ DBT_API int dbt_device_count(int* out);
  * pass 0, dims[0] for a whole grid. */
 DBT_API int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origin[3],
                     int device, int64_t slab_x0, int64_t slab_x1, dbt_grid** out);
+/* Interleaved sharding (LiDAR density falls off as 1/r^2,
+ * so contiguous slabs overload the ranks near the sensor): this part owns the
+ * x-planes whose block x / width is congruent to `part` mod `parts`, stored
+ * in increasing x order. Host arrays of such a grid ("slab arrays" below)
+ * hold its owned planes in that order. */
+DBT_API int dbt_grid_create_interleaved(const int64_t dims[3], double voxel_size, const double origin[3],
+                    int device, int64_t width, int32_t parts, int32_t part, dbt_grid** out);
+/* owned_planes = number of x-planes stored; xmap = {x0, x1, width (0 =
+ * contiguous slab), parts, part}. */
+DBT_API int dbt_grid_layout(const dbt_grid* g, int64_t* owned_planes, int64_t xmap[5]);
 DBT_API int dbt_grid_destroy(dbt_grid* g);
 DBT_API int dbt_grid_reset(dbt_grid* g);
 DBT_API int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* device_bytes);
@@ -108,7 +118,8 @@ DBT_API int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], i
  * record is the reference's 8-byte record). */
 DBT_API int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits);
 DBT_API int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits);
-/* Same for the global x-planes [x_begin, x_end) (inside the slab): arrays of
+/* Same for the global x-planes [x_begin, x_end) (owned and stored
+ * contiguously: inside the slab, or inside one interleave block): arrays of
  * shape (x_end-x_begin, ny, nz). Streams huge grids in pieces. */
 DBT_API int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
                                     uint8_t* hits);

@@ -63,6 +63,9 @@ SIGNATURES = {
     "dbt_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "dbt_grid_create": (ctypes.c_int, [_c_i64p, ctypes.c_double, _c_dp, ctypes.c_int, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "dbt_grid_create_interleaved": (ctypes.c_int, [_c_i64p, ctypes.c_double, _c_dp, ctypes.c_int, ctypes.c_int64,
+                                                   ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]),
+    "dbt_grid_layout": (ctypes.c_int, [_vp, _c_i64p, _c_i64p]),
     "dbt_grid_destroy": (ctypes.c_int, [_vp]),
     "dbt_grid_reset": (ctypes.c_int, [_vp]),
     "dbt_grid_info": (ctypes.c_int, [_vp, _c_i64p, _c_i64p, _c_i64p]),

@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -88,6 +89,30 @@ __host__ __device__ inline void unpack_center(uint64_t c, int64_t& x, int64_t& y
   z = (int64_t)(c & m);
 }
 
+// Owned x-planes of a grid (multi-GPU sharding): every
+// global plane x in [x0, x1) when w == 0 (a contiguous slab), else the planes
+// of [x0, x1) whose block (x - x0) / w is congruent to r mod p (interleaved
+// slabs of w planes dealt round-robin over p ranks). Owned planes are stored
+// in increasing x order; local(x) is the storage plane or -1 when not owned.
+struct XMap {
+  int64_t x0 = 0, x1 = 0;
+  int64_t w = 0;
+  int32_t p = 1, r = 0;
+  __host__ __device__ __forceinline__ int64_t local(int64_t gx) const {
+    if (gx < x0 || gx >= x1) return -1;
+    if (w == 0) return gx - x0;
+    const int64_t u = gx - x0, blk = u / w;
+    if (blk % p != r) return -1;
+    return (blk / p) * w + (u - blk * w);
+  }
+  __host__ int64_t planes() const {
+    if (w == 0) return x1 - x0;
+    int64_t n = 0;
+    for (int64_t b = r; b * w < x1 - x0; b += p) n += std::min(w, x1 - x0 - b * w);
+    return n;
+  }
+};
+
 // Per-scan device counters (one entry per scan of a launch).
 struct ScanCounters {
   unsigned long long n_ok;       // non-discarded returns
@@ -132,12 +157,14 @@ struct dbt_bank {
 struct dbt_grid {
   int device = 0;
   int64_t nx = 0, ny = 0, nz = 0, nzp = 0;  // global dims, padded z stride
-  int64_t x0 = 0, x1 = 0;                   // owned slab
+  int64_t x0 = 0, x1 = 0;                   // owned x range (xm.x0, xm.x1)
+  dbt::XMap xm;                             // owned planes (contiguous or interleaved)
+  int64_t lx = 0;                           // owned plane count (storage x extent)
   double vs = 0, org[3] = {0, 0, 0};
   uint2* cells = nullptr;                   // authoritative voxel records
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
-  int64_t n_cells = 0;                      // (x1-x0)*ny*nzp
+  int64_t n_cells = 0;                      // lx*ny*nzp
   cudaStream_t stream = nullptr;
   bool own_stream = true;
 

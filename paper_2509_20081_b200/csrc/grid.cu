@@ -185,11 +185,11 @@ __global__ void from_records_kernel(uint2* __restrict__ cells, const uint2* __re
 }
 
 __global__ void gather_kernel(const uint2* __restrict__ cells, const int64_t* __restrict__ xyz, int64_t n,
-                              int64_t x0, int64_t ny, int64_t nzp, uint32_t* __restrict__ mask,
+                              XMap xm, int64_t ny, int64_t nzp, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 c = cells[((xyz[3 * i] - x0) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
+    const uint2 c = cells[(xm.local(xyz[3 * i]) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
     mask[i] = c.x;
     sign[i] = meta_sign(c.y);
     hits[i] = meta_hits(c.y);
@@ -241,8 +241,8 @@ int finish_host_write(dbt_grid* g) {
 
 extern "C" {
 
-int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origin[3], int device,
-                    int64_t slab_x0, int64_t slab_x1, dbt_grid** out) {
+static int create_grid(const int64_t dims[3], double voxel_size, const double origin[3], int device,
+                       const XMap& xm, dbt_grid** out) {
   *out = nullptr;
   for (int i = 0; i < 3; ++i)
     if (dims[i] < 1) return set_error(DBT_ERR_CONFIG, "grid dims must be three positive counts");
@@ -250,19 +250,24 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
     if (dims[i] > kMaxDim)
       return set_error(DBT_ERR_CONFIG, "grid dim exceeds 2^21-1 voxels (packed centre encoding)");
   if (!(voxel_size > 0.0)) return set_error(DBT_ERR_CONFIG, "voxel_size must be positive");
-  if (slab_x0 < 0 || slab_x1 > dims[0] || slab_x0 >= slab_x1)
+  if (xm.x0 < 0 || xm.x1 > dims[0] || xm.x0 >= xm.x1)
     return set_error(DBT_ERR_CONFIG, "slab [x0, x1) must be a non-empty range inside [0, nx)");
+  if (xm.w < 0 || xm.p < 1 || xm.r < 0 || xm.r >= xm.p)
+    return set_error(DBT_ERR_CONFIG, "interleave needs width >= 1 and 0 <= part < parts");
+  if (xm.planes() < 1) return set_error(DBT_ERR_CONFIG, "this part owns no x-plane of the grid");
   dbt_grid* g = new dbt_grid();
   g->device = device;
   g->nx = dims[0];
   g->ny = dims[1];
   g->nz = dims[2];
   g->nzp = (dims[2] + 7) & ~int64_t(7);
-  g->x0 = slab_x0;
-  g->x1 = slab_x1;
+  g->x0 = xm.x0;
+  g->x1 = xm.x1;
+  g->xm = xm;
+  g->lx = xm.planes();
   g->vs = voxel_size;
   for (int i = 0; i < 3; ++i) g->org[i] = origin[i];
-  g->n_cells = (g->x1 - g->x0) * g->ny * g->nzp;
+  g->n_cells = g->lx * g->ny * g->nzp;
   int rc = grid_set_device(g);
   if (rc) {
     delete g;
@@ -308,6 +313,38 @@ int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origi
     return rc;
   }
   *out = g;
+  return DBT_OK;
+}
+
+int dbt_grid_create(const int64_t dims[3], double voxel_size, const double origin[3], int device,
+                    int64_t slab_x0, int64_t slab_x1, dbt_grid** out) {
+  XMap xm;
+  xm.x0 = slab_x0;
+  xm.x1 = slab_x1;
+  return create_grid(dims, voxel_size, origin, device, xm, out);
+}
+
+int dbt_grid_create_interleaved(const int64_t dims[3], double voxel_size, const double origin[3], int device,
+                                int64_t width, int32_t parts, int32_t part, dbt_grid** out) {
+  *out = nullptr;
+  if (width < 1) return set_error(DBT_ERR_CONFIG, "interleave width must be >= 1");
+  XMap xm;
+  xm.x0 = 0;
+  xm.x1 = dims[0];
+  xm.w = width;
+  xm.p = parts;
+  xm.r = part;
+  return create_grid(dims, voxel_size, origin, device, xm, out);
+}
+
+int dbt_grid_layout(const dbt_grid* g, int64_t* owned_planes, int64_t xmap[5]) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  *owned_planes = g->lx;
+  xmap[0] = g->xm.x0;
+  xmap[1] = g->xm.x1;
+  xmap[2] = g->xm.w;
+  xmap[3] = g->xm.p;
+  xmap[4] = g->xm.r;
   return DBT_OK;
 }
 
@@ -367,7 +404,7 @@ int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* 
 int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, const uint8_t* hits) {
   int rc = check_grid(g);
   if (rc) return rc;
-  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  const int64_t lx = g->lx, plane = g->ny * g->nz;
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
   if (rc) return rc;
@@ -392,15 +429,12 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
   return finish_host_write(g);
 }
 
-int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
-                            uint8_t* hits) {
-  int rc = check_grid(g);
-  if (rc) return rc;
-  if (x_begin < g->x0 || x_end > g->x1 || x_begin > x_end)
-    return set_error(DBT_ERR_CONFIG, "download range outside the grid's slab");
-  const int64_t lx = x_end - x_begin, plane = g->ny * g->nz;
+// local (storage) planes [l_begin, l_end) -> host arrays of that many planes
+static int download_local(dbt_grid* g, int64_t l_begin, int64_t l_end, uint32_t* mask, uint8_t* sign,
+                          uint8_t* hits) {
+  const int64_t lx = l_end - l_begin, plane = g->ny * g->nz;
   if (lx == 0) return DBT_OK;
-  rc = fold_pending(g, g->stream);
+  int rc = fold_pending(g, g->stream);
   if (rc) return rc;
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * 6)));
   rc = ensure_stage(g, xs * plane * 6);
@@ -411,7 +445,7 @@ int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_
     uint32_t* dm = (uint32_t*)st;
     uint8_t* ds = st + 4 * n;
     uint8_t* dh = ds + n;
-    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + (x_begin - g->x0 + x) * g->ny * g->nzp, dm, ds,
+    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + (l_begin + x) * g->ny * g->nzp, dm, ds,
                                                          dh, n, g->nz, g->nzp);
     DBT_CHECK_LAUNCH("decode_kernel");
     DBT_CUDA(cudaMemcpyAsync(mask + x * plane, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
@@ -422,16 +456,31 @@ int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_
   return DBT_OK;
 }
 
+int dbt_grid_download_range(dbt_grid* g, int64_t x_begin, int64_t x_end, uint32_t* mask, uint8_t* sign,
+                            uint8_t* hits) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (x_begin > x_end) return set_error(DBT_ERR_CONFIG, "download range outside the grid's owned planes");
+  if (x_begin == x_end) return DBT_OK;
+  // the global planes must be owned and stored contiguously (one slab, or
+  // inside one interleave block)
+  const int64_t lb = g->xm.local(x_begin), le = g->xm.local(x_end - 1);
+  if (lb < 0 || le < 0 || le - lb != x_end - 1 - x_begin)
+    return set_error(DBT_ERR_CONFIG, "download range outside the grid's owned planes");
+  return download_local(g, lb, le + 1, mask, sign, hits);
+}
+
 int dbt_grid_download(dbt_grid* g, uint32_t* mask, uint8_t* sign, uint8_t* hits) {
-  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
-  return dbt_grid_download_range(g, g->x0, g->x1, mask, sign, hits);
+  int rc = check_grid(g);
+  if (rc) return rc;
+  return download_local(g, 0, g->lx, mask, sign, hits);
 }
 
 static int readout(dbt_grid* g, int mode, int32_t* pop, uint8_t* obs, double* sdf) {
   int rc = check_grid(g);
   if (!rc) rc = fold_pending(g, g->stream);
   if (rc) return rc;
-  const int64_t lx = g->x1 - g->x0, plane = g->ny * g->nz;
+  const int64_t lx = g->lx, plane = g->ny * g->nz;
   const int64_t per = mode == 0 ? 4 : (mode == 1 ? 1 : 9);
   int64_t xs = std::max<int64_t>(1, std::min<int64_t>(lx, kStageBytes / (plane * per)));
   rc = ensure_stage(g, xs * plane * per);
@@ -471,7 +520,7 @@ int dbt_grid_counts(dbt_grid* g, int64_t* observed, int64_t* occupied) {
   if (rc) return rc;
   unsigned long long* d = (unsigned long long*)g->d_stage;
   DBT_CUDA(cudaMemsetAsync(d, 0, 16, g->stream));
-  const int64_t n = (g->x1 - g->x0) * g->ny * g->nz;
+  const int64_t n = g->lx * g->ny * g->nz;
   count_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, n, g->nz, g->nzp, d);
   DBT_CHECK_LAUNCH("count_kernel");
   unsigned long long h[2];
@@ -487,7 +536,7 @@ int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, 
   if (rc) return rc;
   for (int64_t i = 0; i < n; ++i) {
     const int64_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
-    if (x < g->x0 || x >= g->x1 || y < 0 || y >= g->ny || z < 0 || z >= g->nz)
+    if (g->xm.local(x) < 0 || y < 0 || y >= g->ny || z < 0 || z >= g->nz)
       return set_error(DBT_ERR_CONFIG, "voxel index outside the grid (or the owned slab)");
   }
   if (n == 0) return DBT_OK;
@@ -501,7 +550,7 @@ int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, 
   rc = fold_pending(g, g->stream);
   if (rc) return rc;
   DBT_CUDA(cudaMemcpyAsync(didx, xyz, 24 * n, cudaMemcpyHostToDevice, g->stream));
-  gather_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, didx, n, g->x0, g->ny, g->nzp, dm, ds, dh);
+  gather_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells, didx, n, g->xm, g->ny, g->nzp, dm, ds, dh);
   DBT_CHECK_LAUNCH("gather_kernel");
   if (mask) DBT_CUDA(cudaMemcpyAsync(mask, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
   if (sign) DBT_CUDA(cudaMemcpyAsync(sign, ds, n, cudaMemcpyDeviceToHost, g->stream));
@@ -513,7 +562,7 @@ int dbt_grid_gather(dbt_grid* g, const int64_t* xyz, int64_t n, uint32_t* mask, 
 int dbt_grid_to_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, void* out_records) {
   int rc = check_grid(g);
   if (rc) return rc;
-  if (g->x0 != 0 || g->x1 != g->nx)
+  if (g->x0 != 0 || g->x1 != g->nx || g->xm.w != 0)
     return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
   if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
   if (z_begin < 0 || z_end > g->nz || z_begin > z_end) return set_error(DBT_ERR_CONFIG, "z range outside the grid");
@@ -545,7 +594,7 @@ int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, con
   int rc = check_grid(g);
   if (rc) return rc;
   if (g->ny > 65535) return set_error(DBT_ERR_CONFIG, "record transpose supports ny <= 65535");
-  if (g->x0 != 0 || g->x1 != g->nx)
+  if (g->x0 != 0 || g->x1 != g->nx || g->xm.w != 0)
     return set_error(DBT_ERR_CONFIG, "records are defined for a whole grid, not a slab");
   if (z_begin < 0 || z_end > g->nz || z_begin > z_end) return set_error(DBT_ERR_CONFIG, "z range outside the grid");
   const int64_t plane = g->nx * g->ny;

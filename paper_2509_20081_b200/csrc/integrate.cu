@@ -83,6 +83,7 @@ struct PrepArgs {
   const int8_t* sxyz;
   const int32_t* sstart;
   int64_t x0, x1, nzp;
+  XMap xm;  // owned planes (x0, x1 above are its range)
   int h_max, t_occ;
   // claim mode (no first-return): dedup + cross-launch skip through the stamp
   // certificate bits instead of the hash table
@@ -235,8 +236,9 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
         // already set means the stamp is in the grid from an earlier launch
         // or owned by an earlier return of this launch; either way no sweep.
         // A centre outside this rank's slab has no bit here: always swept.
-        if (cx >= a.x0 && cx < a.x1) {
-          const int64_t cidx = ((cx - a.x0) * a.ny + cy) * a.nzp + cz;
+        const int64_t lcx = a.xm.local(cx);
+        if (lcx >= 0) {
+          const int64_t cidx = (lcx * a.ny + cy) * a.nzp + cz;
           const uint32_t bit = 1u << (cidx & 31);
           claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
           append = !claimed;
@@ -276,9 +278,9 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
         for (int k = 0; k < 8; ++k) {
           if (k >= nsh) break;
           const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
-          const int64_t gx = cx + o.x;
-          if (gx >= a.x0 && gx < a.x1)
-            shadow_add(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+          const int64_t lgx = a.xm.local(cx + o.x);
+          if (lgx >= 0)
+            shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
                        (uint32_t)a.t_occ);
         }
       }
@@ -328,6 +330,7 @@ struct ShadowArgs {
   int64_t n;
   int log2s;  // threads per return = 1 << log2s >= max shadow count
   int64_t x0, x1, ny, nzp;
+  XMap xm;
   int h_max, t_occ;
   int first_return;
   int S;
@@ -358,9 +361,9 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     char4 o = reinterpret_cast<const char4*>(a.sxyz)[st + k];
     int64_t cx, cy, cz;
     unpack_center(c, cx, cy, cz);
-    int64_t gx = cx + o.x;
-    if (gx < a.x0 || gx >= a.x1) continue;
-    shadow_add(&a.cells[((gx - a.x0) * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+    const int64_t lgx = a.xm.local(cx + o.x);
+    if (lgx < 0) continue;
+    shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
                (uint32_t)a.t_occ);
   }
 }
@@ -376,6 +379,7 @@ struct SweepArgs {
   const int32_t* rowoff;  // [rows]
   int K, R, nd;
   int64_t x0, x1, ny, nzp;
+  XMap xm;
 };
 
 constexpr int kSweepUnroll = 4;
@@ -418,11 +422,14 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     // 16-bit reciprocal (exact for j < 2^15)
     const int nch = (sh + a.K + 7) >> 3;
     const uint32_t magic = (65536u + nch - 1) / nch;
-    const int64_t base = ((cx - a.x0) * a.ny + cy) * a.nzp + (zs & ~int64_t(7));
-    // slab clip (multi-GPU): rows are dx-major, so the owned dx range is a
-    // contiguous range of chunk indices
-    const int64_t dxlo = max((int64_t)-a.R, a.x0 - cx);
-    const int64_t dxhi = min((int64_t)a.R, a.x1 - 1 - cx);
+    const bool ilv = a.xm.w != 0;  // interleaved slabs: x-planes mapped per row
+    const int64_t sx = a.ny * a.nzp;
+    const int64_t base0 = cy * a.nzp + (zs & ~int64_t(7));
+    const int64_t base = ilv ? base0 : (cx - a.x0) * sx + base0;
+    // slab clip (multi-GPU): rows are dx-major, so the owned dx range of a
+    // contiguous slab is a contiguous range of chunk indices
+    const int64_t dxlo = ilv ? -a.R : max((int64_t)-a.R, a.x0 - cx);
+    const int64_t dxhi = ilv ? a.R : min((int64_t)a.R, a.x1 - 1 - cx);
     if (dxlo > dxhi) continue;
     const int jlo = (int)((dxlo + a.R) * a.K * nch);
     const int jhi = (int)((dxhi + a.R + 1) * a.K * nch);
@@ -433,12 +440,19 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 #pragma unroll
       for (int k = 0; k < kSweepUnroll; ++k) {
         const int j = j0 + 32 * k;
-        const bool v = j < jhi;
+        bool v = j < jhi;
         const int jj = v ? j : jlo;
         const int row = (int)(((uint32_t)jj * magic) >> 16);
         const int ch = jj - row * nch;
         const int2 ri = rowinfo[row];
         off[k] = base + ri.x + 8 * ch;
+        if (ilv) {
+          // row offset = dx*sx + dy*nzp: swap the dx plane for its storage plane
+          const int dx = row / a.K - a.R;
+          const int64_t lgx = a.xm.local(cx + dx);
+          v = v && lgx >= 0;
+          off[k] = v ? lgx * sx + (ri.x - dx * sx) + base0 + 8 * ch : 0;
+        }
         d8[k] = v ? dt[ri.y + ch] : make_uint2(0x40404040u, 0x40404040u);
         w[k] = *reinterpret_cast<const uint2*>(a.dist + off[k]);
       }
@@ -498,6 +512,7 @@ struct CullArgs {
   const uint32_t* stamped;
   int K, R, nd, CH;
   int64_t x0, x1, ny, nzp;
+  XMap xm;
 };
 
 constexpr int kFar = 1 << 20;
@@ -540,9 +555,9 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       uint32_t nb3 = 0;
       if (lane < 9) {
         const int na = lane / 3 - 1, nbb = lane % 3 - 1;
-        const int64_t gx = cx + na;
-        if (gx >= a.x0 && gx < a.x1) {
-          const int64_t idx = ((gx - a.x0) * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
+        const int64_t lgx = a.xm.local(cx + na);
+        if (lgx >= 0) {
+          const int64_t idx = (lgx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
           const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
           const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
           nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
@@ -552,8 +567,9 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
 #define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
       // per lane: kernel x-offset dx, its dy interval and z-cut terms
       const int dx = lane - R;
-      const int64_t gx = cx + dx;
-      bool dead = lane >= K || gx < a.x0 || gx >= a.x1;
+      const int64_t lgx = lane < K ? a.xm.local(cx + dx) : -1;
+      bool dead = lgx < 0;
+      const int64_t xbase = dead ? 0 : lgx * sx;  // storage offset of this lane's x-plane
       int ylo = -R, yhi = R;
       int mp[3] = {kFar, kFar, kFar}, mm[3] = {-kFar, -kFar, -kFar};  // index b + 1
 #pragma unroll
@@ -585,7 +601,7 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       const int64_t zs = cz - R;
       const int sh = (int)(zs & 7);
       const int64_t zb = zs >> 3;  // chunk index of the kernel's first chunk
-      const int64_t cbase = ((cx - a.x0) * a.ny + cy) * a.nzp + (zb << 3);
+      const int64_t cbase = cy * a.nzp + (zb << 3);
       for (int t0 = 0; t0 < total; t0 += 32) {
         const int t = t0 + lane;
         int own = 0;  // owner lane: the last lane whose exclusive prefix is <= t
@@ -597,6 +613,7 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
         }
         const int o_pre = __shfl_sync(0xffffffffu, pre, own);
         const int o_ylo = __shfl_sync(0xffffffffu, ylo, own);
+        const int64_t o_xb = __shfl_sync(0xffffffffu, xbase, own);
         const int mp0 = __shfl_sync(0xffffffffu, mp[0], own), mp1 = __shfl_sync(0xffffffffu, mp[1], own),
                   mp2 = __shfl_sync(0xffffffffu, mp[2], own);
         const int mm0 = __shfl_sync(0xffffffffu, mm[0], own), mm1 = __shfl_sync(0xffffffffu, mm[1], own),
@@ -621,7 +638,7 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
         if (alive) {
           const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
           const int drow = sh * a.nd * a.CH + __ldg(rowd + (rdx + R) * K + (rdy + R));
-          task = pack_task(cbase + rdx * sx + rdy * a.nzp, c0, c1, drow);
+          task = pack_task(o_xb + cbase + rdy * a.nzp, c0, c1, drow);
         }
         const unsigned m = __ballot_sync(0xffffffffu, alive);
         int qb = 0;
@@ -944,6 +961,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.sstart = b->d_shadow_start;
   pa.x0 = g->x0;
   pa.x1 = g->x1;
+  pa.xm = g->xm;
   pa.nzp = g->nzp;
   pa.h_max = p->h_max;
   pa.t_occ = p->t_occ;
@@ -997,6 +1015,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sa.log2s = l2;
     sa.x0 = g->x0;
     sa.x1 = g->x1;
+    sa.xm = g->xm;
     sa.ny = g->ny;
     sa.nzp = g->nzp;
     sa.h_max = p->h_max;
@@ -1044,6 +1063,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     wa.CH = b->chunks_per_row;
     wa.x0 = g->x0;
     wa.x1 = g->x1;
+    wa.xm = g->xm;
     wa.ny = g->ny;
     wa.nzp = g->nzp;
     // persistent blocks fetching kCullWarps centres at a time
@@ -1086,6 +1106,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   wa.R = b->R;
   wa.x0 = g->x0;
   wa.x1 = g->x1;
+  wa.xm = g->xm;
   wa.ny = g->ny;
   wa.nzp = g->nzp;
   unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 7) / 8));

@@ -44,6 +44,17 @@ VOXEL_DTYPE = np.dtype([("mask", "<u4"), ("sign", "u1"), ("hits", "u1"), ("reser
 DEFAULT_MEMORY_CAP = 8 << 30  # bytes of voxel payload (reference accounting: 8 B/voxel)
 
 
+def owned_planes(nx: int, slab=(0, None), interleave=None) -> np.ndarray:
+    """Global x of the planes a grid stores, in storage order: the slab
+    [x0, x1), or the interleaved blocks (width, parts, part) of [0, nx)."""
+    if interleave is None:
+        x0, x1 = slab[0], nx if slab[1] is None else slab[1]
+        return np.arange(x0, x1, dtype=np.int64)
+    w, p, r = interleave
+    x = np.arange(nx, dtype=np.int64)
+    return x[(x // w) % p == r]
+
+
 class _GridHandle:
     def __init__(self, ptr):
         self.ptr = ptr
@@ -59,22 +70,37 @@ class VoxelGrid:
     """Fixed-size axis-aligned grid; structure immutable after construction,
     voxel contents updated in place by the integrator (grid.py:39-58)."""
 
-    def __init__(self, dims, voxel_size, origin, *, device: int | None = None, slab=None):
+    def __init__(self, dims, voxel_size, origin, *, device: int | None = None, slab=None, interleave=None):
+        """slab=(x0, x1): own the contiguous x-planes [x0, x1); interleave=
+        (width, parts, part): own the planes whose block x // width is
+        congruent to part mod parts (multi-GPU sharding, sharded.py)."""
         self.dims = tuple(int(d) for d in dims)
         self.voxel_size = float(voxel_size)
         self.origin = np.asarray(origin, dtype=np.float64).copy()
         self.h_max = 255
         self.t_occ = 2
         self.device = _native.default_device() if device is None else int(device)
-        x0, x1 = (0, self.dims[0]) if slab is None else (int(slab[0]), int(slab[1]))
-        self.slab = (x0, x1)
         dims_a = np.array(self.dims, dtype=np.int64)
         org = np.ascontiguousarray(self.origin)
         out = ctypes.c_void_p()
-        _native.check(_native.lib().dbt_grid_create(dims_a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                                                    self.voxel_size, org.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-                                                    self.device, x0, x1, ctypes.byref(out)))
+        L = _native.lib()
+        if interleave is not None:
+            w, p, r = (int(v) for v in interleave)
+            self.slab = (0, self.dims[0])
+            self.interleave = (w, p, r)
+            _native.check(L.dbt_grid_create_interleaved(dims_a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                        self.voxel_size,
+                                                        org.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                                        self.device, w, p, r, ctypes.byref(out)))
+        else:
+            x0, x1 = (0, self.dims[0]) if slab is None else (int(slab[0]), int(slab[1]))
+            self.slab = (x0, x1)
+            self.interleave = None
+            _native.check(L.dbt_grid_create(dims_a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                            self.voxel_size, org.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            self.device, x0, x1, ctypes.byref(out)))
         self._handle = _GridHandle(out)
+        self.owned_x = owned_planes(self.dims[0], self.slab, self.interleave)
         self._host = None  # (mask, sign, hits) mirror when exposed
 
     # ---- handle / mirror protocol -------------------------------------
@@ -84,7 +110,7 @@ class VoxelGrid:
 
     @property
     def local_dims(self):
-        return (self.slab[1] - self.slab[0], self.dims[1], self.dims[2])
+        return (len(self.owned_x), self.dims[1], self.dims[2])
 
     @property
     def num_voxels(self) -> int:

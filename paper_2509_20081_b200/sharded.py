@@ -96,13 +96,27 @@ def reduce_stats(stats: list, dist, group=None, device=None) -> list:
 
 
 class ShardedGrid:
-    """This rank's slab of a globally-sized grid, device resident."""
+    """This rank's share of a globally-sized grid, device resident: the
+    contiguous slab ``slab_bounds`` gives, or (interleave=width) the x-blocks
+    of ``width`` planes dealt round-robin over the ranks, which balances the
+    1/r^2 return density around the sensor across ranks."""
 
-    def __init__(self, dims, voxel_size, origin, rank: int, world: int, device: int | None = None):
+    def __init__(self, dims, voxel_size, origin, rank: int, world: int, device: int | None = None,
+                 interleave: int | None = None):
         self.dims = tuple(int(d) for d in dims)
         self.rank, self.world = rank, world
-        self.slab = slab_bounds(self.dims[0], world, rank)
-        self.local = VoxelGrid(self.dims, voxel_size, origin, device=device, slab=self.slab)
+        if interleave:
+            self.slab = (0, self.dims[0])
+            self.local = VoxelGrid(self.dims, voxel_size, origin, device=device,
+                                   interleave=(int(interleave), world, rank))
+        else:
+            self.slab = slab_bounds(self.dims[0], world, rank)
+            self.local = VoxelGrid(self.dims, voxel_size, origin, device=device, slab=self.slab)
+
+    @property
+    def owned_x(self) -> np.ndarray:
+        """Global x of this rank's planes, in storage order."""
+        return self.local.owned_x
 
     def integrate_device(self, bank: KernelBank, points, counts, poses, params: IntegrationParams, stream=None):
         """Stamp this rank's slab from device-resident points (torch CUDA

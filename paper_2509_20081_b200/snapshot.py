@@ -35,7 +35,7 @@ def _planes_per_chunk(grid_dims) -> int:
 def save_grid(grid: VoxelGrid, path) -> None:
     """io.py:449-459: magic, header, voxel records in linear-index order."""
     path = Path(path)
-    if grid.slab != (0, grid.dims[0]):
+    if grid.slab != (0, grid.dims[0]) or grid.interleave is not None:
         raise ConfigurationError("a snapshot needs the whole grid, not one slab")
     nx, ny, nz = grid.dims
     header = _HEADER.pack(nx, ny, nz, float(grid.voxel_size), *[float(o) for o in grid.origin],

@@ -475,6 +475,86 @@ class TestPinnedScans:
                 L.dbt_host_free(b)
 
 
+class TestOrderIndependence:
+    """The reference stamps in sorted centre order (integrator.py:266-284);
+    the engine's updates commute, so any point order, any batching and any
+    repetition gives the same grid."""
+
+    def test_permuted_and_repeated_scan(self, golden):
+        c = next(c for c in CONFIG if c.name == "cfg2_scans0-2")
+        bank = build_kernel_bank(**c.bank)
+        rng = np.random.default_rng(99)
+        grids = []
+        for variant in ("orig", "permuted", "split"):
+            g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 42)
+            for pts, pose in c.frames:
+                if variant == "permuted":
+                    pts = pts[rng.permutation(len(pts))]
+                if variant == "split":  # the scan as 3 launches of uneven size
+                    for part in np.split(pts, [5000, 41000]):
+                        integrate_frame(g, bank, ScanFrame(points=part, pose=pose), IntegrationParams())
+                else:
+                    integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams())
+            grids.append(g.download_range(0, c.dims[0]))
+        ref = golden["cases"][c.name]
+        for m, s_, h in grids:
+            assert cases.sha(m) == ref["mask"] and cases.sha(s_) == ref["sign"] and cases.sha(h) == ref["hits"]
+
+
+class TestInterleavedSharding:
+    """Interleaved x-blocks (dbt_grid_create_interleaved): each part stamps
+    only its blocks; the parts reassemble to the reference grid. Both sweeps
+    (culling for the standard kernel, generic for an asymmetric one)."""
+
+    @staticmethod
+    def _assemble(parts, dims):
+        m = np.empty(dims, np.uint32)
+        s_ = np.empty(dims, np.uint8)
+        h = np.empty(dims, np.uint8)
+        for g in parts:
+            m[g.owned_x], s_[g.owned_x], h[g.owned_x] = g.mask, g.sign, g.hits
+        return m, s_, h
+
+    def test_parts_reassemble_to_reference(self, golden):
+        from paper_2509_20081_b200.grid import VoxelGrid
+
+        c = next(c for c in CONFIG if c.name == "cfg2_scans0-2")
+        bank = build_kernel_bank(**c.bank)
+        for w, P in ((16, 3), (64, 2), (7, 4)):
+            parts = [VoxelGrid(c.dims, c.voxel_size, c.origin, interleave=(w, P, r)) for r in range(P)]
+            assert sum(len(g.owned_x) for g in parts) == c.dims[0]
+            for g in parts:
+                g.release_host()
+                for pts, pose in c.frames:
+                    integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams())
+            m, s_, h = self._assemble(parts, c.dims)
+            ref = golden["cases"][c.name]
+            assert cases.sha(m) == ref["mask"] and cases.sha(s_) == ref["sign"] and cases.sha(h) == ref["hits"]
+
+    def test_generic_sweep_interleaved(self):
+        import dataclasses
+
+        from paper_2509_20081_b200.grid import VoxelGrid
+
+        base = build_kernel_bank(shadow_radius=2)
+        dk = base.distance_kernel.copy()
+        dk[12:, 14:, :] &= np.uint32(0x3F)
+        bank = dataclasses.replace(base, distance_kernel=dk, _device={})
+        rng = np.random.default_rng(21)
+        frames = [(rng.uniform(1.15, 3.6, size=(400, 3)), cases.yaw_pose(0.3 * k, (0.02 * k, 0, 0))) for k in range(2)]
+        dims = (48, 48, 48)
+        parts = [VoxelGrid(dims, 0.1, (0, 0, 0), interleave=(5, 3, r)) for r in range(3)]
+        for g in parts:
+            for pts, pose in frames:
+                integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams())
+        m, s_, h = self._assemble(parts, dims)
+        og = oracle.OracleGrid(dims, 0.1, (0, 0, 0))
+        ob = oracle.OracleBank.from_bank(bank)
+        for pts, pose in frames:
+            oracle.integrate_frame(og, ob, pts, pose)
+        assert np.array_equal(m, og.mask) and np.array_equal(s_, og.sign) and np.array_equal(h, og.hits)
+
+
 class TestSweepPaths:
     """The symmetric-kernel sweep (base-pair table) and the generic sweep
     (distinct-row table) must both reproduce the reference stamping."""

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case_name, out_path):
+def _worker(rank, world, port, case_name, out_path, interleave=0):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch
@@ -44,8 +44,16 @@ def _worker(rank, world, port, case_name, out_path):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     c = next(x for x in C.config_cases(include_slow=False) if x.name == case_name)
-    x0, x1 = sharded.slab_bounds(c.dims[0], world, rank)
-    g = oracle.OracleGrid(c.dims, c.voxel_size, c.origin, slab=(x0, x1))
+    from paper_2509_20081_b200.grid import owned_planes
+
+    if interleave:
+        owned = owned_planes(c.dims[0], interleave=(interleave, world, rank))
+    else:
+        owned = np.arange(*sharded.slab_bounds(c.dims[0], world, rank))
+    # the oracle's slab stamping per contiguous run of owned planes stands in
+    # for the device engine (the GPU tests cover the engine's layouts)
+    runs = np.split(owned, np.nonzero(np.diff(owned) != 1)[0] + 1)
+    grids = [oracle.OracleGrid(c.dims, c.voxel_size, c.origin, slab=(int(r[0]), int(r[-1]) + 1)) for r in runs]
     ob = oracle.OracleBank.build(**c.bank)
     stats_all = []
     for pts, pose in c.frames:
@@ -55,30 +63,32 @@ def _worker(rank, world, port, case_name, out_path):
             payload, counts, poses = None, None, None
         pts_r, counts_r, poses_r = sharded.broadcast_batch(payload, counts, poses, dist)
         assert pts_r.dtype == torch.float32 and int(counts_r[0]) == len(pts)
-        st = oracle.integrate_frame(g, ob, pts_r.numpy(), poses_r[0], threads=2)
-        local = FrameStats(st.points_in, st.points_discarded, st.voxels_written)
+        sts = [oracle.integrate_frame(g, ob, pts_r.numpy(), poses_r[0], threads=2) for g in grids]
+        local = FrameStats(sts[0].points_in, sts[0].points_discarded, sum(s.voxels_written for s in sts))
         stats_all.append(sharded.reduce_stats([local], dist)[0])
     parts = [None] * world
-    dist.all_gather_object(parts, (x0, x1, g.mask, g.sign, g.hits))
+    dist.all_gather_object(parts, (owned, np.concatenate([g.mask for g in grids]),
+                                   np.concatenate([g.sign for g in grids]), np.concatenate([g.hits for g in grids])))
     if rank == 0:
-        parts.sort(key=lambda t: t[0])
-        assert parts[0][0] == 0 and parts[-1][1] == c.dims[0]
-        assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
-        mask = np.concatenate([p[2] for p in parts])
-        sign = np.concatenate([p[3] for p in parts])
-        hits = np.concatenate([p[4] for p in parts])
+        xs = np.concatenate([p[0] for p in parts])
+        assert np.array_equal(np.sort(xs), np.arange(c.dims[0]))  # a partition of the planes
+        mask = np.empty(c.dims, np.uint32)
+        sign = np.empty(c.dims, np.uint8)
+        hits = np.empty(c.dims, np.uint8)
+        for ox, m, s, h in parts:
+            mask[ox], sign[ox], hits[ox] = m, s, h
         np.savez(out_path, mask_sha=C.sha(mask), sign_sha=C.sha(sign), hits_sha=C.sha(hits),
                  stats=np.array([[s.points_in, s.points_discarded, s.voxels_written] for s in stats_all]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case_name", ["cfg1_scan0", "cfg2_scans0-2"])
-def test_two_rank_slab_sharding_reproduces_reference(case_name, golden, tmp_path):
+@pytest.mark.parametrize("case_name,interleave", [("cfg1_scan0", 0), ("cfg2_scans0-2", 0), ("cfg2_scans0-2", 32)])
+def test_two_rank_slab_sharding_reproduces_reference(case_name, interleave, golden, tmp_path):
     import torch.multiprocessing as mp
 
     out = tmp_path / "r0.npz"
-    mp.spawn(_worker, args=(2, _free_port(), case_name, str(out)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), case_name, str(out), interleave), nprocs=2, join=True)
     r = np.load(out)
     ref = golden["cases"][case_name]
     assert str(r["mask_sha"]) == ref["mask"]
