@@ -167,7 +167,9 @@ __device__ __forceinline__ bool floor_index(double v, double o, double vs, long 
   return true;
 }
 
-__global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool live = i < a.n;
@@ -290,32 +292,68 @@ __global__ void __launch_bounds__(128) prep_kernel(PrepArgs a) {
     a.center[i] = packed;
     if (a.outcome) a.outcome[i] = ok ? 1 : 0;
   }
-  // sweep work items: one atomicAdd per warp on the launch-wide counter
+  // Launch-wide counters are aggregated per block: one atomic per block and
+  // counter instead of one per warp (same-address atomics serialise at L2).
+  __shared__ unsigned w_app[kPrepThreads / 32], w_clm[kPrepThreads / 32], w_ok[kPrepThreads / 32],
+      w_fb[kPrepThreads / 32];
+  __shared__ int w_scan[kPrepThreads / 32];
+  __shared__ unsigned long long blk_base;
+  const int warp = threadIdx.x >> 5, nwarps = kPrepThreads / 32;
   const unsigned app = __ballot_sync(0xffffffffu, append);
-  if (app) {
-    const int leader = __ffs(app) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(&a.lc->n_unique, (unsigned long long)__popc(app));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (append) a.uniq[base + __popc(app & ((1u << lane) - 1u))] = packed;
-  }
   const unsigned clm = __ballot_sync(0xffffffffu, claimed);
-  if (clm && lane == __ffs(clm) - 1) atomicAdd(&a.lc->skipped, (unsigned long long)__popc(clm));
-  // per-scan counters, warp-aggregated when the warp lies inside one scan
-  unsigned act = __ballot_sync(0xffffffffu, live);
-  if (!act) return;
-  int s0 = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
-  bool uniform = __all_sync(0xffffffffu, !live || s == s0);
-  if (uniform) {
-    int nok = __popc(__ballot_sync(0xffffffffu, live && ok));
-    int nkn = __popc(__ballot_sync(0xffffffffu, live && ok && fallback));
-    if (lane == __ffs(act) - 1) {
-      if (nok) atomicAdd(&a.sc[s0].n_ok, (unsigned long long)nok);
-      if (nkn) atomicAdd(&a.sc[s0].n_fallback, (unsigned long long)nkn);
+  const unsigned act = __ballot_sync(0xffffffffu, live);
+  const unsigned okm = __ballot_sync(0xffffffffu, live && ok);
+  const unsigned fbm = __ballot_sync(0xffffffffu, live && ok && fallback);
+  // the scan of this warp's returns, -1 when they span several scans
+  const int s0 = act ? __shfl_sync(0xffffffffu, s, __ffs(act) - 1) : 0;
+  const bool uniform = __all_sync(0xffffffffu, !live || s == s0);
+  if (lane == 0) {
+    w_app[warp] = __popc(app);
+    w_clm[warp] = __popc(clm);
+    w_ok[warp] = __popc(okm);
+    w_fb[warp] = __popc(fbm);
+    w_scan[warp] = !act ? -2 : (uniform ? s0 : -1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned napp = 0, nclm = 0, nok = 0, nfb = 0;
+    int sb = -2;
+    bool same = true;
+    for (int w = 0; w < nwarps; ++w) {
+      napp += w_app[w];
+      nclm += w_clm[w];
+      nok += w_ok[w];
+      nfb += w_fb[w];
+      if (w_scan[w] == -2) continue;
+      if (sb == -2) sb = w_scan[w];
+      same = same && w_scan[w] == sb && sb >= 0;
     }
-  } else if (live) {
-    if (ok) atomicAdd(&a.sc[s].n_ok, 1ull);
-    if (ok && fallback) atomicAdd(&a.sc[s].n_fallback, 1ull);
+    blk_base = napp ? atomicAdd(&a.lc->n_unique, (unsigned long long)napp) : 0ull;
+    if (nclm) atomicAdd(&a.lc->skipped, (unsigned long long)nclm);
+    if (same && sb >= 0) {
+      if (nok) atomicAdd(&a.sc[sb].n_ok, (unsigned long long)nok);
+      if (nfb) atomicAdd(&a.sc[sb].n_fallback, (unsigned long long)nfb);
+      w_scan[0] = -3;  // counted for the whole block
+    }
+  }
+  __syncthreads();
+  // sweep work items at this warp's offset inside the block's range
+  if (append) {
+    unsigned long long off = blk_base;
+    for (int w = 0; w < warp; ++w) off += w_app[w];
+    a.uniq[off + __popc(app & ((1u << lane) - 1u))] = packed;
+  }
+  if (w_scan[0] != -3 && live) {
+    // the block spans several scans: per-scan counters per warp (or thread)
+    if (uniform) {
+      if (lane == __ffs(act) - 1) {
+        if (okm) atomicAdd(&a.sc[s0].n_ok, (unsigned long long)__popc(okm));
+        if (fbm) atomicAdd(&a.sc[s0].n_fallback, (unsigned long long)__popc(fbm));
+      }
+    } else {
+      if (ok) atomicAdd(&a.sc[s].n_ok, 1ull);
+      if (ok && fallback) atomicAdd(&a.sc[s].n_fallback, 1ull);
+    }
   }
 }
 
@@ -995,7 +1033,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   if (rc) return rc;
   int tok;
   prof_begin(g, "prep_kernel", st, &tok);
-  prep_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(pa);
+  prep_kernel<<<(unsigned)((n + kPrepThreads - 1) / kPrepThreads), kPrepThreads, 0, st>>>(pa);
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("prep_kernel");
 
