@@ -733,8 +733,14 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
     }
     __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
+  // one atomic per block (same-address atomics serialise at L2)
+  __shared__ unsigned long long blk_changed;
+  if (threadIdx.x == 0) blk_changed = 0;
   for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
-  if (lane == 0 && changed) atomicAdd(&a.lc->changed, changed);
+  __syncthreads();
+  if (lane == 0 && changed) atomicAdd(&blk_changed, changed);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_changed) atomicAdd(&a.lc->changed, blk_changed);
 }
 
 typedef void (*SweepFn)(SweepArgs);
