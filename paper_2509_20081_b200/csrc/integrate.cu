@@ -534,9 +534,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 // Per centre the surviving region is, for each kernel x-offset dx (lane), a
 // dy interval (neighbours with delta_z = 0 cut whole rows) and per row a dz
 // interval (delta_z = +-1 neighbours cut z prefixes/suffixes). A block takes
-// kCullWarps centres at a time: phase A, one warp per centre, compacts the surviving
-// rows into a shared-memory queue of row tasks (row start, chunk range,
-// d-table row); phase B, the whole block, sweeps the queued rows one thread
+// kCullWarps centres at a time: phase A, one warp per centre, writes the
+// surviving rows into a shared-memory queue of row tasks (row start, chunk
+// range, d-table row), each lane its own column's rows at its prefix-sum
+// offset; phase B, the whole block, sweeps the queued rows one thread
 // per row (1-4 chunk loads in flight each), testing them as sweep_kernel
 // does. Rows of a heavy centre (a fresh surface: nothing culled) thus spread
 // over the block instead of serialising one warp.
@@ -640,49 +641,35 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       const int sh = (int)(zs & 7);
       const int64_t zb = zs >> 3;  // chunk index of the kernel's first chunk
       const int64_t cbase = cy * a.nzp + (zb << 3);
-      for (int t0 = 0; t0 < total; t0 += 32) {
-        const int t = t0 + lane;
-        int own = 0;  // owner lane: the last lane whose exclusive prefix is <= t
-#pragma unroll
-        for (int st = 16; st; st >>= 1) {
-          const int cand = own + st;
-          const int pv = __shfl_sync(0xffffffffu, pre, cand & 31);
-          if (cand < 32 && pv <= t) own = cand;
-        }
-        const int o_pre = __shfl_sync(0xffffffffu, pre, own);
-        const int o_ylo = __shfl_sync(0xffffffffu, ylo, own);
-        const int64_t o_xb = __shfl_sync(0xffffffffu, xbase, own);
-        const int mp0 = __shfl_sync(0xffffffffu, mp[0], own), mp1 = __shfl_sync(0xffffffffu, mp[1], own),
-                  mp2 = __shfl_sync(0xffffffffu, mp[2], own);
-        const int mm0 = __shfl_sync(0xffffffffu, mm[0], own), mm1 = __shfl_sync(0xffffffffu, mm[1], own),
-                  mm2 = __shfl_sync(0xffffffffu, mm[2], own);
-        bool alive = t < total;
-        const int rdx = own - R;
-        const int rdy = o_ylo + (t - o_pre);
+      // each lane writes its own column's rows at its prefix offset (no owner
+      // search, no per-row shuffles); a row with an empty dz interval fills
+      // its reserved slot with kEmptyKey
+      int qb = 0;
+      if (lane == 0 && total) qb = atomicAdd(&q_n, total);
+      qb = __shfl_sync(0xffffffffu, qb, 0);
+      const int zhi0 = min(R, max(mp[1], -R + 1) - 1), zlo0 = max(-R, min(mm[1], R - 1) + 1);
+      const int drow0 = sh * a.nd * a.CH;
+      const uint16_t* rowd_dx = rowd + (dx + R) * K + R;
+      for (int k = 0; k < cnt; ++k) {
+        const int rdy = ylo + k;
         // dz interval: delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1),
         // delta_z = -1 ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only
         // when v is in their y-window)
-        int zhi = min(R, max(mp1, -R + 1) - 1), zlo = max(-R, min(mm1, R - 1) + 1);
+        int zhi = zhi0, zlo = zlo0;
         if (rdy <= R - 1) {  // b = -1
-          zhi = min(zhi, max(mp0 + rdy, -R + 1) - 1);
-          zlo = max(zlo, min(mm0 - rdy, R - 1) + 1);
+          zhi = min(zhi, max(mp[0] + rdy, -R + 1) - 1);
+          zlo = max(zlo, min(mm[0] - rdy, R - 1) + 1);
         }
         if (rdy >= -R + 1) {  // b = +1
-          zhi = min(zhi, max(mp2 - rdy, -R + 1) - 1);
-          zlo = max(zlo, min(mm2 + rdy, R - 1) + 1);
+          zhi = min(zhi, max(mp[2] - rdy, -R + 1) - 1);
+          zlo = max(zlo, min(mm[2] + rdy, R - 1) + 1);
         }
-        alive = alive && zlo <= zhi;
-        uint64_t task = 0;
-        if (alive) {
+        uint64_t task = kEmptyKey;
+        if (zlo <= zhi) {
           const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
-          const int drow = sh * a.nd * a.CH + __ldg(rowd + (rdx + R) * K + (rdy + R));
-          task = pack_task(o_xb + cbase + rdy * a.nzp, c0, c1, drow);
+          task = pack_task(xbase + cbase + rdy * a.nzp, c0, c1, drow0 + __ldg(rowd_dx + rdy));
         }
-        const unsigned m = __ballot_sync(0xffffffffu, alive);
-        int qb = 0;
-        if (lane == 0 && m) qb = atomicAdd(&q_n, __popc(m));
-        qb = __shfl_sync(0xffffffffu, qb, 0);
-        if (alive) queue[qb + __popc(m & ((1u << lane) - 1u))] = task;
+        queue[qb + pre + k] = task;
       }
     }
     __syncthreads();
@@ -698,9 +685,9 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int qi = i + r * blockDim.x;
-        const uint64_t task = qi < nq ? queue[qi] : 0ull;
+        const uint64_t task = qi < nq ? queue[qi] : kEmptyKey;
         rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
-        const int c0 = (int)((task >> 37) & 3), c1 = qi < nq ? (int)((task >> 39) & 3) : -1;
+        const int c0 = (int)((task >> 37) & 3), c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
         cb[r] = c0;
         const uint2* drow = dtab + (int)(task >> 41);
 #pragma unroll
