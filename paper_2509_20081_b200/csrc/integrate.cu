@@ -389,8 +389,10 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     if (a.first_return) {
       if (a.hmin[a.slot[i]] != (uint32_t)i) continue;
       if (k == 0) {
-        int s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
-        atomicAdd(&a.sc[s].n_applied, 1ull);
+        // one atomic per group of lanes counting the same scan
+        const int s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+        const unsigned grp = __match_any_sync(__activemask(), s);
+        if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&a.sc[s].n_applied, (unsigned long long)__popc(grp));
       }
     }
     int b = a.bin[i];

@@ -564,8 +564,10 @@ class TestSweepPaths:
         og = oracle.OracleGrid(dims, 0.1, (0, 0, 0))
         ob = oracle.OracleBank.from_bank(bank)
         for pts, pose in frames:
-            integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams(first_return_per_voxel=first_return))
-            oracle.integrate_frame(og, ob, pts, pose, first_return=first_return)
+            st = integrate_frame(g, bank, ScanFrame(points=pts, pose=pose),
+                                 IntegrationParams(first_return_per_voxel=first_return))
+            ost = oracle.integrate_frame(og, ob, pts, pose, first_return=first_return)
+            assert st.points_applied == ost.points_applied  # first-return winners / applied returns
         assert np.array_equal(g.mask, og.mask) and np.array_equal(g.sign, og.sign) and np.array_equal(g.hits, og.hits)
 
     @pytest.mark.parametrize("first_return", [False, True])
