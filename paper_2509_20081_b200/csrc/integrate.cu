@@ -604,7 +604,34 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
           nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
         }
       }
+      // axis neighbours at distance 2 and 3 (sparse returns: the next beam
+      // or azimuth step is often 2-3 voxels away): c + k e_x (lanes 9-12),
+      // c + k e_y (lanes 13-16), c + k e_z (lane 17, the centre row's bits
+      // cz-3 .. cz+3). Each cuts the half-space 2 k o_axis > k^2, i.e.
+      // o_axis >= 2 (-2 for the negative side), inside its window for R >= 1.
+      uint32_t ax = 0;
+      if (lane >= 9 && lane < 17) {
+        const int j = (lane - 9) & 3, k = 2 + (j & 1), sg = j < 2 ? 1 : -1;
+        const bool along_x = lane < 13;
+        const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
+        const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(qx) : -1;
+        if (lq >= 0) {
+          const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+          ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
+        }
+      } else if (lane == 17 && cz >= 3 && cz + 3 < a.nzp) {  // padding bits are never set
+        const int64_t lq = a.xm.local(cx);
+        if (lq >= 0) {
+          const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 3);
+          const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+          const uint32_t w1 = ((idx & 31) > 25) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+          const uint32_t b7 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7Fu;  // bit i: cz - 3 + i
+          // z+2, z+3 -> bits 8, 9; z-2, z-3 -> bits 10, 11
+          ax = (((b7 >> 5) & 1u) << 8) | (((b7 >> 6) & 1u) << 9) | (((b7 >> 1) & 1u) << 10) | ((b7 & 1u) << 11);
+        }
+      }
       const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
+      const uint32_t axm = __reduce_or_sync(0xffffffffu, ax);
 #define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
       // per lane: kernel x-offset dx, its dy interval and z-cut terms
       const int dx = lane - R;
@@ -630,6 +657,14 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
         }
       }
 #undef NB
+      // axis neighbours at distance 2-3 (bits: x+ 0-1, x- 2-3, y+ 4-5, y- 6-7,
+      // z+ 8-9, z- 10-11)
+      if ((axm & 0x003u) && dx >= 2) dead = true;
+      if ((axm & 0x00Cu) && dx <= -2) dead = true;
+      if (axm & 0x030u) yhi = min(yhi, 1);
+      if (axm & 0x0C0u) ylo = max(ylo, -1);
+      if (axm & 0x300u) mp[1] = min(mp[1], 2);   // dz >= 2 culled
+      if (axm & 0xC00u) mm[1] = max(mm[1], -2);  // dz <= -2 culled
       const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
       int pre = cnt;  // inclusive scan
 #pragma unroll
