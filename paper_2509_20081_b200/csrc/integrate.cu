@@ -604,30 +604,33 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
           nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
         }
       }
-      // axis neighbours at distance 2 and 3 (sparse returns: the next beam
-      // or azimuth step is often 2-3 voxels away): c + k e_x (lanes 9-12),
-      // c + k e_y (lanes 13-16), c + k e_z (lane 17, the centre row's bits
-      // cz-3 .. cz+3). Each cuts the half-space 2 k o_axis > k^2, i.e.
-      // o_axis >= 2 (-2 for the negative side), inside its window for R >= 1.
+      // axis neighbours at distance k = 2..5 (sparse returns: the next beam
+      // or azimuth step is often several voxels away): c + k e_x (lanes
+      // 9-16), c + k e_y (lanes 17-24), c + k e_z (lane 25: the centre row's
+      // bits cz-5 .. cz+5). Each cuts the half-space 2 k o_axis > k^2, i.e.
+      // o_axis >= k/2 + 1 on its side (inside its window: o_axis >= k - R).
+      // Bits: 4 per direction (k = 2..5): x+ 0-3, x- 4-7, y+ 8-11, y- 12-15,
+      // z+ 16-19, z- 20-23.
       uint32_t ax = 0;
-      if (lane >= 9 && lane < 17) {
-        const int j = (lane - 9) & 3, k = 2 + (j & 1), sg = j < 2 ? 1 : -1;
-        const bool along_x = lane < 13;
+      if (lane >= 9 && lane < 25) {
+        const int j = (lane - 9) & 7, k = 2 + (j & 3), sg = j < 4 ? 1 : -1;
+        const bool along_x = lane < 17;
         const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
         const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(qx) : -1;
         if (lq >= 0) {
           const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
           ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
         }
-      } else if (lane == 17 && cz >= 3 && cz + 3 < a.nzp) {  // padding bits are never set
+      } else if (lane == 25 && cz >= 5 && cz + 5 < a.nzp) {  // padding bits are never set
         const int64_t lq = a.xm.local(cx);
         if (lq >= 0) {
-          const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 3);
+          const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 5);
           const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-          const uint32_t w1 = ((idx & 31) > 25) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
-          const uint32_t b7 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7Fu;  // bit i: cz - 3 + i
-          // z+2, z+3 -> bits 8, 9; z-2, z-3 -> bits 10, 11
-          ax = (((b7 >> 5) & 1u) << 8) | (((b7 >> 6) & 1u) << 9) | (((b7 >> 1) & 1u) << 10) | ((b7 & 1u) << 11);
+          const uint32_t w1 = ((idx & 31) > 21) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+          const uint32_t b11 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7FFu;  // bit i: cz - 5 + i
+          const uint32_t up = (b11 >> 7) & 0xFu;                                // cz+2 .. cz+5
+          const uint32_t dn = __brev(b11 & 0xFu) >> 28;                         // cz-2 .. cz-5
+          ax = (up << 16) | (dn << 20);
         }
       }
       const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
@@ -657,14 +660,21 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
         }
       }
 #undef NB
-      // axis neighbours at distance 2-3 (bits: x+ 0-1, x- 2-3, y+ 4-5, y- 6-7,
-      // z+ 8-9, z- 10-11)
-      if ((axm & 0x003u) && dx >= 2) dead = true;
-      if ((axm & 0x00Cu) && dx <= -2) dead = true;
-      if (axm & 0x030u) yhi = min(yhi, 1);
-      if (axm & 0x0C0u) ylo = max(ylo, -1);
-      if (axm & 0x300u) mp[1] = min(mp[1], 2);   // dz >= 2 culled
-      if (axm & 0xC00u) mm[1] = max(mm[1], -2);  // dz <= -2 culled
+      // axis neighbours: per direction the nearest present k gives the cut
+      // threshold thr = max(k / 2 + 1, k - R) (0 when none)
+      int thr[6];
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        const uint32_t bits = (axm >> (4 * d)) & 0xFu;
+        const int k = bits ? 2 + (__ffs(bits) - 1) : 0;
+        thr[d] = k ? max(k / 2 + 1, k - R) : 0;
+      }
+      if (thr[0] && dx >= thr[0]) dead = true;
+      if (thr[1] && dx <= -thr[1]) dead = true;
+      if (thr[2]) yhi = min(yhi, thr[2] - 1);
+      if (thr[3]) ylo = max(ylo, 1 - thr[3]);
+      if (thr[4]) mp[1] = min(mp[1], thr[4]);   // dz >= thr culled
+      if (thr[5]) mm[1] = max(mm[1], -thr[5]);  // dz <= -thr culled
       const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
       int pre = cnt;  // inclusive scan
 #pragma unroll
