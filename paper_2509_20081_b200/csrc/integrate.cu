@@ -557,6 +557,7 @@ struct CullArgs {
 };
 
 constexpr int kFar = 1 << 20;
+constexpr int kPlaneGatherBelow = 8;  // certified adjacent centres below which plane neighbours are read
 constexpr int kCullWarps = 4;  // centres per block batch (one per warp; 4 measured best of 1/2/4/8)
 
 // row task: bits 0-36 row start / 8 (cells), 37-38 first chunk, 39-40 last
@@ -635,6 +636,46 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       }
       const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
       const uint32_t axm = __reduce_or_sync(0xffffffffu, ax);
+      // sparse neighbourhood (few of the 26 adjacent centres certified): also
+      // gather the norm-2 plane neighbours below (a second round of loads,
+      // skipped for dense surfaces where they add little)
+      uint32_t plm = 0;
+      if (__popc(nb) < kPlaneGatherBelow) {
+        // plane neighbours of norm 2 with one zero coordinate besides the
+        // axes: (a, b, 0) (lanes 0-11, bit cz) and (a, 0, c) (lanes 12-15: rows
+        // cx+1, cx-1, cx+2, cx-2 at bits cz-2 .. cz+2). Their cuts are
+        // constant per lane (a dy interval or a dz threshold). Index i of
+        // either list: |a|,|b| = (2,1) for i < 4, (1,2) for i < 8, (2,2) else;
+        // first sign + for even i>>1, second sign + for even i.
+        uint32_t plb = 0;
+        if (lane < 12) {
+          const int g = lane >> 2, sa = (lane & 2) ? -1 : 1, sb = (lane & 1) ? -1 : 1;
+          const int pa = sa * (g == 1 ? 1 : 2), pb = sb * (g == 0 ? 1 : 2);
+          const int64_t qy = cy + pb;
+          const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(cx + pa) : -1;
+          if (lq >= 0) {
+            const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+            plb = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
+          }
+        } else if (lane < 16 && cz >= 2 && cz + 2 < a.nzp) {
+          const int pa = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
+          const int64_t lq = a.xm.local(cx + pa);
+          if (lq >= 0) {
+            const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 2);
+            const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+            const uint32_t w1 = ((idx & 31) > 27) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+            const uint32_t b5 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x1Fu;  // bit i: cz - 2 + i
+            const uint32_t cp1 = (b5 >> 3) & 1u, cm1 = (b5 >> 1) & 1u, cp2 = (b5 >> 4) & 1u, cm2 = b5 & 1u;
+            uint32_t xz = 0;
+            if (lane == 12) xz = (cp2 << 4) | (cm2 << 5);
+            if (lane == 13) xz = (cp2 << 6) | (cm2 << 7);
+            if (lane == 14) xz = cp1 | (cm1 << 1) | (cp2 << 8) | (cm2 << 9);
+            if (lane == 15) xz = (cp1 << 2) | (cm1 << 3) | (cp2 << 10) | (cm2 << 11);
+            plb = xz << 12;
+          }
+        }
+        plm = __reduce_or_sync(0xffffffffu, plb);
+      }
 #define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
       // per lane: kernel x-offset dx, its dy interval and z-cut terms
       const int dx = lane - R;
@@ -675,6 +716,26 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       if (thr[3]) ylo = max(ylo, 1 - thr[3]);
       if (thr[4]) mp[1] = min(mp[1], thr[4]);   // dz >= thr culled
       if (thr[5]) mm[1] = max(mm[1], -thr[5]);  // dz <= -thr culled
+      // plane neighbours: (a, b, 0) cut b dy >= T - a dx, (a, 0, c) cut
+      // c dz >= T - a dx, T = |delta|^2 / 2 + 1, each inside its window
+      if (plm) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const int g = i >> 2, s1 = (i & 2) ? -1 : 1, s2 = (i & 1) ? -1 : 1;
+          const int pa = s1 * (g == 1 ? 1 : 2), q = s2 * (g == 0 ? 1 : 2);
+          const bool xw = dx - pa <= R && pa - dx <= R;  // v inside e's x-window
+          const int num = (g == 2 ? 5 : 3) - pa * dx;
+          const int cdiv = g == 0 ? num : (num + 1) >> 1;  // ceil(num / |q|)
+          if (xw && ((plm >> i) & 1u)) {  // (pa, q, 0): dy cut
+            if (q > 0) yhi = min(yhi, max(cdiv, q - R) - 1);
+            else ylo = max(ylo, min(-cdiv, R + q) + 1);
+          }
+          if (xw && ((plm >> (12 + i)) & 1u)) {  // (pa, 0, q): dz cut
+            if (q > 0) mp[1] = min(mp[1], max(cdiv, q - R));
+            else mm[1] = max(mm[1], min(-cdiv, R + q));
+          }
+        }
+      }
       const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
       int pre = cnt;  // inclusive scan
 #pragma unroll
