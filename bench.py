@@ -322,7 +322,7 @@ def main():
         torch.cuda.synchronize()
         L.dbt_profile_reset(sg.local.handle)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        cnt = {"applied": 0, "swept": 0, "written": 0, "skipped": 0}
+        cnt = {"applied": 0, "swept": 0, "written": 0, "skipped": 0, "rows": 0}
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -342,6 +342,7 @@ def main():
                 cnt["swept"] += sts[0].unique_centers
                 cnt["written"] += sts[0].voxels_written
                 cnt["skipped"] += sts[0].centers_skipped
+                cnt["rows"] += sts[0].rows_swept
         torch.cuda.synchronize()
         launches = L.dbt_launch_count() - launches0
         dev_ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -360,7 +361,7 @@ def main():
     # per-kernel device time: a second, identical pass with CUDA events around
     # every kernel on its own stream (not inside the timed region above)
     prof_ms, _, pc = run_pass(timed=False)
-    swept, written, skipped = pc["swept"], pc["written"], pc["skipped"]
+    swept, written, skipped, rows = pc["swept"], pc["written"], pc["skipped"], pc["rows"]
     names = ctypes.create_string_buffer(32 * 16)
     ms = (ctypes.c_double * 16)()
     cnt_ = (ctypes.c_int64 * 16)()
@@ -377,10 +378,12 @@ def main():
     applied_per_launch = applied / max(args.steps, 1)
     alg_bytes = b_alg(shadow_cells) * applied_per_launch / max(world, 1)
     achieved = alg_bytes / (sweep["avg_us"] * 1e-6) / 1e9
-    # bytes the sweep actually touches (device counters): the 1-byte distance
-    # cache over the K^3 cube of every swept centre + word RED.AND and cache
-    # store per lowered voxel (the shadow kernel runs concurrently)
-    touched = (swept * K_EDGE ** 3 + written * 5) / max(args.steps, 1)
+    # bytes the sweep actually touches (device counters): one 32-byte sector of
+    # the 1-byte distance cache per kernel row it read after culling (a row's
+    # 1-4 chunks span 1-2 sectors) + the 4-byte RED.AND and the cache byte of
+    # every lowered voxel (the shadow kernel runs concurrently). Generic
+    # (non-culling) sweep: the full K^3 cube of every swept centre.
+    touched = ((rows * 32 if rows else swept * K_EDGE ** 3) + written * 5) / max(args.steps, 1)
     traffic, lts = None, None
     tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
     if os.path.exists(tpath) and args.config == 2 and B == 1:
@@ -414,13 +417,15 @@ def main():
                      "alg_bytes_def": f"4*21^3 + 4*|S| = {b_alg(shadow_cells):.0f} B per applied return "
                                       "(SURVEY.md 8(d)) x applied returns per launch",
                      "traffic_source": "ncu dram__bytes_read+write per sweep launch (config 2), "
-                                       "profiles/dram_per_launch.json",
+                                       "profiles/kernel_traffic.json",
                      "touched_bytes_per_launch": touched,
                      "touched_gbs": touched / (sweep["avg_us"] * 1e-6) / 1e9,
                      "why_frac_above_1": "B_alg is the reference's per-return traffic; the engine sweeps each "
                                          "centre voxel once (dedup), skips centres whose stamp is already applied "
-                                         "(certificates) and reads a 1-byte cache: touched/traffic are the bytes "
-                                         "actually moved",
+                                         "(certificates), skips the voxels a closer certified neighbour centre "
+                                         "covers (culling) and reads a 1-byte cache: touched/traffic are the "
+                                         "bytes actually moved",
+                     "rows_swept_per_launch": rows / max(args.steps, 1),
                      "centres_swept_per_launch": swept / max(args.steps, 1),
                      "returns_skipped_per_launch": skipped / max(args.steps, 1),
                      "l2_probe": {"red_and_gops": l2[0], "red_and_gbs": l2[1], "ldcg_gbs": l2[2],

@@ -88,6 +88,8 @@ typedef struct dbt_stats {
                                component below 2^-1020 or above 2^993); 0 in practice */
   double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */
   double device_ms;         /* CUDA-event time of the device work (H2D .. stats D2H) */
+  int64_t rows_swept;       /* kernel z-rows the sweep read (after neighbour culling);
+                               launch-wide, reported on the first scan */
 } dbt_stats;
 
 DBT_API const char* dbt_last_error(void);

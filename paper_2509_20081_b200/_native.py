@@ -53,6 +53,7 @@ class Stats(ctypes.Structure):
         ("bin_fallbacks", ctypes.c_int64),
         ("elapsed_ms", ctypes.c_double),
         ("device_ms", ctypes.c_double),
+        ("rows_swept", ctypes.c_int64),
     ]
 
 

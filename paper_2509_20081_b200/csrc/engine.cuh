@@ -126,6 +126,8 @@ struct LaunchCounters {
   unsigned long long changed;    // mask cells changed (voxels_written)
   unsigned long long skipped;    // centres whose stamp was already applied (cache byte 0)
   unsigned long long work;       // sweep work-item cursor (dynamic fetch)
+  unsigned long long rows;       // kernel rows the sweep read
+  unsigned long long pad[3];
 };
 
 struct ProfEvent {

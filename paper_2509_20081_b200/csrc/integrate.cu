@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
   const int R = a.R, K = a.K;
   const int64_t n_items = (int64_t)a.lc->n_unique;
   const int64_t sx = a.ny * a.nzp;
-  unsigned long long changed = 0;
+  unsigned long long changed = 0, rows_done = 0;
   while (true) {
     if (threadIdx.x == 0) {
       batch0 = batch_next;
@@ -794,6 +794,7 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
       for (int r = 0; r < 2; ++r) {
         const int qi = i + r * blockDim.x;
         const uint64_t task = qi < nq ? queue[qi] : kEmptyKey;
+        rows_done += task != kEmptyKey;
         rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
         const int c0 = (int)((task >> 37) & 3), c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
         cb[r] = c0;
@@ -828,14 +829,19 @@ __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a)
     }
     __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
-  // one atomic per block (same-address atomics serialise at L2)
-  __shared__ unsigned long long blk_changed;
-  if (threadIdx.x == 0) blk_changed = 0;
-  for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
+  // one atomic per block and counter (same-address atomics serialise at L2)
+  __shared__ unsigned long long blk_changed, blk_rows;
+  if (threadIdx.x == 0) blk_changed = blk_rows = 0;
+  for (int o = 16; o; o >>= 1) {
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    rows_done += __shfl_xor_sync(0xffffffffu, rows_done, o);
+  }
   __syncthreads();
   if (lane == 0 && changed) atomicAdd(&blk_changed, changed);
+  if (lane == 0 && rows_done) atomicAdd(&blk_rows, rows_done);
   __syncthreads();
   if (threadIdx.x == 0 && blk_changed) atomicAdd(&a.lc->changed, blk_changed);
+  if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
 }
 
 typedef void (*SweepFn)(SweepArgs);
@@ -1277,6 +1283,7 @@ void fill_stats(dbt_grid* g, const dbt_params* p, dbt_stats* out, int S) {
       o.voxels_written = (int64_t)g->h_lcnt->changed;
       o.unique_centers = (int64_t)g->h_lcnt->n_unique;
       o.centers_skipped = (int64_t)g->h_lcnt->skipped;
+      o.rows_swept = (int64_t)g->h_lcnt->rows;
     }
   }
 }

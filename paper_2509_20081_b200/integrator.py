@@ -117,12 +117,14 @@ class FrameStats:
     centers_skipped: int = field(default=0, compare=False)
     bin_fallbacks: int = field(default=0, compare=False)
     device_ms: float = field(default=0.0, compare=False)
+    rows_swept: int = field(default=0, compare=False)
 
     @classmethod
     def from_native(cls, s: _native.Stats, elapsed_ms: float | None = None) -> "FrameStats":
         return cls(int(s.points_in), int(s.points_discarded), int(s.voxels_written),
                    float(s.elapsed_ms if elapsed_ms is None else elapsed_ms), int(s.points_applied),
-                   int(s.unique_centers), int(s.centers_skipped), int(s.bin_fallbacks), float(s.device_ms))
+                   int(s.unique_centers), int(s.centers_skipped), int(s.bin_fallbacks), float(s.device_ms),
+                   int(s.rows_swept))
 
 
 def _scan_times(scan: ScanFrame) -> np.ndarray:

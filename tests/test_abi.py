@@ -47,7 +47,7 @@ def test_ctypes_mirror_binds_every_symbol():
 
 def test_abi_struct_layout():
     assert ctypes.sizeof(_native.Params) == 24
-    assert ctypes.sizeof(_native.Stats) == 72
+    assert ctypes.sizeof(_native.Stats) == 80
     txt = HEADER.read_text()
     for f, _ in _native.Params._fields_:
         assert f in txt
