@@ -501,6 +501,35 @@ class TestOrderIndependence:
             assert cases.sha(m) == ref["mask"] and cases.sha(s_) == ref["sign"] and cases.sha(h) == ref["hits"]
 
 
+class TestLongSequenceSnapshots:
+    """Reference acceptance C3 (test_acceptance.py:73-102: byte-identical
+    snapshots for threads 1 vs 8 over a 200-frame sequence) for this engine:
+    a 40-scan config-2 trajectory integrated scan by scan, in batches of 8 and
+    in batches of 5 gives byte-identical DBTSDF01 snapshots."""
+
+    def test_batching_invariance_bytes(self, tmp_path):
+        import workloads
+
+        from paper_2509_20081_b200 import save_grid
+
+        w = workloads.get(2)
+        frames = [ScanFrame(points=w.scan(k), pose=w.poses[k]) for k in range(40)]
+        bank = build_kernel_bank(shadow_radius=w.shadow_radius)
+        blobs = []
+        for batch in (1, 8, 5):
+            g = new_grid(w.dims, w.voxel_size, w.origin)
+            g.release_host()
+            for i in range(0, len(frames), batch):
+                if batch == 1:
+                    integrate_frame(g, bank, frames[i], IntegrationParams())
+                else:
+                    integrate_frames(g, bank, frames[i:i + batch], IntegrationParams())
+            p = tmp_path / f"b{batch}.dbtsdf"
+            save_grid(g, p)
+            blobs.append(p.read_bytes())
+        assert blobs[0] == blobs[1] == blobs[2]
+
+
 class TestInterleavedSharding:
     """Interleaved x-blocks (dbt_grid_create_interleaved): each part stamps
     only its blocks; the parts reassemble to the reference grid. Both sweeps
