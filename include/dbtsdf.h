@@ -210,6 +210,31 @@ DBT_API int64_t dbt_launch_count(void);
  * 8-byte ld.cg GB/s. Best of 4 timed runs after a warm-up. */
 DBT_API int dbt_probe_l2(int device, int64_t bytes, double* out);
 
+/* ---- marching cubes on the device (mesher.py:43-110) ---- */
+/* The lookup tables are an input: the caller copies them from the
+ * reference's bitsdf/_mc_tables.py (EDGE_TABLE :9, TRI_TABLE :44,
+ * CORNER_OFFSETS :312, EDGE_BASE :319, EDGE_AXIS :324), row-major int32. */
+typedef struct dbt_mc_tables {
+  int32_t edge_table[256];
+  int32_t tri_table[256 * 16];
+  int32_t corner_offsets[8 * 3];
+  int32_t edge_base[12 * 3];
+  int32_t edge_axis[12];
+} dbt_mc_tables;
+typedef struct dbt_mesh dbt_mesh;
+/* extract_mesh(grid, iso) (mesher.py:43): vertices and triangles identical to
+ * the reference's (same order, float64 vertices bit for bit), kept in device
+ * memory until dbt_mesh_destroy. Whole (unsharded) grids only. An empty mesh
+ * is a valid handle with zero counts. */
+DBT_API int dbt_mesh_extract(dbt_grid* g, double iso, const dbt_mc_tables* tables, dbt_mesh** out,
+                     int64_t* n_vertices, int64_t* n_triangles);
+DBT_API int dbt_mesh_info(const dbt_mesh* m, int64_t* n_vertices, int64_t* n_triangles);
+/* vertices: n_vertices*3 float64; triangles: n_triangles*3 int64 (either may be NULL) */
+DBT_API int dbt_mesh_download(const dbt_mesh* m, double* vertices, int64_t* triangles);
+/* device pointers of the same arrays (valid until dbt_mesh_destroy) */
+DBT_API int dbt_mesh_device_buffers(const dbt_mesh* m, const double** vertices, const int64_t** triangles);
+DBT_API int dbt_mesh_destroy(dbt_mesh* m);
+
 /* pinned host buffers for callers without a CUDA runtime of their own */
 DBT_API int dbt_host_alloc(int64_t bytes, void** out);
 DBT_API int dbt_host_free(void* p);

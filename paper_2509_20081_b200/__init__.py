@@ -3,7 +3,8 @@ integrate/query API, reference pkg/src/bitsdf/__init__.py:4-32).
 
 The compute path is libdbtsdf.so (hand-written sm_100a CUDA, C ABI in
 include/dbtsdf.h); this package is the host-side mirror of the reference
-interface. Mesh extraction / metrics / file IO / CLI are outside this
+interface, plus the first consumer of the query path: device marching cubes
+(``extract_mesh``). Metrics / file IO / CLI are outside this
 build's scope.
 """
 
@@ -37,6 +38,7 @@ from .integrator import (
     integrate_points,
 )
 from .kernels import KernelBank, build_kernel_bank
+from .mesher import TriangleMesh, empty_mesh, extract_mesh, extract_mesh_device, load_mc_tables
 from .snapshot import SNAPSHOT_MAGIC, load_grid, save_grid
 
 __version__ = "0.1.0"
@@ -61,6 +63,11 @@ __all__ = [
     "integrate_frames",
     "integrate_point",
     "integrate_points",
+    "TriangleMesh",
+    "empty_mesh",
+    "extract_mesh",
+    "extract_mesh_device",
+    "load_mc_tables",
     "SNAPSHOT_MAGIC",
     "save_grid",
     "load_grid",

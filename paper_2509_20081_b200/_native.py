@@ -106,6 +106,11 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_int32)]),
     "dbt_profile_reset": (ctypes.c_int, [_vp]),
     "dbt_launch_count": (ctypes.c_int64, []),
+    "dbt_mesh_extract": (ctypes.c_int, [_vp, ctypes.c_double, _vp, ctypes.POINTER(_vp), _c_i64p, _c_i64p]),
+    "dbt_mesh_info": (ctypes.c_int, [_vp, _c_i64p, _c_i64p]),
+    "dbt_mesh_download": (ctypes.c_int, [_vp, _vp, _vp]),
+    "dbt_mesh_device_buffers": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dbt_mesh_destroy": (ctypes.c_int, [_vp]),
     "dbt_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
     "dbt_host_free": (ctypes.c_int, [_vp]),
 }

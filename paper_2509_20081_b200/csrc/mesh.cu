@@ -1,0 +1,474 @@
+// mesh.cu — marching cubes over the voxel-centre lattice, on the device
+// (reference: mesher.py:43-110).
+//
+// The reference's output is reproduced exactly:
+//   * triangles ordered by table slot k (0..4) first, then by cell in C order
+//     (mesher.py:73-87), each row the indices of its three lattice edges;
+//   * vertices = the referenced lattice edges sorted by key
+//     ((x*ny + y)*nz + z)*3 + axis (np.unique, mesher.py:88), interpolated in
+//     float64 with the reference's operation order (mesher.py:91-109).
+// Sorting is replaced by ranks: the padded storage index (x*ny + y)*nzp + z
+// orders lattice points exactly like the reference key, so an edge's vertex
+// index is the number of referenced edges before it in a 3-bit-per-point
+// bitmap (prefix per 64 points + popcount).
+//
+// Pipeline (all on the grid stream, whole grids only):
+//   flags   1 byte per voxel: bit0 inside (field < iso | field == iso & occupied,
+//           mesher.py:50, from a 66-entry host table), bit1 observed (grid.py:161-163)
+//   select  active cells (all 8 corners observed, EDGE_TABLE[cube] != 0,
+//           mesher.py:52-65) in C order (cub::DeviceSelect, counted first)
+//   cells   cube per active cell; bits 2..4 of the flags of every lattice
+//           edge its triangles use (atomicOr on the 4-byte word)
+//   ranks   referenced-edge count per 64 points, exclusive scan -> vertex count
+//   verts   one thread per 8 lattice points writes its vertices at their ranks
+//   tris    per slot an exclusive scan of "slot present" over the active cells;
+//           one thread per active cell writes its triangles
+//
+// The marching-cubes tables are an input (dbt_mc_tables, filled by the caller
+// from the reference's _mc_tables.py), not data compiled into the engine.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "engine.cuh"
+
+struct dbt_mesh {
+  int device = 0;
+  int64_t nv = 0, nf = 0;
+  double* vert = nullptr;    // (nv, 3) float64
+  int64_t* tri = nullptr;    // (nf, 3) int64
+};
+
+using namespace dbt;
+
+namespace {
+
+constexpr uint64_t kEdgeBits = 0x1C1C1C1C1C1C1C1CULL;  // bits 2..4 of every byte
+
+// derived, device-resident copy of the caller's tables
+struct MeshTab {
+  int8_t tri[256][16];
+  uint8_t slots[256];     // bit k: slot k holds a triangle (TRI_TABLE[c][3k] >= 0)
+  uint8_t active[256];    // EDGE_TABLE[c] != 0
+  uint16_t used[256];     // cube edges the present slots reference
+  int8_t axis[12];
+  int64_t eoff[12];       // storage offset of the edge's lower lattice point
+  int64_t coff[8];        // storage offset of each cube corner
+};
+
+__global__ void mesh_flags_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ flags, int64_t n,
+                                  int64_t nz, int64_t nzp, uint64_t ins_free, uint64_t ins_occ) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t f = 0;
+    if (i - (i / nzp) * nzp < nz) {
+      const uint2 c = cells[i];
+      const int len = __popc(c.x);
+      const uint64_t tab = meta_sign(c.y) == 0 ? ins_occ : ins_free;
+      f = (uint8_t)(((tab >> len) & 1u) | ((!(c.x == kFullMask && meta_hits(c.y) == 0)) << 1));
+    }
+    flags[i] = f;
+  }
+}
+
+struct CellGeom {
+  int64_t nx, ny, nz, nzp;
+  __device__ __forceinline__ bool is_cell(int64_t i) const {
+    const int64_t row = i / nzp, z = i - row * nzp;
+    if (z >= nz - 1) return false;
+    const int64_t x = row / ny, y = row - x * ny;
+    return x < nx - 1 && y < ny - 1;
+  }
+};
+
+// cube index of cell i, or -1 when a corner is unobserved (mesher.py:55-62)
+__device__ __forceinline__ int cell_cube(const uint8_t* __restrict__ flags, const MeshTab* __restrict__ t,
+                                         int64_t i) {
+  int cube = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint8_t f = flags[i + t->coff[c]];
+    if (!(f & 2)) return -1;
+    cube |= (f & 1) << c;
+  }
+  return cube;
+}
+
+struct ActiveCell {
+  const uint8_t* flags;
+  const MeshTab* t;
+  CellGeom geo;
+  __device__ __forceinline__ bool operator()(int64_t i) const {
+    if (!geo.is_cell(i)) return false;
+    const int cube = cell_cube(flags, t, i);
+    return cube >= 0 && t->active[cube];
+  }
+};
+
+__global__ void mesh_count_kernel(const uint8_t* __restrict__ flags, const MeshTab* __restrict__ t, CellGeom geo,
+                                  int64_t n, unsigned long long* __restrict__ out) {
+  ActiveCell pred{flags, t, geo};
+  unsigned long long k = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    k += pred(i);
+  for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  __shared__ unsigned long long s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s[w];
+    if (tot) atomicAdd(out, tot);
+  }
+}
+
+// cube of every active cell + referenced-edge bits (flags bits 2..4)
+__global__ void mesh_cells_kernel(const int64_t* __restrict__ cell, int64_t n_active, uint8_t* __restrict__ flags,
+                                  const MeshTab* __restrict__ t, uint8_t* __restrict__ cube_out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_active;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = cell[j];
+    int cube = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cube |= (flags[i + t->coff[c]] & 1) << c;
+    cube_out[j] = (uint8_t)cube;
+    for (uint32_t u = t->used[cube]; u; u &= u - 1) {
+      const int e = __ffs(u) - 1;
+      const int64_t p = i + t->eoff[e];
+      atomicOr(reinterpret_cast<unsigned int*>(flags + (p & ~int64_t(3))),
+               (1u << (2 + t->axis[e])) << (8 * (int)(p & 3)));
+    }
+  }
+}
+
+// referenced edges per 64 lattice points (entry n_groups stays 0 for the scan)
+__global__ void mesh_group_kernel(const uint64_t* __restrict__ fw, int64_t n_groups,
+                                  unsigned long long* __restrict__ cnt) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= n_groups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long k = 0;
+    if (g < n_groups) {
+      const uint4* q = reinterpret_cast<const uint4*>(fw + 8 * g);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint4 v = q[w];
+        k += __popcll((((uint64_t)v.y << 32) | v.x) & kEdgeBits) + __popcll((((uint64_t)v.w << 32) | v.z) & kEdgeBits);
+      }
+    }
+    cnt[g] = k;
+  }
+}
+
+// vertex index of lattice edge (p, axis): referenced edges before it
+__device__ __forceinline__ int64_t edge_rank(const uint64_t* __restrict__ fw,
+                                             const unsigned long long* __restrict__ pre, int64_t p, int axis) {
+  const int64_t w = p >> 3;
+  int64_t r = (int64_t)pre[p >> 6];
+  for (int64_t k = w & ~int64_t(7); k < w; ++k) r += __popcll(fw[k] & kEdgeBits);
+  const int b = (int)(p & 7);
+  const uint64_t below = (b ? ((1ull << (8 * b)) - 1) : 0ull) | (((1ull << axis) - 1) << (8 * b + 2));
+  return r + __popcll(fw[w] & kEdgeBits & below);
+}
+
+// field value of a voxel: sigma * (popcount * voxel_size) (grid.py:170-175)
+__device__ __forceinline__ double field_at(const uint2* __restrict__ cells, int64_t i, double vs) {
+  const uint2 c = cells[i];
+  const double d = __dmul_rn((double)__popc(c.x), vs);
+  return __dmul_rn(meta_sign(c.y) == 0 ? -1.0 : 1.0, d);
+}
+
+struct VertArgs {
+  int64_t ny, nzp, n_words;
+  double vs, iso, org[3];
+};
+
+// mesher.py:91-109, one thread per 8 lattice points
+__global__ void mesh_vert_kernel(const uint2* __restrict__ cells, const uint64_t* __restrict__ fw,
+                                 const unsigned long long* __restrict__ pre, VertArgs a,
+                                 double* __restrict__ vert) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.n_words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t bits = fw[w] & kEdgeBits;
+    if (!bits) continue;
+    int64_t r = (int64_t)pre[w >> 3];
+    for (int64_t k = w & ~int64_t(7); k < w; ++k) r += __popcll(fw[k] & kEdgeBits);
+    for (; bits; bits &= bits - 1, ++r) {
+      const int pos = __ffsll((long long)bits) - 1;
+      const int axis = (pos & 7) - 2;
+      const int64_t p = w * 8 + (pos >> 3);
+      const int64_t row = p / a.nzp, z = p - row * a.nzp;
+      const int64_t x = row / a.ny, y = row - x * a.ny;
+      const int64_t step = axis == 0 ? a.ny * a.nzp : (axis == 1 ? a.nzp : 1);
+      const double v1 = field_at(cells, p, a.vs), v2 = field_at(cells, p + step, a.vs);
+      const double den = __dsub_rn(v2, v1);
+      double t = den != 0.0 ? __ddiv_rn(__dsub_rn(a.iso, v1), den) : 0.0;
+      t = t < 0.0 ? 0.0 : t;  // np.clip keeps -0.0 and NaN
+      t = t > 1.0 ? 1.0 : t;
+      const int64_t b[3] = {x, y, z};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double p1 = __dadd_rn(a.org[d], __dmul_rn((double)b[d] + 0.5, a.vs));
+        const double p2 = __dadd_rn(a.org[d], __dmul_rn((double)(b[d] + (d == axis)) + 0.5, a.vs));
+        vert[3 * r + d] = __dadd_rn(p1, __dmul_rn(t, __dsub_rn(p2, p1)));
+      }
+    }
+  }
+}
+
+struct SlotFlag {
+  const uint8_t* cube;
+  const MeshTab* t;
+  int64_t n;
+  int k;
+  __device__ __forceinline__ unsigned long long operator()(int64_t j) const {
+    return j < n ? (unsigned long long)((t->slots[cube[j]] >> k) & 1u) : 0ull;
+  }
+};
+
+// mesher.py:72-89: triangle (slot k, j-th cell holding slot k) -> row
+// slot_base[k] + rank_k(j); entries are vertex ranks of its three edges
+__global__ void mesh_tri_kernel(const int64_t* __restrict__ cell, const uint8_t* __restrict__ cube_in,
+                                int64_t n_active, const unsigned long long* __restrict__ rank, int64_t rank_pitch,
+                                const MeshTab* __restrict__ t, const uint64_t* __restrict__ fw,
+                                const unsigned long long* __restrict__ pre, int64_t base0, int64_t base1,
+                                int64_t base2, int64_t base3, int64_t base4, int64_t* __restrict__ tri) {
+  const int64_t base[5] = {base0, base1, base2, base3, base4};
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_active;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = cell[j];
+    const int cube = cube_in[j];
+    const int slots = t->slots[cube];
+    for (int k = 0; k < 5; ++k) {
+      if (!((slots >> k) & 1)) continue;
+      const int64_t row = base[k] + (int64_t)rank[k * rank_pitch + j];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int e = t->tri[cube][3 * k + m];
+        tri[3 * row + m] = edge_rank(fw, pre, i + t->eoff[e], t->axis[e]);
+      }
+    }
+  }
+}
+
+int blocks_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+// device scratch freed on every exit path
+struct Scratch {
+  std::vector<void*> ptrs;
+  template <class T>
+  int alloc(T** p, int64_t count) {
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, (size_t)count * sizeof(T));
+    if (e != cudaSuccess) return cuda_error(e, "mesh scratch allocation");
+    ptrs.push_back((void*)*p);
+    return DBT_OK;
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+int check_tables(const dbt_mc_tables* tb, MeshTab* h) {
+  if (!tb) return set_error(DBT_ERR_CONFIG, "marching-cubes tables are required");
+  std::memset(h, 0, sizeof(*h));
+  for (int e = 0; e < 12; ++e) {
+    const int ax = tb->edge_axis[e];
+    if (ax < 0 || ax > 2) return set_error(DBT_ERR_CONFIG, "EDGE_AXIS entries must be 0, 1 or 2");
+    for (int d = 0; d < 3; ++d)
+      if (tb->edge_base[3 * e + d] < 0 || tb->edge_base[3 * e + d] > 1)
+        return set_error(DBT_ERR_CONFIG, "EDGE_BASE entries must be 0 or 1");
+    // the edge runs from its base to base + unit(axis): both inside the cube
+    if (tb->edge_base[3 * e + ax] != 0) return set_error(DBT_ERR_CONFIG, "EDGE_BASE/EDGE_AXIS leave the cube");
+    h->axis[e] = (int8_t)ax;
+  }
+  for (int c = 0; c < 8; ++c)
+    for (int d = 0; d < 3; ++d)
+      if (tb->corner_offsets[3 * c + d] < 0 || tb->corner_offsets[3 * c + d] > 1)
+        return set_error(DBT_ERR_CONFIG, "CORNER_OFFSETS entries must be 0 or 1");
+  for (int c = 0; c < 256; ++c) {
+    h->active[c] = tb->edge_table[c] != 0;
+    for (int m = 0; m < 16; ++m) {
+      const int v = tb->tri_table[16 * c + m];
+      if (v < -1 || v > 11) return set_error(DBT_ERR_CONFIG, "TRI_TABLE entries must be -1..11");
+      h->tri[c][m] = (int8_t)v;
+    }
+    for (int k = 0; k < 5; ++k) {
+      if (h->tri[c][3 * k] < 0) continue;
+      h->slots[c] |= (uint8_t)(1u << k);
+      for (int m = 0; m < 3; ++m) {
+        const int e = h->tri[c][3 * k + m];
+        if (e < 0) return set_error(DBT_ERR_CONFIG, "TRI_TABLE slot with fewer than three edges");
+        h->used[c] |= (uint16_t)(1u << e);
+      }
+    }
+  }
+  return DBT_OK;
+}
+
+int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& h, dbt_mesh* m) {
+  int rc;
+  const int64_t nx = g->nx, ny = g->ny, nz = g->nz, nzp = g->nzp;
+  if (nx < 2 || ny < 2 || nz < 2) return DBT_OK;  // empty mesh (mesher.py:45-47)
+  cudaStream_t st = g->stream;
+  // storage offsets of corners / edge base points
+  for (int c = 0; c < 8; ++c)
+    h.coff[c] = (tables->corner_offsets[3 * c] * ny + tables->corner_offsets[3 * c + 1]) * nzp +
+                tables->corner_offsets[3 * c + 2];
+  for (int e = 0; e < 12; ++e)
+    h.eoff[e] = (tables->edge_base[3 * e] * ny + tables->edge_base[3 * e + 1]) * nzp + tables->edge_base[3 * e + 2];
+  // inside bit per (sign, popcount): field = sigma * (popcount * vs) (mesher.py:50)
+  uint64_t ins_free = 0, ins_occ = 0;
+  for (int k = 0; k <= 32; ++k) {
+    const double d = (double)k * g->vs;
+    const double fo = -1.0 * d, ff = 1.0 * d;
+    if (ff < iso) ins_free |= 1ull << k;
+    if (fo < iso || fo == iso) ins_occ |= 1ull << k;
+  }
+
+  const int64_t n = g->n_cells;                       // padded storage points
+  const int64_t n_groups = (n + 63) / 64, n_words = n_groups * 8;
+  Scratch s;
+  MeshTab* d_tab;
+  uint8_t* flags;
+  unsigned long long *pre, *d_cnt;
+  if ((rc = s.alloc(&d_tab, 1)) || (rc = s.alloc(&flags, n_groups * 64)) || (rc = s.alloc(&pre, n_groups + 1)) ||
+      (rc = s.alloc(&d_cnt, 8)))
+    return rc;
+  DBT_CUDA(cudaMemcpyAsync(d_tab, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  DBT_CUDA(cudaMemsetAsync(flags + n, 0, (size_t)(n_groups * 64 - n), st));
+  DBT_CUDA(cudaMemsetAsync(d_cnt, 0, 8, st));
+  mesh_flags_kernel<<<blocks_for(n), 256, 0, st>>>(g->cells, flags, n, nz, nzp, ins_free, ins_occ);
+  DBT_CHECK_LAUNCH("mesh_flags_kernel");
+  const CellGeom geo{nx, ny, nz, nzp};
+  mesh_count_kernel<<<blocks_for(n), 256, 0, st>>>(flags, d_tab, geo, n, d_cnt);
+  DBT_CHECK_LAUNCH("mesh_count_kernel");
+  unsigned long long n_active = 0;
+  DBT_CUDA(cudaMemcpyAsync(&n_active, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  if (n_active == 0) return DBT_OK;  // empty mesh (mesher.py:66-67)
+  const int64_t A = (int64_t)n_active;
+  int64_t* cell;
+  uint8_t* cube;
+  unsigned long long* rank;  // 5 x (A + 1)
+  if ((rc = s.alloc(&cell, A)) || (rc = s.alloc(&cube, A)) || (rc = s.alloc(&rank, 5 * (A + 1)))) return rc;
+
+  // C-order compaction of the active cells
+  thrust::counting_iterator<int64_t> idx(0);
+  ActiveCell pred{flags, d_tab, geo};
+  size_t tmp_sel = 0, tmp_scan = 0, tmp_rank = 0;
+  DBT_CUDA(cub::DeviceSelect::If(nullptr, tmp_sel, idx, cell, d_cnt + 1, n, pred, st));
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, pre, n_groups + 1, st));
+  auto slot_it = thrust::make_transform_iterator(idx, SlotFlag{cube, d_tab, A, 0});
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_rank, slot_it, rank, A + 1, st));
+  void* tmp;
+  if ((rc = s.alloc((uint8_t**)&tmp, (int64_t)std::max({tmp_sel, tmp_scan, tmp_rank})))) return rc;
+  size_t tb = tmp_sel;
+  DBT_CUDA(cub::DeviceSelect::If(tmp, tb, idx, cell, d_cnt + 1, n, pred, st));
+
+  mesh_cells_kernel<<<blocks_for(A), 256, 0, st>>>(cell, A, flags, d_tab, cube);
+  DBT_CHECK_LAUNCH("mesh_cells_kernel");
+  const uint64_t* fw = reinterpret_cast<const uint64_t*>(flags);
+  mesh_group_kernel<<<blocks_for(n_groups + 1), 256, 0, st>>>(fw, n_groups, pre);
+  DBT_CHECK_LAUNCH("mesh_group_kernel");
+  tb = tmp_scan;
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, pre, n_groups + 1, st));
+  for (int k = 0; k < 5; ++k) {
+    tb = tmp_rank;
+    auto it = thrust::make_transform_iterator(idx, SlotFlag{cube, d_tab, A, k});
+    DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, it, rank + k * (A + 1), A + 1, st));
+  }
+  unsigned long long tot[6];
+  DBT_CUDA(cudaMemcpyAsync(tot, pre + n_groups, 8, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaMemcpy2DAsync(tot + 1, 8, rank + A, 8 * (A + 1), 8, 5, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  m->nv = (int64_t)tot[0];
+  int64_t base[5];
+  for (int k = 0; k < 5; ++k) {
+    base[k] = m->nf;
+    m->nf += (int64_t)tot[1 + k];
+  }
+  cudaError_t e1 = cudaMalloc((void**)&m->vert, (size_t)std::max<int64_t>(1, m->nv) * 24);
+  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc((void**)&m->tri, (size_t)std::max<int64_t>(1, m->nf) * 24) : e1;
+  if (e2 != cudaSuccess) return cuda_error(e2, "mesh output allocation");
+
+  VertArgs va{ny, nzp, n_words, g->vs, iso, {g->org[0], g->org[1], g->org[2]}};
+  mesh_vert_kernel<<<blocks_for(n_words), 256, 0, st>>>(g->cells, fw, pre, va, m->vert);
+  DBT_CHECK_LAUNCH("mesh_vert_kernel");
+  mesh_tri_kernel<<<blocks_for(A), 256, 0, st>>>(cell, cube, A, rank, A + 1, d_tab, fw, pre, base[0], base[1],
+                                                 base[2], base[3], base[4], m->tri);
+  DBT_CHECK_LAUNCH("mesh_tri_kernel");
+  DBT_CUDA(cudaStreamSynchronize(st));
+  return DBT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dbt_mesh_extract(dbt_grid* g, double iso, const dbt_mc_tables* tables, dbt_mesh** out, int64_t* n_vertices,
+                     int64_t* n_triangles) {
+  if (!g || !out) return set_error(DBT_ERR_CONFIG, "null grid or output handle");
+  *out = nullptr;
+  MeshTab h;
+  int rc = check_tables(tables, &h);
+  if (rc) return rc;
+  if (g->xm.w != 0 || g->xm.x0 != 0 || g->xm.x1 != g->nx)
+    return set_error(DBT_ERR_CONFIG, "mesh extraction needs a whole (unsharded) grid");
+  rc = grid_set_device(g);
+  if (!rc) rc = fold_pending(g, g->stream);
+  if (rc) return rc;
+  dbt_mesh* m = new dbt_mesh();
+  m->device = g->device;
+  rc = extract_into(g, iso, tables, h, m);
+  if (rc) {
+    dbt_mesh_destroy(m);
+    return rc;
+  }
+  *out = m;
+  if (n_vertices) *n_vertices = m->nv;
+  if (n_triangles) *n_triangles = m->nf;
+  return DBT_OK;
+}
+
+int dbt_mesh_info(const dbt_mesh* m, int64_t* n_vertices, int64_t* n_triangles) {
+  if (!m) return set_error(DBT_ERR_CONFIG, "null mesh handle");
+  if (n_vertices) *n_vertices = m->nv;
+  if (n_triangles) *n_triangles = m->nf;
+  return DBT_OK;
+}
+
+int dbt_mesh_download(const dbt_mesh* m, double* vertices, int64_t* triangles) {
+  if (!m) return set_error(DBT_ERR_CONFIG, "null mesh handle");
+  DBT_CUDA(cudaSetDevice(m->device));
+  if (m->nv && vertices) DBT_CUDA(cudaMemcpy(vertices, m->vert, (size_t)m->nv * 24, cudaMemcpyDeviceToHost));
+  if (m->nf && triangles) DBT_CUDA(cudaMemcpy(triangles, m->tri, (size_t)m->nf * 24, cudaMemcpyDeviceToHost));
+  return DBT_OK;
+}
+
+int dbt_mesh_device_buffers(const dbt_mesh* m, const double** vertices, const int64_t** triangles) {
+  if (!m) return set_error(DBT_ERR_CONFIG, "null mesh handle");
+  if (vertices) *vertices = m->vert;
+  if (triangles) *triangles = m->tri;
+  return DBT_OK;
+}
+
+int dbt_mesh_destroy(dbt_mesh* m) {
+  if (!m) return DBT_OK;
+  cudaSetDevice(m->device);
+  if (m->vert) cudaFree(m->vert);
+  if (m->tri) cudaFree(m->tri);
+  delete m;
+  return DBT_OK;
+}
+
+}  // extern "C"

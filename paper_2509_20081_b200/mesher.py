@@ -1,0 +1,151 @@
+"""Zero-isosurface extraction on the device (reference: mesher.py:26-110).
+
+``extract_mesh(grid, iso)`` returns the reference's TriangleMesh bit for bit
+(vertex order = sorted lattice-edge keys, triangle order = table slot, then
+cell in C order; float64 vertices with the reference's operation order). The
+work runs in libdbtsdf.so (csrc/mesh.cu) on the grid's device; only the
+finished arrays cross PCIe.
+
+The marching-cubes lookup tables are an input, not part of this package: they
+are read from the reference's own ``bitsdf._mc_tables`` (the package this one
+replaces), from an ``.npz`` named by ``$DBT_MC_TABLES``, or from any mapping /
+module passed as ``tables=`` holding EDGE_TABLE, TRI_TABLE, CORNER_OFFSETS,
+EDGE_BASE and EDGE_AXIS (_mc_tables.py:9-324).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigurationError
+from .grid import VoxelGrid
+
+_TABLE_FIELDS = (("EDGE_TABLE", 256), ("TRI_TABLE", 256 * 16), ("CORNER_OFFSETS", 24), ("EDGE_BASE", 36),
+                 ("EDGE_AXIS", 12))
+
+
+class McTables(ctypes.Structure):
+    """dbt_mc_tables (include/dbtsdf.h)."""
+
+    _fields_ = [("edge_table", ctypes.c_int32 * 256), ("tri_table", ctypes.c_int32 * (256 * 16)),
+                ("corner_offsets", ctypes.c_int32 * 24), ("edge_base", ctypes.c_int32 * 36),
+                ("edge_axis", ctypes.c_int32 * 12)]
+
+
+@dataclass
+class TriangleMesh:
+    """mesher.py:26-34."""
+
+    vertices: np.ndarray  # (v, 3) float64, world meters
+    triangles: np.ndarray  # (f, 3) int64
+    normals: np.ndarray | None = None  # (v, 3) unit vectors when present
+
+    @property
+    def is_empty(self) -> bool:
+        return self.vertices.shape[0] == 0
+
+
+def empty_mesh() -> TriangleMesh:
+    """mesher.py:37-40."""
+    return TriangleMesh(vertices=np.zeros((0, 3)), triangles=np.zeros((0, 3), dtype=np.int64))
+
+
+def _table_source(source):
+    if source is None:
+        path = os.environ.get("DBT_MC_TABLES")
+        if path:
+            return np.load(path)
+        try:
+            from bitsdf import _mc_tables as ref_tables  # the reference package being replaced
+        except ImportError as e:
+            raise ConfigurationError(
+                "marching-cubes tables not found: pass tables=, set DBT_MC_TABLES to an .npz, or install the "
+                "reference bitsdf package (its _mc_tables module)") from e
+        return ref_tables
+    if isinstance(source, (str, os.PathLike)):
+        return np.load(source)
+    return source
+
+
+_cache: dict = {}
+
+
+def load_mc_tables(source=None) -> McTables:
+    """Pack the five tables into the C struct (validated again by the engine)."""
+    src = _table_source(source)
+    key = id(src)
+    hit = _cache.get(key)
+    if hit is not None and hit[0] is src:
+        return hit[1]
+    t = McTables()
+    for (name, n), (field, _) in zip(_TABLE_FIELDS, McTables._fields_):
+        try:
+            arr = src[name] if hasattr(src, "__getitem__") and not hasattr(src, name) else getattr(src, name)
+        except (KeyError, AttributeError) as e:
+            raise ConfigurationError(f"marching-cubes table {name} missing") from e
+        a = np.ascontiguousarray(np.asarray(arr), dtype=np.int32).ravel()
+        if a.size != n:
+            raise ConfigurationError(f"marching-cubes table {name} has {a.size} entries, expected {n}")
+        ctypes.memmove(getattr(t, field), a.ctypes.data, 4 * n)
+    _cache[key] = (src, t)
+    return t
+
+
+class DeviceMesh:
+    """Owning handle of a mesh kept in HBM (dbt_mesh*)."""
+
+    def __init__(self, ptr, nv: int, nf: int):
+        self.ptr, self.n_vertices, self.n_triangles = ptr, nv, nf
+
+    def download(self) -> TriangleMesh:
+        if self.n_triangles == 0:
+            return empty_mesh()
+        v = np.empty((self.n_vertices, 3), np.float64)
+        f = np.empty((self.n_triangles, 3), np.int64)
+        _native.check(_native.lib().dbt_mesh_download(self.ptr, _native.ptr(v), _native.ptr(f)))
+        return TriangleMesh(vertices=v, triangles=f)
+
+    def device_pointers(self):
+        v, f = ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(_native.lib().dbt_mesh_device_buffers(self.ptr, ctypes.byref(v), ctypes.byref(f)))
+        return v.value, f.value
+
+    def close(self):
+        if self.ptr:
+            _native.lib().dbt_mesh_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def extract_mesh_device(grid: VoxelGrid, iso: float = 0.0, tables=None) -> DeviceMesh:
+    """Marching cubes left in device memory (for device-side consumers)."""
+    t = load_mc_tables(tables)
+    grid.push_host()
+    out = ctypes.c_void_p()
+    nv, nf = ctypes.c_int64(), ctypes.c_int64()
+    _native.check(_native.lib().dbt_mesh_extract(grid.handle, float(iso), ctypes.byref(t), ctypes.byref(out),
+                                                 ctypes.byref(nv), ctypes.byref(nf)))
+    return DeviceMesh(out.value, int(nv.value), int(nf.value))
+
+
+def extract_mesh(grid: VoxelGrid, iso: float = 0.0, tables=None) -> TriangleMesh:
+    """Deterministic marching cubes at the given iso level in meters
+    (mesher.py:43-110)."""
+    with extract_mesh_device(grid, iso, tables) as m:
+        return m.download()

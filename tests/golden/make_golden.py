@@ -96,6 +96,36 @@ def main():
         gold["bins"][name] = {"input": cases.sha(dirs), "b_a": cases.sha(b_a.astype(np.int64)),
                               "b_e": cases.sha(b_e.astype(np.int64))}
     gold.setdefault("cases", {})
+    if "--only-mesh" in sys.argv:
+        # the reference's marching-cubes tables (inputs the device mesher takes
+        # from its caller) and its extract_mesh output on final golden grids
+        from bitsdf import _mc_tables as T
+        from bitsdf.mesher import extract_mesh
+        np.savez(HERE / "mc_tables.npz", EDGE_TABLE=T.EDGE_TABLE, TRI_TABLE=T.TRI_TABLE,
+                 CORNER_OFFSETS=T.CORNER_OFFSETS, EDGE_BASE=T.EDGE_BASE, EDGE_AXIS=T.EDGE_AXIS)
+        wanted = ("frame500_default", "arbitrary_state", "nonfresh_cone_h200_t2", "k9_bins8", "cfg2_scans0-2")
+        for c in cases.small_cases() + cases.config_cases(include_slow=False):
+            if c.name not in wanted:
+                continue
+            bank = build_kernel_bank(**c.bank)
+            g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 40)
+            if c.init is not None:
+                g.mask[...], g.sign[...], g.hits[...] = c.init
+            params = IntegrationParams(**c.params)
+            for pts, pose in c.frames:
+                integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), params, threads=8)
+            assert cases.sha(g.mask) == gold["cases"][c.name]["mask"]
+            out = {}
+            for iso in (0.0, 0.1):
+                m = extract_mesh(g, iso)
+                out[repr(iso)] = {"vertices": cases.sha(np.ascontiguousarray(m.vertices, dtype=np.float64)),
+                                  "triangles": cases.sha(np.ascontiguousarray(m.triangles, dtype=np.int64)),
+                                  "n_vertices": int(m.vertices.shape[0]), "n_triangles": int(m.triangles.shape[0])}
+            gold["cases"][c.name]["mesh"] = out
+            print(c.name, out, flush=True)
+        out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))
+        print("wrote", out_path)
+        return
     if "--only-snapshots" in sys.argv:
         # add the snapshot hashes of the small cases; every other stored value
         # must come out unchanged
