@@ -233,6 +233,15 @@ DBT_API int dbt_mesh_info(const dbt_mesh* m, int64_t* n_vertices, int64_t* n_tri
 DBT_API int dbt_mesh_download(const dbt_mesh* m, double* vertices, int64_t* triangles);
 /* device pointers of the same arrays (valid until dbt_mesh_destroy) */
 DBT_API int dbt_mesh_device_buffers(const dbt_mesh* m, const double** vertices, const int64_t** triangles);
+/* a mesh from host arrays (any TriangleMesh), e.g. for dbt_mesh_normals */
+DBT_API int dbt_mesh_from_host(int device, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                       int64_t n_triangles, dbt_mesh** out);
+/* vertex_normals (mesher.py:113-127): area-weighted unit normals, bit-exact
+ * with the reference (corner sums in np.add.at order); zero for vertices
+ * without a non-degenerate incident triangle. Negative indices wrap like
+ * numpy; other out-of-range indices fail with DBT_ERR_CONFIG. */
+DBT_API int dbt_mesh_normals(dbt_mesh* m);
+DBT_API int dbt_mesh_download_normals(const dbt_mesh* m, double* normals);
 DBT_API int dbt_mesh_destroy(dbt_mesh* m);
 
 /* pinned host buffers for callers without a CUDA runtime of their own */

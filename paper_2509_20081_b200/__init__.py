@@ -38,7 +38,7 @@ from .integrator import (
     integrate_points,
 )
 from .kernels import KernelBank, build_kernel_bank
-from .mesher import TriangleMesh, empty_mesh, extract_mesh, extract_mesh_device, load_mc_tables
+from .mesher import TriangleMesh, empty_mesh, extract_mesh, extract_mesh_device, load_mc_tables, vertex_normals
 from .snapshot import SNAPSHOT_MAGIC, load_grid, save_grid
 
 __version__ = "0.1.0"
@@ -68,6 +68,7 @@ __all__ = [
     "extract_mesh",
     "extract_mesh_device",
     "load_mc_tables",
+    "vertex_normals",
     "SNAPSHOT_MAGIC",
     "save_grid",
     "load_grid",

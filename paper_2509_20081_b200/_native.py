@@ -111,6 +111,9 @@ SIGNATURES = {
     "dbt_mesh_download": (ctypes.c_int, [_vp, _vp, _vp]),
     "dbt_mesh_device_buffers": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "dbt_mesh_destroy": (ctypes.c_int, [_vp]),
+    "dbt_mesh_from_host": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "dbt_mesh_normals": (ctypes.c_int, [_vp]),
+    "dbt_mesh_download_normals": (ctypes.c_int, [_vp, _vp]),
     "dbt_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
     "dbt_host_free": (ctypes.c_int, [_vp]),
 }

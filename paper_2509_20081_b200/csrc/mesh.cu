@@ -26,6 +26,7 @@
 //
 // The marching-cubes tables are an input (dbt_mc_tables, filled by the caller
 // from the reference's _mc_tables.py), not data compiled into the engine.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -42,6 +43,7 @@ struct dbt_mesh {
   int64_t nv = 0, nf = 0;
   double* vert = nullptr;    // (nv, 3) float64
   int64_t* tri = nullptr;    // (nf, 3) int64
+  double* nrm = nullptr;     // (nv, 3) float64 once dbt_mesh_normals ran
 };
 
 using namespace dbt;
@@ -256,6 +258,73 @@ __global__ void mesh_tri_kernel(const int64_t* __restrict__ cell, const uint8_t*
   }
 }
 
+// ---- vertex normals (mesher.py:113-127) ----------------------------------
+// face normal = cross(v1 - v0, v2 - v0) with numpy's operation order
+// (a1*b2 - a2*b1, a2*b0 - a0*b2, a0*b1 - a1*b0); one (key = vertex, value =
+// j*nf + f) pair per triangle corner, in the order np.add.at visits them.
+// Negative indices wrap like numpy; anything else out of range sets *bad.
+__global__ void mesh_face_kernel(const double* __restrict__ v, const int64_t* __restrict__ tri, int64_t nv,
+                                 int64_t nf, double* __restrict__ fn, uint32_t* __restrict__ key,
+                                 int64_t* __restrict__ val, uint32_t* __restrict__ deg, int* __restrict__ bad) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t id[3];
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      int64_t k = tri[3 * f + j];
+      if (k < 0) k += nv;
+      ok &= k >= 0 && k < nv;
+      id[j] = k;
+    }
+    if (!ok) {
+      *bad = 1;
+      continue;
+    }
+    double a[3], b[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      a[d] = __dsub_rn(v[3 * id[1] + d], v[3 * id[0] + d]);
+      b[d] = __dsub_rn(v[3 * id[2] + d], v[3 * id[0] + d]);
+    }
+    fn[3 * f + 0] = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+    fn[3 * f + 1] = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+    fn[3 * f + 2] = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      key[j * nf + f] = (uint32_t)id[j];
+      val[j * nf + f] = j * nf + f;
+      atomicAdd(deg + id[j], 1u);
+    }
+  }
+}
+
+// per vertex: sequential sum of its corner normals in np.add.at order, then
+// norm = sqrt((x*x + y*y) + z*z) (np.linalg.norm) and the division
+__global__ void mesh_normal_kernel(const double* __restrict__ fn, const int64_t* __restrict__ val,
+                                   const uint32_t* __restrict__ off, int64_t nv, int64_t nf,
+                                   double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (uint32_t k = off[i]; k < off[i + 1]; ++k) {
+      const int64_t e = val[k], f = e % nf;
+      x = __dadd_rn(x, fn[3 * f]);
+      y = __dadd_rn(y, fn[3 * f + 1]);
+      z = __dadd_rn(z, fn[3 * f + 2]);
+    }
+    const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    if (n > 0.0) {
+      x = __ddiv_rn(x, n);
+      y = __ddiv_rn(y, n);
+      z = __ddiv_rn(z, n);
+    }
+    out[3 * i] = x;
+    out[3 * i + 1] = y;
+    out[3 * i + 2] = z;
+  }
+}
+
 int blocks_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -440,6 +509,82 @@ int dbt_mesh_extract(dbt_grid* g, double iso, const dbt_mc_tables* tables, dbt_m
   return DBT_OK;
 }
 
+int dbt_mesh_from_host(int device, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                       int64_t n_triangles, dbt_mesh** out) {
+  if (!out || n_vertices < 0 || n_triangles < 0 || (n_vertices && !vertices) || (n_triangles && !triangles))
+    return set_error(DBT_ERR_CONFIG, "bad mesh arrays");
+  *out = nullptr;
+  DBT_CUDA(cudaSetDevice(device));
+  dbt_mesh* m = new dbt_mesh();
+  m->device = device;
+  m->nv = n_vertices;
+  m->nf = n_triangles;
+  cudaError_t e = cudaMalloc((void**)&m->vert, (size_t)std::max<int64_t>(1, n_vertices) * 24);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->tri, (size_t)std::max<int64_t>(1, n_triangles) * 24);
+  if (e == cudaSuccess && n_vertices) e = cudaMemcpy(m->vert, vertices, (size_t)n_vertices * 24, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n_triangles)
+    e = cudaMemcpy(m->tri, triangles, (size_t)n_triangles * 24, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    dbt_mesh_destroy(m);
+    return cuda_error(e, "mesh upload");
+  }
+  *out = m;
+  return DBT_OK;
+}
+
+int dbt_mesh_normals(dbt_mesh* m) {
+  if (!m) return set_error(DBT_ERR_CONFIG, "null mesh handle");
+  DBT_CUDA(cudaSetDevice(m->device));
+  if (m->nv >= (int64_t)UINT32_MAX || 3 * m->nf >= (int64_t)UINT32_MAX)
+    return set_error(DBT_ERR_RESOURCE, "mesh too large for vertex normals (2^32 corners)");
+  if (!m->nrm) DBT_CUDA(cudaMalloc((void**)&m->nrm, (size_t)std::max<int64_t>(1, m->nv) * 24));
+  if (m->nv == 0) return DBT_OK;
+  const int64_t nv = m->nv, nf = m->nf, nc = 3 * nf;
+  Scratch s;
+  double* fn;
+  uint32_t *key, *key2, *deg;
+  int64_t *val, *val2;
+  int* bad;
+  int rc;
+  if ((rc = s.alloc(&fn, 3 * nf)) || (rc = s.alloc(&key, nc)) || (rc = s.alloc(&key2, nc)) ||
+      (rc = s.alloc(&val, nc)) || (rc = s.alloc(&val2, nc)) || (rc = s.alloc(&deg, nv + 1)) || (rc = s.alloc(&bad, 1)))
+    return rc;
+  cudaStream_t st = nullptr;
+  DBT_CUDA(cudaMemsetAsync(deg, 0, (size_t)(nv + 1) * 4, st));
+  DBT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  if (nf) {
+    mesh_face_kernel<<<blocks_for(nf), 256, 0, st>>>(m->vert, m->tri, nv, nf, fn, key, val, deg, bad);
+    DBT_CHECK_LAUNCH("mesh_face_kernel");
+  }
+  int end_bit = 1;
+  while (end_bit < 32 && ((int64_t)1 << end_bit) < nv) ++end_bit;
+  size_t t_sort = 0, t_scan = 0;
+  DBT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, key, key2, val, val2, nc, 0, end_bit, st));
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, deg, nv + 1, st));
+  uint8_t* tmp;
+  if ((rc = s.alloc(&tmp, (int64_t)std::max(t_sort, t_scan)))) return rc;
+  if (nc) DBT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t_sort, key, key2, val, val2, nc, 0, end_bit, st));
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t_scan, deg, nv + 1, st));
+  mesh_normal_kernel<<<blocks_for(nv), 256, 0, st>>>(fn, val2, deg, nv, nf, m->nrm);
+  DBT_CHECK_LAUNCH("mesh_normal_kernel");
+  int h_bad = 0;
+  DBT_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) {
+    cudaFree(m->nrm);
+    m->nrm = nullptr;
+    return set_error(DBT_ERR_CONFIG, "triangle index out of range");
+  }
+  return DBT_OK;
+}
+
+int dbt_mesh_download_normals(const dbt_mesh* m, double* normals) {
+  if (!m || !m->nrm) return set_error(DBT_ERR_CONFIG, "mesh normals not computed (dbt_mesh_normals)");
+  DBT_CUDA(cudaSetDevice(m->device));
+  if (m->nv) DBT_CUDA(cudaMemcpy(normals, m->nrm, (size_t)m->nv * 24, cudaMemcpyDeviceToHost));
+  return DBT_OK;
+}
+
 int dbt_mesh_info(const dbt_mesh* m, int64_t* n_vertices, int64_t* n_triangles) {
   if (!m) return set_error(DBT_ERR_CONFIG, "null mesh handle");
   if (n_vertices) *n_vertices = m->nv;
@@ -467,6 +612,7 @@ int dbt_mesh_destroy(dbt_mesh* m) {
   cudaSetDevice(m->device);
   if (m->vert) cudaFree(m->vert);
   if (m->tri) cudaFree(m->tri);
+  if (m->nrm) cudaFree(m->nrm);
   delete m;
   return DBT_OK;
 }

@@ -110,6 +110,13 @@ class DeviceMesh:
         _native.check(_native.lib().dbt_mesh_download(self.ptr, _native.ptr(v), _native.ptr(f)))
         return TriangleMesh(vertices=v, triangles=f)
 
+    def normals(self) -> np.ndarray:
+        """Area-weighted unit vertex normals computed on the device."""
+        _native.check(_native.lib().dbt_mesh_normals(self.ptr))
+        out = np.empty((self.n_vertices, 3), np.float64)
+        _native.check(_native.lib().dbt_mesh_download_normals(self.ptr, _native.ptr(out)))
+        return out
+
     def device_pointers(self):
         v, f = ctypes.c_void_p(), ctypes.c_void_p()
         _native.check(_native.lib().dbt_mesh_device_buffers(self.ptr, ctypes.byref(v), ctypes.byref(f)))
@@ -149,3 +156,21 @@ def extract_mesh(grid: VoxelGrid, iso: float = 0.0, tables=None) -> TriangleMesh
     (mesher.py:43-110)."""
     with extract_mesh_device(grid, iso, tables) as m:
         return m.download()
+
+
+def vertex_normals(mesh: TriangleMesh, device: int | None = None) -> TriangleMesh:
+    """Attach area-weighted unit vertex normals (mesher.py:113-127), computed
+    on the device bit-exactly; vertices with no incident non-degenerate
+    triangle keep a zero normal."""
+    if mesh.is_empty:
+        return TriangleMesh(mesh.vertices, mesh.triangles, np.zeros((0, 3)))
+    v = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+    f = np.ascontiguousarray(mesh.triangles, dtype=np.int64)
+    if v.ndim != 2 or v.shape[1] != 3 or f.ndim != 2 or f.shape[1] != 3:
+        raise ConfigurationError("vertices and triangles must be (n, 3) arrays")
+    dev = _native.default_device() if device is None else int(device)
+    out = ctypes.c_void_p()
+    _native.check(_native.lib().dbt_mesh_from_host(dev, _native.ptr(v), v.shape[0], _native.ptr(f), f.shape[0],
+                                                   ctypes.byref(out)))
+    with DeviceMesh(out.value, v.shape[0], f.shape[0]) as m:
+        return TriangleMesh(mesh.vertices, mesh.triangles, m.normals())

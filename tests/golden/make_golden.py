@@ -100,7 +100,7 @@ def main():
         # the reference's marching-cubes tables (inputs the device mesher takes
         # from its caller) and its extract_mesh output on final golden grids
         from bitsdf import _mc_tables as T
-        from bitsdf.mesher import extract_mesh
+        from bitsdf.mesher import extract_mesh, vertex_normals
         np.savez(HERE / "mc_tables.npz", EDGE_TABLE=T.EDGE_TABLE, TRI_TABLE=T.TRI_TABLE,
                  CORNER_OFFSETS=T.CORNER_OFFSETS, EDGE_BASE=T.EDGE_BASE, EDGE_AXIS=T.EDGE_AXIS)
         wanted = ("frame500_default", "arbitrary_state", "nonfresh_cone_h200_t2", "k9_bins8", "cfg2_scans0-2")
@@ -120,7 +120,8 @@ def main():
                 m = extract_mesh(g, iso)
                 out[repr(iso)] = {"vertices": cases.sha(np.ascontiguousarray(m.vertices, dtype=np.float64)),
                                   "triangles": cases.sha(np.ascontiguousarray(m.triangles, dtype=np.int64)),
-                                  "n_vertices": int(m.vertices.shape[0]), "n_triangles": int(m.triangles.shape[0])}
+                                  "n_vertices": int(m.vertices.shape[0]), "n_triangles": int(m.triangles.shape[0]),
+                                  "normals": cases.sha(vertex_normals(m).normals)}
             gold["cases"][c.name]["mesh"] = out
             print(c.name, out, flush=True)
         out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))

@@ -85,6 +85,7 @@ class TestOracleMesh:
         for iso in (0.0, 0.1):
             v, f = mc_oracle.mesh(g.mask, g.sign, g.hits, c.voxel_size, c.origin, iso, tables())
             assert mesh_hashes(v, f) == gold_tuple(ref["mesh"][repr(iso)])
+            assert cases.sha(mc_oracle.normals(v, f)) == ref["mesh"][repr(iso)]["normals"]
 
     def test_single_voxel_closed_surface(self):
         v, f = mc_oracle.mesh(*one_voxel_state(), 0.1, (0, 0, 0), 0.0, tables())
@@ -240,6 +241,54 @@ class TestDeviceMesh:
         g = VoxelGrid((16, 8, 8), 0.1, (0, 0, 0), slab=(0, 8))
         with pytest.raises(ConfigurationError):
             device_mesh(g)
+
+    @pytest.mark.parametrize("name", ("arbitrary_state", "cfg2_scans0-2"))
+    def test_normals_match_reference(self, name, golden):
+        from test_gpu_parity import engine_run
+
+        from paper_2509_20081_b200.mesher import vertex_normals
+
+        c = next(c for c in cases.small_cases() + cases.config_cases(include_slow=False) if c.name == name)
+        g, _, _ = engine_run(c)
+        for iso in (0.0, 0.1):
+            m = vertex_normals(device_mesh(g, iso))
+            assert cases.sha(m.normals) == golden["cases"][name]["mesh"][repr(iso)]["normals"]
+
+    def test_normals_device_handle(self):
+        from paper_2509_20081_b200.mesher import extract_mesh_device
+
+        st = ball_state()
+        v, f = mc_oracle.mesh(*st, 0.05, (0, 0, 0), 0.0, tables())
+        with extract_mesh_device(device_grid(st, 0.05), 0.0, tables()) as dm:
+            n = dm.normals()
+        want = mc_oracle.normals(v, f)
+        assert np.array_equal(n.view(np.uint64), want.view(np.uint64))
+        radial = v - 0.5
+        radial /= np.linalg.norm(radial, axis=1, keepdims=True)
+        assert np.mean(np.abs(np.sum(n * radial, axis=1))) > 0.9
+
+    def test_normals_hand_meshes(self):
+        from paper_2509_20081_b200.errors import ConfigurationError
+        from paper_2509_20081_b200.mesher import TriangleMesh, vertex_normals
+
+        rng = np.random.default_rng(3)
+        v = rng.normal(size=(40, 3))
+        f = rng.integers(0, 40, size=(120, 3))
+        f[:5] = [[0, 0, 1], [2, 3, 2], [4, 4, 4], [5, 6, 7], [5, 6, 7]]  # degenerate + duplicate faces
+        v[39] = [5, 5, 5]
+        f[f == 39] = 38                                                   # vertex 39 isolated
+        f[7] = [-2, -3, 3]                                                # numpy-style negative indices
+        got = vertex_normals(TriangleMesh(v, f)).normals
+        assert np.array_equal(got.view(np.uint64), mc_oracle.normals(v, f).view(np.uint64))
+        assert np.all(got[39] == 0.0)
+        one = vertex_normals(TriangleMesh(np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]]), np.array([[0, 1, 2]])))
+        assert np.allclose(np.abs(one.normals[:, 2]), 1.0) and np.allclose(one.normals[:, :2], 0.0)
+        e = vertex_normals(TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64)))
+        assert e.normals.shape == (0, 3)
+        lone = vertex_normals(TriangleMesh(np.ones((2, 3)), np.zeros((0, 3), dtype=np.int64)))
+        assert np.array_equal(lone.normals, np.zeros((2, 3)))
+        with pytest.raises(ConfigurationError):
+            vertex_normals(TriangleMesh(v, np.array([[0, 1, 40]])))
 
     def test_bad_tables_rejected(self):
         from paper_2509_20081_b200.errors import ConfigurationError
