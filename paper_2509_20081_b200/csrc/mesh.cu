@@ -63,89 +63,117 @@ struct MeshTab {
   int64_t coff[8];        // storage offset of each cube corner
 };
 
-__global__ void mesh_flags_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ flags, int64_t n,
+// one warp per (x, y) row, 4 z per lane: 32-byte record loads, 4-byte flag stores
+__global__ void mesh_flags_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ flags, int64_t rows,
                                   int64_t nz, int64_t nzp, uint64_t ins_free, uint64_t ins_occ) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint8_t f = 0;
-    if (i - (i / nzp) * nzp < nz) {
-      const uint2 c = cells[i];
-      const int len = __popc(c.x);
-      const uint64_t tab = meta_sign(c.y) == 0 ? ins_occ : ins_free;
-      f = (uint8_t)(((tab >> len) & 1u) | ((!(c.x == kFullMask && meta_hits(c.y) == 0)) << 1));
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    for (int64_t z = 4 * lane; z < nzp; z += 128) {
+      const uint4* q = reinterpret_cast<const uint4*>(cells + r * nzp + z);
+      const uint4 c01 = q[0], c23 = q[1];
+      const uint32_t mx[4] = {c01.x, c01.z, c23.x, c23.z}, my[4] = {c01.y, c01.w, c23.y, c23.w};
+      uint32_t w = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t tab = meta_sign(my[k]) == 0 ? ins_occ : ins_free;
+        const uint32_t f = (uint32_t)((tab >> __popc(mx[k])) & 1u) |
+                           ((uint32_t)(!(mx[k] == kFullMask && meta_hits(my[k]) == 0)) << 1);
+        w |= (z + k < nz ? f : 0u) << (8 * k);
+      }
+      *reinterpret_cast<uint32_t*>(flags + r * nzp + z) = w;
     }
-    flags[i] = f;
   }
 }
 
-struct CellGeom {
+// Active cells (all 8 corners observed, EDGE_TABLE[cube] != 0; mesher.py:
+// 52-65), one warp per cell row (x, y), 4 cells per lane. kEmit = false:
+// per-row counts; kEmit = true: C-order cell list + cube at the row's scanned
+// offset, and bits 2..4 (referenced lattice edges) of the flags of every edge
+// the cell's triangles use (atomicOr; other lanes only read bits 0..1).
+struct RowGeom {
   int64_t nx, ny, nz, nzp;
-  __device__ __forceinline__ bool is_cell(int64_t i) const {
-    const int64_t row = i / nzp, z = i - row * nzp;
-    if (z >= nz - 1) return false;
-    const int64_t x = row / ny, y = row - x * ny;
-    return x < nx - 1 && y < ny - 1;
-  }
+  int64_t roff[8];  // corner row offset (ox*ny + oy)*nzp
+  int oz[8];        // corner z offset
 };
 
-// cube index of cell i, or -1 when a corner is unobserved (mesher.py:55-62)
-__device__ __forceinline__ int cell_cube(const uint8_t* __restrict__ flags, const MeshTab* __restrict__ t,
-                                         int64_t i) {
-  int cube = 0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint8_t f = flags[i + t->coff[c]];
-    if (!(f & 2)) return -1;
-    cube |= (f & 1) << c;
+template <bool kEmit>
+__global__ void __launch_bounds__(256) mesh_active_kernel(uint8_t* __restrict__ flags, const MeshTab* __restrict__ t,
+                                                          RowGeom rg, unsigned long long* __restrict__ rowcnt,
+                                                          int64_t* __restrict__ cell_out,
+                                                          uint8_t* __restrict__ cube_out) {
+  __shared__ uint8_t s_active[256];
+  __shared__ uint16_t s_used[256];
+  __shared__ int64_t s_eoff[12];
+  __shared__ uint32_t s_ebit[12];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    s_active[i] = t->active[i];
+    s_used[i] = t->used[i];
   }
-  return cube;
-}
-
-struct ActiveCell {
-  const uint8_t* flags;
-  const MeshTab* t;
-  CellGeom geo;
-  __device__ __forceinline__ bool operator()(int64_t i) const {
-    if (!geo.is_cell(i)) return false;
-    const int cube = cell_cube(flags, t, i);
-    return cube >= 0 && t->active[cube];
+  if (threadIdx.x < 12) {
+    s_eoff[threadIdx.x] = t->eoff[threadIdx.x];
+    s_ebit[threadIdx.x] = 1u << (2 + t->axis[threadIdx.x]);
   }
-};
-
-__global__ void mesh_count_kernel(const uint8_t* __restrict__ flags, const MeshTab* __restrict__ t, CellGeom geo,
-                                  int64_t n, unsigned long long* __restrict__ out) {
-  ActiveCell pred{flags, t, geo};
-  unsigned long long k = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    k += pred(i);
-  for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-  __shared__ unsigned long long s[32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = k;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s[w];
-    if (tot) atomicAdd(out, tot);
-  }
-}
-
-// cube of every active cell + referenced-edge bits (flags bits 2..4)
-__global__ void mesh_cells_kernel(const int64_t* __restrict__ cell, int64_t n_active, uint8_t* __restrict__ flags,
-                                  const MeshTab* __restrict__ t, uint8_t* __restrict__ cube_out) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_active;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = cell[j];
-    int cube = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (rg.nx - 1) * rg.ny, zc = rg.nz - 1;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const bool edge_row = (r % rg.ny) == rg.ny - 1;  // y = ny-1: no cells
+    const int64_t base = r * rg.nzp;
+    unsigned long long run = kEmit ? rowcnt[r] : 0ull;
+    for (int64_t z0 = 0; z0 < zc && !edge_row; z0 += 128) {
+      const int64_t z = z0 + 4 * lane;
+      uint32_t amask = 0, cubes = 0;
+      if (z < zc) {
+        uint64_t v[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) cube |= (flags[i + t->coff[c]] & 1) << c;
-    cube_out[j] = (uint8_t)cube;
-    for (uint32_t u = t->used[cube]; u; u &= u - 1) {
-      const int e = __ffs(u) - 1;
-      const int64_t p = i + t->eoff[e];
-      atomicOr(reinterpret_cast<unsigned int*>(flags + (p & ~int64_t(3))),
-               (1u << (2 + t->axis[e])) << (8 * (int)(p & 3)));
+        for (int c = 0; c < 8; ++c) {
+          const uint8_t* q = flags + base + rg.roff[c] + z;
+          const uint64_t w = (uint64_t)*reinterpret_cast<const uint32_t*>(q) |
+                             ((uint64_t)*reinterpret_cast<const uint32_t*>(q + 4) << 32);
+          v[c] = w >> (8 * rg.oz[c]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t cube = 0, obs = 1;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t b = (uint32_t)(v[c] >> (8 * k));
+            obs &= b >> 1;
+            cube |= (b & 1u) << c;
+          }
+          if (z + k < zc && obs && s_active[cube]) {
+            amask |= 1u << k;
+            cubes |= cube << (8 * k);
+          }
+        }
+      }
+      const uint32_t cnt = __popc(amask);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (kEmit && amask) {
+        unsigned long long j = run + incl - cnt;
+        for (uint32_t mk = amask; mk; mk &= mk - 1, ++j) {
+          const int k = __ffs(mk) - 1;
+          const int64_t i = base + z + k;
+          const uint32_t cube = (cubes >> (8 * k)) & 0xFFu;
+          cell_out[j] = i;
+          cube_out[j] = (uint8_t)cube;
+          for (uint32_t u = s_used[cube]; u; u &= u - 1) {
+            const int e = __ffs(u) - 1;
+            const int64_t p = i + s_eoff[e];
+            atomicOr(reinterpret_cast<unsigned int*>(flags + (p & ~int64_t(3))), s_ebit[e] << (8 * (int)(p & 3)));
+          }
+        }
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
     }
+    if (!kEmit && lane == 0) rowcnt[r] = run;
   }
 }
 
@@ -330,20 +358,42 @@ int blocks_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
-// device scratch freed on every exit path
+// Mesh buffers come from the device's stream-ordered pool: repeated
+// extractions reuse memory instead of paying cudaMalloc/cudaFree (which
+// synchronise the device) per call. Up to kPoolKeep bytes stay reserved.
+constexpr uint64_t kPoolKeep = 2ull << 30;
+
+int pool_init(int device) {
+  static bool done[256] = {};
+  if (device < 0 || device >= 256 || done[device]) return DBT_OK;
+  cudaMemPool_t pool;
+  DBT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = kPoolKeep;
+  DBT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
+  return DBT_OK;
+}
+
+template <class T>
+int pool_alloc(T** p, int64_t count, cudaStream_t st, const char* what) {
+  *p = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)p, (size_t)std::max<int64_t>(1, count) * sizeof(T), st);
+  return e == cudaSuccess ? DBT_OK : cuda_error(e, what);
+}
+
+// device scratch, released (stream-ordered) on every exit path
 struct Scratch {
+  cudaStream_t st;
   std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
   template <class T>
   int alloc(T** p, int64_t count) {
-    *p = nullptr;
-    if (count <= 0) count = 1;
-    cudaError_t e = cudaMalloc((void**)p, (size_t)count * sizeof(T));
-    if (e != cudaSuccess) return cuda_error(e, "mesh scratch allocation");
-    ptrs.push_back((void*)*p);
-    return DBT_OK;
+    int rc = pool_alloc(p, count, st, "mesh scratch allocation");
+    if (!rc) ptrs.push_back((void*)*p);
+    return rc;
   }
   ~Scratch() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, st);
   }
 };
 
@@ -384,15 +434,27 @@ int check_tables(const dbt_mc_tables* tb, MeshTab* h) {
   return DBT_OK;
 }
 
+#define MESH_LAUNCH(name, grid_, call)          \
+  do {                                          \
+    int _tok;                                   \
+    prof_begin(g, name, st, &_tok);             \
+    call;                                       \
+    prof_end(g, st, _tok);                      \
+    DBT_CHECK_LAUNCH(name);                     \
+  } while (0)
+
 int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& h, dbt_mesh* m) {
   int rc;
   const int64_t nx = g->nx, ny = g->ny, nz = g->nz, nzp = g->nzp;
   if (nx < 2 || ny < 2 || nz < 2) return DBT_OK;  // empty mesh (mesher.py:45-47)
   cudaStream_t st = g->stream;
-  // storage offsets of corners / edge base points
-  for (int c = 0; c < 8; ++c)
-    h.coff[c] = (tables->corner_offsets[3 * c] * ny + tables->corner_offsets[3 * c + 1]) * nzp +
-                tables->corner_offsets[3 * c + 2];
+  RowGeom rg{nx, ny, nz, nzp, {}, {}};
+  for (int c = 0; c < 8; ++c) {
+    const int32_t* o = tables->corner_offsets + 3 * c;
+    rg.roff[c] = (o[0] * ny + o[1]) * nzp;
+    rg.oz[c] = o[2];
+    h.coff[c] = rg.roff[c] + o[2];
+  }
   for (int e = 0; e < 12; ++e)
     h.eoff[e] = (tables->edge_base[3 * e] * ny + tables->edge_base[3 * e + 1]) * nzp + tables->edge_base[3 * e + 2];
   // inside bit per (sign, popcount): field = sigma * (popcount * vs) (mesher.py:50)
@@ -404,25 +466,37 @@ int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& 
     if (fo < iso || fo == iso) ins_occ |= 1ull << k;
   }
 
-  const int64_t n = g->n_cells;                       // padded storage points
+  const int64_t n = g->n_cells;                       // padded storage points (nzp % 8 == 0)
+  const int64_t rows = nx * ny, cell_rows = (nx - 1) * ny;
   const int64_t n_groups = (n + 63) / 64, n_words = n_groups * 8;
-  Scratch s;
+  Scratch s(st);
   MeshTab* d_tab;
   uint8_t* flags;
-  unsigned long long *pre, *d_cnt;
-  if ((rc = s.alloc(&d_tab, 1)) || (rc = s.alloc(&flags, n_groups * 64)) || (rc = s.alloc(&pre, n_groups + 1)) ||
-      (rc = s.alloc(&d_cnt, 8)))
+  unsigned long long *pre, *rowoff;
+  // flags: +64 bytes so the 8-byte corner loads of the last row stay inside
+  if ((rc = s.alloc(&d_tab, 1)) || (rc = s.alloc(&flags, n_groups * 64 + 64)) || (rc = s.alloc(&pre, n_groups + 1)) ||
+      (rc = s.alloc(&rowoff, cell_rows + 1)))
     return rc;
   DBT_CUDA(cudaMemcpyAsync(d_tab, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  DBT_CUDA(cudaMemsetAsync(flags + n, 0, (size_t)(n_groups * 64 - n), st));
-  DBT_CUDA(cudaMemsetAsync(d_cnt, 0, 8, st));
-  mesh_flags_kernel<<<blocks_for(n), 256, 0, st>>>(g->cells, flags, n, nz, nzp, ins_free, ins_occ);
-  DBT_CHECK_LAUNCH("mesh_flags_kernel");
-  const CellGeom geo{nx, ny, nz, nzp};
-  mesh_count_kernel<<<blocks_for(n), 256, 0, st>>>(flags, d_tab, geo, n, d_cnt);
-  DBT_CHECK_LAUNCH("mesh_count_kernel");
+  DBT_CUDA(cudaMemsetAsync(flags + n, 0, (size_t)(n_groups * 64 + 64 - n), st));
+  DBT_CUDA(cudaMemsetAsync(rowoff + cell_rows, 0, 8, st));
+  const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 7) / 8, 148 * 8));
+  const int cblocks = (int)std::max<int64_t>(1, std::min<int64_t>((cell_rows + 7) / 8, 148 * 8));
+  MESH_LAUNCH("mesh_flags_kernel", wblocks,
+              (mesh_flags_kernel<<<wblocks, 256, 0, st>>>(g->cells, flags, rows, nz, nzp, ins_free, ins_occ)));
+  MESH_LAUNCH("mesh_active_count", cblocks,
+              (mesh_active_kernel<false><<<cblocks, 256, 0, st>>>(flags, d_tab, rg, rowoff, nullptr, nullptr)));
+  size_t tmp_rows = 0, tmp_groups = 0;
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_rows, rowoff, cell_rows + 1, st));
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_groups, pre, n_groups + 1, st));
+  void* tmp;
+  if ((rc = s.alloc((uint8_t**)&tmp, (int64_t)std::max(tmp_rows, tmp_groups)))) return rc;
+  int tok;
+  prof_begin(g, "cub_scan_rows", st, &tok);
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_rows, rowoff, cell_rows + 1, st));
+  prof_end(g, st, tok);
   unsigned long long n_active = 0;
-  DBT_CUDA(cudaMemcpyAsync(&n_active, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+  DBT_CUDA(cudaMemcpyAsync(&n_active, rowoff + cell_rows, 8, cudaMemcpyDeviceToHost, st));
   DBT_CUDA(cudaStreamSynchronize(st));
   if (n_active == 0) return DBT_OK;  // empty mesh (mesher.py:66-67)
   const int64_t A = (int64_t)n_active;
@@ -430,31 +504,28 @@ int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& 
   uint8_t* cube;
   unsigned long long* rank;  // 5 x (A + 1)
   if ((rc = s.alloc(&cell, A)) || (rc = s.alloc(&cube, A)) || (rc = s.alloc(&rank, 5 * (A + 1)))) return rc;
+  MESH_LAUNCH("mesh_active_emit", cblocks,
+              (mesh_active_kernel<true><<<cblocks, 256, 0, st>>>(flags, d_tab, rg, rowoff, cell, cube)));
 
-  // C-order compaction of the active cells
-  thrust::counting_iterator<int64_t> idx(0);
-  ActiveCell pred{flags, d_tab, geo};
-  size_t tmp_sel = 0, tmp_scan = 0, tmp_rank = 0;
-  DBT_CUDA(cub::DeviceSelect::If(nullptr, tmp_sel, idx, cell, d_cnt + 1, n, pred, st));
-  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, pre, n_groups + 1, st));
-  auto slot_it = thrust::make_transform_iterator(idx, SlotFlag{cube, d_tab, A, 0});
-  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_rank, slot_it, rank, A + 1, st));
-  void* tmp;
-  if ((rc = s.alloc((uint8_t**)&tmp, (int64_t)std::max({tmp_sel, tmp_scan, tmp_rank})))) return rc;
-  size_t tb = tmp_sel;
-  DBT_CUDA(cub::DeviceSelect::If(tmp, tb, idx, cell, d_cnt + 1, n, pred, st));
-
-  mesh_cells_kernel<<<blocks_for(A), 256, 0, st>>>(cell, A, flags, d_tab, cube);
-  DBT_CHECK_LAUNCH("mesh_cells_kernel");
   const uint64_t* fw = reinterpret_cast<const uint64_t*>(flags);
-  mesh_group_kernel<<<blocks_for(n_groups + 1), 256, 0, st>>>(fw, n_groups, pre);
-  DBT_CHECK_LAUNCH("mesh_group_kernel");
-  tb = tmp_scan;
-  DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, pre, n_groups + 1, st));
+  MESH_LAUNCH("mesh_group_kernel", 0,
+              (mesh_group_kernel<<<blocks_for(n_groups + 1), 256, 0, st>>>(fw, n_groups, pre)));
+  prof_begin(g, "cub_scan_groups", st, &tok);
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_groups, pre, n_groups + 1, st));
+  prof_end(g, st, tok);
+  // per slot: rank of each active cell among those holding the slot
+  thrust::counting_iterator<int64_t> idx(0);
+  size_t tmp_rank = 0;
+  auto it0 = thrust::make_transform_iterator(idx, SlotFlag{cube, d_tab, A, 0});
+  DBT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_rank, it0, rank, A + 1, st));
+  void* tmp2;
+  if ((rc = s.alloc((uint8_t**)&tmp2, (int64_t)tmp_rank))) return rc;
   for (int k = 0; k < 5; ++k) {
-    tb = tmp_rank;
+    size_t tb = tmp_rank;
     auto it = thrust::make_transform_iterator(idx, SlotFlag{cube, d_tab, A, k});
-    DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, it, rank + k * (A + 1), A + 1, st));
+    prof_begin(g, "cub_scan_slots", st, &tok);
+    DBT_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb, it, rank + k * (A + 1), A + 1, st));
+    prof_end(g, st, tok);
   }
   unsigned long long tot[6];
   DBT_CUDA(cudaMemcpyAsync(tot, pre + n_groups, 8, cudaMemcpyDeviceToHost, st));
@@ -466,16 +537,16 @@ int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& 
     base[k] = m->nf;
     m->nf += (int64_t)tot[1 + k];
   }
-  cudaError_t e1 = cudaMalloc((void**)&m->vert, (size_t)std::max<int64_t>(1, m->nv) * 24);
-  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc((void**)&m->tri, (size_t)std::max<int64_t>(1, m->nf) * 24) : e1;
-  if (e2 != cudaSuccess) return cuda_error(e2, "mesh output allocation");
+  if ((rc = pool_alloc(&m->vert, 3 * m->nv, st, "mesh output allocation")) ||
+      (rc = pool_alloc(&m->tri, 3 * m->nf, st, "mesh output allocation")))
+    return rc;
 
   VertArgs va{ny, nzp, n_words, g->vs, iso, {g->org[0], g->org[1], g->org[2]}};
-  mesh_vert_kernel<<<blocks_for(n_words), 256, 0, st>>>(g->cells, fw, pre, va, m->vert);
-  DBT_CHECK_LAUNCH("mesh_vert_kernel");
-  mesh_tri_kernel<<<blocks_for(A), 256, 0, st>>>(cell, cube, A, rank, A + 1, d_tab, fw, pre, base[0], base[1],
-                                                 base[2], base[3], base[4], m->tri);
-  DBT_CHECK_LAUNCH("mesh_tri_kernel");
+  MESH_LAUNCH("mesh_vert_kernel", 0,
+              (mesh_vert_kernel<<<blocks_for(n_words), 256, 0, st>>>(g->cells, fw, pre, va, m->vert)));
+  MESH_LAUNCH("mesh_tri_kernel", 0,
+              (mesh_tri_kernel<<<blocks_for(A), 256, 0, st>>>(cell, cube, A, rank, A + 1, d_tab, fw, pre, base[0],
+                                                              base[1], base[2], base[3], base[4], m->tri)));
   DBT_CUDA(cudaStreamSynchronize(st));
   return DBT_OK;
 }
@@ -494,6 +565,7 @@ int dbt_mesh_extract(dbt_grid* g, double iso, const dbt_mc_tables* tables, dbt_m
   if (g->xm.w != 0 || g->xm.x0 != 0 || g->xm.x1 != g->nx)
     return set_error(DBT_ERR_CONFIG, "mesh extraction needs a whole (unsharded) grid");
   rc = grid_set_device(g);
+  if (!rc) rc = pool_init(g->device);
   if (!rc) rc = fold_pending(g, g->stream);
   if (rc) return rc;
   dbt_mesh* m = new dbt_mesh();
@@ -519,9 +591,15 @@ int dbt_mesh_from_host(int device, const double* vertices, int64_t n_vertices, c
   m->device = device;
   m->nv = n_vertices;
   m->nf = n_triangles;
-  cudaError_t e = cudaMalloc((void**)&m->vert, (size_t)std::max<int64_t>(1, n_vertices) * 24);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&m->tri, (size_t)std::max<int64_t>(1, n_triangles) * 24);
-  if (e == cudaSuccess && n_vertices) e = cudaMemcpy(m->vert, vertices, (size_t)n_vertices * 24, cudaMemcpyHostToDevice);
+  int rc = pool_init(device);
+  if (!rc) rc = pool_alloc(&m->vert, 3 * n_vertices, nullptr, "mesh upload");
+  if (!rc) rc = pool_alloc(&m->tri, 3 * n_triangles, nullptr, "mesh upload");
+  if (rc) {
+    dbt_mesh_destroy(m);
+    return rc;
+  }
+  cudaError_t e = cudaSuccess;
+  if (n_vertices) e = cudaMemcpy(m->vert, vertices, (size_t)n_vertices * 24, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && n_triangles)
     e = cudaMemcpy(m->tri, triangles, (size_t)n_triangles * 24, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -537,19 +615,19 @@ int dbt_mesh_normals(dbt_mesh* m) {
   DBT_CUDA(cudaSetDevice(m->device));
   if (m->nv >= (int64_t)UINT32_MAX || 3 * m->nf >= (int64_t)UINT32_MAX)
     return set_error(DBT_ERR_RESOURCE, "mesh too large for vertex normals (2^32 corners)");
-  if (!m->nrm) DBT_CUDA(cudaMalloc((void**)&m->nrm, (size_t)std::max<int64_t>(1, m->nv) * 24));
+  cudaStream_t st = nullptr;
+  int rc;
+  if (!m->nrm && (rc = pool_alloc(&m->nrm, 3 * m->nv, st, "mesh normals allocation"))) return rc;
   if (m->nv == 0) return DBT_OK;
   const int64_t nv = m->nv, nf = m->nf, nc = 3 * nf;
-  Scratch s;
+  Scratch s(st);
   double* fn;
   uint32_t *key, *key2, *deg;
   int64_t *val, *val2;
   int* bad;
-  int rc;
   if ((rc = s.alloc(&fn, 3 * nf)) || (rc = s.alloc(&key, nc)) || (rc = s.alloc(&key2, nc)) ||
       (rc = s.alloc(&val, nc)) || (rc = s.alloc(&val2, nc)) || (rc = s.alloc(&deg, nv + 1)) || (rc = s.alloc(&bad, 1)))
     return rc;
-  cudaStream_t st = nullptr;
   DBT_CUDA(cudaMemsetAsync(deg, 0, (size_t)(nv + 1) * 4, st));
   DBT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
   if (nf) {
@@ -571,7 +649,7 @@ int dbt_mesh_normals(dbt_mesh* m) {
   DBT_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
   DBT_CUDA(cudaStreamSynchronize(st));
   if (h_bad) {
-    cudaFree(m->nrm);
+    cudaFreeAsync(m->nrm, st);
     m->nrm = nullptr;
     return set_error(DBT_ERR_CONFIG, "triangle index out of range");
   }
@@ -610,9 +688,11 @@ int dbt_mesh_device_buffers(const dbt_mesh* m, const double** vertices, const in
 int dbt_mesh_destroy(dbt_mesh* m) {
   if (!m) return DBT_OK;
   cudaSetDevice(m->device);
-  if (m->vert) cudaFree(m->vert);
-  if (m->tri) cudaFree(m->tri);
-  if (m->nrm) cudaFree(m->nrm);
+  // the legacy stream orders the release after any work on blocking streams;
+  // extract/normals synchronise before returning
+  if (m->vert) cudaFreeAsync(m->vert, nullptr);
+  if (m->tri) cudaFreeAsync(m->tri, nullptr);
+  if (m->nrm) cudaFreeAsync(m->nrm, nullptr);
   delete m;
   return DBT_OK;
 }
