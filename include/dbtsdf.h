@@ -58,6 +58,10 @@ extern "C" {
                                         a kernel concurrent with the sweep (measurement) */
 #define DBT_FLAG_GENERIC_SWEEP 32u   /* distinct-row sweep even for an isotropic kernel
                                         (measurement; identical grid) */
+#define DBT_FLAG_EXACT_WRITTEN 128u  /* voxels_written = the reference's serial count (stamps in
+                                        ascending centre order, integrator.py:268-285) instead
+                                        of the concurrent change count; one scan per launch,
+                                        whole grids, ~ms per scan */
 #define DBT_FLAG_STAGE_COPY 64u      /* stage pinned host scans with an H2D copy instead of
                                         reading them zero-copy in preprocessing (measurement) */
 
@@ -78,7 +82,8 @@ typedef struct dbt_params {
 typedef struct dbt_stats {
   int64_t points_in;        /* after downsampling */
   int64_t points_discarded; /* points_in - #(degenerate or out-of-bounds) */
-  int64_t voxels_written;   /* mask cells changed (concurrent count) */
+  int64_t voxels_written;   /* mask cells changed: concurrent count, or the reference's
+                               serial count with DBT_FLAG_EXACT_WRITTEN */
   int64_t points_applied;   /* stamped returns (after first-return dedup) */
   int64_t unique_centers;   /* centre voxels swept by this launch */
   int64_t centers_skipped;  /* applied returns whose centre needed no sweep: its K^3 stamp

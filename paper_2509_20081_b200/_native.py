@@ -25,6 +25,7 @@ FLAG_NO_SKIP = 8
 FLAG_FUSE_SHADOW = 16
 FLAG_GENERIC_SWEEP = 32
 FLAG_STAGE_COPY = 64
+FLAG_EXACT_WRITTEN = 128
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_dp = ctypes.POINTER(ctypes.c_double)

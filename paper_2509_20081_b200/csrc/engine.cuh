@@ -127,7 +127,8 @@ struct LaunchCounters {
   unsigned long long skipped;    // centres whose stamp was already applied (cache byte 0)
   unsigned long long work;       // sweep work-item cursor (dynamic fetch)
   unsigned long long rows;       // kernel rows the sweep read
-  unsigned long long pad[3];
+  unsigned long long exact_written;  // serial voxels_written (DBT_FLAG_EXACT_WRITTEN)
+  unsigned long long pad[2];
 };
 
 struct ProfEvent {
@@ -166,6 +167,7 @@ struct dbt_grid {
   uint2* cells = nullptr;                   // authoritative voxel records
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
+  uint32_t* d_exact_bits = nullptr;         // centre + touched bitmaps (exact.cu), lazily
   int64_t n_cells = 0;                      // lx*ny*nzp
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -235,6 +237,8 @@ namespace dbt {
 
 // pending shadow visits (grid.cu): make the records final before a read
 int fold_pending(dbt_grid* g, cudaStream_t st);
+// serial voxels_written of a one-scan launch, between prep and sweep (exact.cu)
+int launch_exact_written(dbt_grid* g, const dbt_bank* b, cudaStream_t st);
 
 // error plumbing (abi.cu)
 int set_error(int code, const std::string& msg);

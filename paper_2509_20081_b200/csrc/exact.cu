@@ -1,0 +1,213 @@
+// exact.cu — the reference's serial FrameStats.voxels_written on the device
+// (DBT_FLAG_EXACT_WRITTEN; reference integrator.py:139-160, 268-285).
+//
+// The reference stamps the applied returns one by one in ascending centre
+// order (stable argsort of the C-order centre index, integrator.py:268-274)
+// and counts, per stamp, the K^3 cells whose mask the AND changed. The final
+// grid does not depend on that order, but the count does. It is recovered
+// exactly from three facts:
+//  * a return whose centre was already stamped (same scan or a certified
+//    earlier one, engine.cuh "stamp certificates") changes nothing and leaves
+//    the state unchanged, so only this launch's new centres (the sweep's work
+//    list) matter, each once;
+//  * cell v sees the new centres c with v in box(c), i.e. c in box(v), in
+//    lexicographic (cx, cy, cz) order — rows (cx, cy) ascending, cz ascending;
+//  * a stamp changes v iff (m & k) != m for the running mask m, starting from
+//    v's mask before the launch.
+// One warp per touched cell: lanes take kernel rows, an AND-scan across lanes
+// gives each row its incoming mask, each lane replays its row in z order.
+// Costs ~ms per scan (every cell of every new centre's box is visited), so it
+// is opt-in; the default path reports the concurrent change count.
+#include "engine.cuh"
+
+using namespace dbt;
+
+namespace {
+
+struct ExactArgs {
+  const uint2* cells;
+  const uint64_t* uniq;
+  const LaunchCounters* lc_in;
+  unsigned long long* out;
+  uint32_t* cbits;        // centre bitmap (storage index)
+  uint32_t* tbits;        // touched-cell bitmap (storage index)
+  const uint8_t* len;     // K^3 kernel run lengths
+  int64_t nx, ny, nzp, nz, n_words;
+  int K, R;
+};
+
+__device__ __forceinline__ uint32_t run_mask(int len) { return len >= 32 ? 0xFFFFFFFFu : ((1u << len) - 1u); }
+
+// bits [b, b + w) of a bitmap (w <= 32)
+__device__ __forceinline__ uint32_t bits_at(const uint32_t* __restrict__ bm, int64_t b, int w) {
+  const int64_t q = b >> 5;
+  const int s = (int)(b & 31);
+  const uint64_t v = (uint64_t)__ldcg(bm + q) | ((uint64_t)__ldcg(bm + q + 1) << 32);
+  return (uint32_t)(v >> s) & (w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u));
+}
+
+__device__ __forceinline__ void set_bits(uint32_t* bm, int64_t b, int w) {
+  const int64_t q = b >> 5;
+  const int s = (int)(b & 31);
+  const uint64_t v = (uint64_t)((w >= 32 ? 0xFFFFFFFFull : ((1ull << w) - 1ull))) << s;
+  if ((uint32_t)v) atomicOr(bm + q, (uint32_t)v);
+  if ((uint32_t)(v >> 32)) atomicOr(bm + q + 1, (uint32_t)(v >> 32));
+}
+
+// warp per new centre: its bit in cbits, its K^3 box in tbits
+__global__ void exact_mark_kernel(ExactArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = (int64_t)a.lc_in->n_unique;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
+    int64_t cx, cy, cz;
+    unpack_center(a.uniq[u], cx, cy, cz);
+    const int64_t ci = (cx * a.ny + cy) * a.nzp + cz;
+    if (lane == 0) atomicOr(a.cbits + (ci >> 5), 1u << (ci & 31));
+    for (int r = lane; r < a.K * a.K; r += 32) {
+      const int dx = r / a.K - a.R, dy = r % a.K - a.R;
+      set_bits(a.tbits, ((cx + dx) * a.ny + (cy + dy)) * a.nzp + cz - a.R, a.K);
+    }
+  }
+}
+
+__global__ void exact_clear_kernel(ExactArgs a) {
+  const int64_t n = (int64_t)a.lc_in->n_unique;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t cx, cy, cz;
+    unpack_center(a.uniq[u], cx, cy, cz);
+    const int64_t ci = (cx * a.ny + cy) * a.nzp + cz;
+    a.cbits[ci >> 5] = 0u;  // every centre bit of the word is being cleared
+  }
+}
+
+// serial change count of cell v (whole warp; returns the count on every lane)
+__device__ __forceinline__ unsigned cell_changes(const ExactArgs& a, int64_t v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = v / a.nzp, z = v - row * a.nzp;
+  const int64_t x = row / a.ny, y = row - x * a.ny;
+  uint32_t carry = a.cells[v].x;  // mask before this launch
+  if (carry == 0u) return 0u;     // nothing left to clear
+  const int K = a.K, R = a.R, KK = K * K;
+  const int64_t zlo = z - R < 0 ? 0 : z - R;
+  const int64_t zhi = z + R > a.nz - 1 ? a.nz - 1 : z + R;
+  const int w = (int)(zhi - zlo + 1);
+  unsigned cnt = 0;
+  for (int r0 = 0; r0 < KK; r0 += 32) {
+    const int r = r0 + lane;
+    uint32_t win = 0;
+    int kbase = 0;
+    if (r < KK) {
+      const int ia = r / K, ib = r - ia * K;  // centre row (x - R + ia, y - R + ib)
+      const int64_t cx = x - R + ia, cy = y - R + ib;
+      if (cx >= 0 && cy >= 0 && cx < a.nx && cy < a.ny) {
+        win = bits_at(a.cbits, (cx * a.ny + cy) * a.nzp + zlo, w);
+        // kernel offset v - c = (R - ia, R - ib, z - cz): row index (2R-ia, 2R-ib)
+        kbase = ((2 * R - ia) * K + (2 * R - ib)) * K;
+      }
+    }
+    // pass 1: AND of this row's kernel masks
+    uint32_t prod = 0xFFFFFFFFu;
+    for (uint32_t b = win; b; b &= b - 1) {
+      const int64_t cz = zlo + (__ffs(b) - 1);
+      prod &= run_mask(a.len[kbase + (int)(z - cz + R)]);
+    }
+    // exclusive AND-scan across lanes (row order)
+    uint32_t incl = prod;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl &= t;
+    }
+    uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0xFFFFFFFFu;
+    // pass 2: replay the row from its incoming mask
+    uint32_t m = carry & excl;
+    for (uint32_t b = win; b; b &= b - 1) {
+      const int64_t cz = zlo + (__ffs(b) - 1);
+      const uint32_t k = run_mask(a.len[kbase + (int)(z - cz + R)]);
+      if ((m & k) != m) {
+        ++cnt;
+        m &= k;
+      }
+    }
+    carry &= __shfl_sync(0xffffffffu, incl, 31);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  return cnt;
+}
+
+// warps walk the touched bitmap 32 words at a time (clearing it) and count
+// every set cell; one atomic per block
+__global__ void exact_count_kernel(ExactArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long tot = 0;
+  for (int64_t w0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < a.n_words;
+       w0 += warps * 32) {
+    uint32_t word = 0;
+    if (w0 + lane < a.n_words) {
+      word = a.tbits[w0 + lane];
+      if (word) a.tbits[w0 + lane] = 0u;
+    }
+    for (unsigned todo = __ballot_sync(0xffffffffu, word != 0); todo; todo &= todo - 1) {
+      const int src = __ffs(todo) - 1;
+      for (uint32_t bits = __shfl_sync(0xffffffffu, word, src); bits; bits &= bits - 1) {
+        const int64_t v = (w0 + src) * 32 + (__ffs(bits) - 1);
+        tot += cell_changes(a, v);
+      }
+    }
+  }
+  __shared__ unsigned long long s[32];
+  if (lane == 0) s[threadIdx.x >> 5] = tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    if (t) atomicAdd(a.out, t);
+  }
+}
+
+}  // namespace
+
+namespace dbt {
+
+int launch_exact_written(dbt_grid* g, const dbt_bank* b, cudaStream_t st) {
+  if (g->xm.w != 0 || g->xm.x0 != 0 || g->xm.x1 != g->nx)
+    return set_error(DBT_ERR_CONFIG, "exact voxels_written needs a whole (unsharded) grid");
+  const int64_t n_words = (g->n_cells + 31) / 32 + 2;
+  if (!g->d_exact_bits) {
+    DBT_CUDA(cudaMalloc(&g->d_exact_bits, (size_t)(2 * n_words) * 4));
+    DBT_CUDA(cudaMemsetAsync(g->d_exact_bits, 0, (size_t)(2 * n_words) * 4, st));
+  }
+  ExactArgs a;
+  a.cells = g->cells;
+  a.uniq = g->d_uniq;
+  a.lc_in = g->d_lcnt;
+  a.out = &g->d_lcnt->exact_written;
+  a.cbits = g->d_exact_bits;
+  a.tbits = g->d_exact_bits + n_words;
+  a.len = b->d_len;
+  a.nx = g->nx;
+  a.ny = g->ny;
+  a.nzp = g->nzp;
+  a.nz = g->nz;
+  a.n_words = n_words - 2;
+  a.K = b->K;
+  a.R = b->R;
+  int tok;
+  prof_begin(g, "exact_mark_kernel", st, &tok);
+  exact_mark_kernel<<<148 * 8, 256, 0, st>>>(a);
+  prof_end(g, st, tok);
+  DBT_CHECK_LAUNCH("exact_mark_kernel");
+  prof_begin(g, "exact_count_kernel", st, &tok);
+  exact_count_kernel<<<148 * 8, 256, 0, st>>>(a);
+  prof_end(g, st, tok);
+  DBT_CHECK_LAUNCH("exact_count_kernel");
+  exact_clear_kernel<<<148 * 4, 256, 0, st>>>(a);
+  DBT_CHECK_LAUNCH("exact_clear_kernel");
+  return DBT_OK;
+}
+
+}  // namespace dbt

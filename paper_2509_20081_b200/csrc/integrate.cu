@@ -1184,6 +1184,13 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     joined = true;
   }
 
+  if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
+    // the reference's serial count needs the masks before this launch's stamps
+    if (S != 1 || d_map_sensor) return set_error(DBT_ERR_CONFIG, "exact voxels_written needs one scan per launch");
+    rc = launch_exact_written(g, b, st);
+    if (rc) return rc;
+  }
+
   if (b->iso && !(p->flags & DBT_FLAG_GENERIC_SWEEP)) {
     const size_t smem = (size_t)kCullWarps * b->K * b->K * sizeof(uint64_t);
     if (g->sweep_ch != -b->K) {
@@ -1280,7 +1287,8 @@ void fill_stats(dbt_grid* g, const dbt_params* p, dbt_stats* out, int S) {
     o.points_applied = p->first_return ? (int64_t)g->h_scnt[s].n_applied : nok;
     o.bin_fallbacks = (int64_t)g->h_scnt[s].n_fallback;
     if (s == 0) {
-      o.voxels_written = (int64_t)g->h_lcnt->changed;
+      o.voxels_written = (int64_t)((p->flags & DBT_FLAG_EXACT_WRITTEN) ? g->h_lcnt->exact_written
+                                                                        : g->h_lcnt->changed);
       o.unique_centers = (int64_t)g->h_lcnt->n_unique;
       o.centers_skipped = (int64_t)g->h_lcnt->skipped;
       o.rows_swept = (int64_t)g->h_lcnt->rows;

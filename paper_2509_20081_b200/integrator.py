@@ -20,6 +20,7 @@ Differences that are not semantic:
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -91,6 +92,10 @@ class IntegrationParams:
     compensation: str = "none"
     downsample: int = 1
     first_return_per_voxel: bool = False
+    # FrameStats.voxels_written as the reference's serial count (stamps in
+    # ascending centre order) instead of the concurrent change count; costs
+    # ~ms per scan (exact.cu). Default from $DBT_EXACT_VOXELS_WRITTEN.
+    exact_voxels_written: bool = field(default_factory=lambda: os.environ.get("DBT_EXACT_VOXELS_WRITTEN") == "1")
 
     def __post_init__(self):
         if not 1 <= self.t_occ <= self.h_max <= 255:
@@ -101,6 +106,8 @@ class IntegrationParams:
             raise ConfigurationError("downsample factor must be >= 1")
 
     def native(self, flags: int = 0, downsample: int | None = None):
+        if self.exact_voxels_written:
+            flags |= _native.FLAG_EXACT_WRITTEN
         return _native.make_params(self.h_max, self.t_occ, self.downsample if downsample is None else downsample,
                                    self.first_return_per_voxel, flags)
 
@@ -239,6 +246,9 @@ def integrate_frames(grid: VoxelGrid, bank: KernelBank, scans, params: Integrati
     the one sequential integrate_frame calls produce (order-free updates).
     Compensated scans are deskewed on the host first."""
     scans = list(scans)
+    if params.exact_voxels_written:
+        # the serial count is per scan: one launch each
+        return [integrate_frame(grid, bank, s, params) for s in scans]
     if params.compensation != "none":
         prepped = []
         for s in scans:

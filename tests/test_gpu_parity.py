@@ -712,3 +712,54 @@ class TestGridSemantics:
         n0 = _native.lib().dbt_launch_count()
         integrate_frame(g, bank, ScanFrame(points=np.full((10, 3), 2.05), pose=np.eye(4)), IntegrationParams())
         assert _native.lib().dbt_launch_count() - n0 >= 2  # prep (+ fused shadow), sweep
+
+
+class TestExactVoxelsWritten:
+    """DBT_FLAG_EXACT_WRITTEN: FrameStats.voxels_written equal to the
+    reference's serial count (integrator.py:268-285), every FrameStats field
+    exact, on every golden case with frames."""
+
+    @staticmethod
+    def run(c, **extra):
+        bank = build_kernel_bank(**c.bank)
+        g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 42)
+        if c.init is not None:
+            g.mask[...], g.sign[...], g.hits[...] = c.init
+            g.release_host()
+        params = IntegrationParams(**c.params, exact_voxels_written=True, **extra)
+        frames = [ScanFrame(points=p, pose=pose) for p, pose in c.frames]
+        sts = integrate_frames(g, bank, frames, params)
+        return g, [[s.points_in, s.points_discarded, s.voxels_written] for s in sts]
+
+    @pytest.mark.parametrize("c", [c for c in SMALL + CONFIG if c.frames], ids=lambda c: c.name)
+    def test_stats_match_reference(self, c, golden):
+        g, stats = self.run(c)
+        ref = golden["cases"][c.name]
+        assert stats == ref["stats"]
+        m, s, h = g.download_range(0, c.dims[0])
+        assert cases.sha(m) == ref["mask"] and cases.sha(s) == ref["sign"] and cases.sha(h) == ref["hits"]
+
+    def test_repeated_scan_writes_nothing(self):
+        c = next(c for c in SMALL if c.name == "frame500_default")
+        bank = build_kernel_bank(**c.bank)
+        g = new_grid(c.dims, c.voxel_size, c.origin)
+        prm = IntegrationParams(exact_voxels_written=True)
+        f = ScanFrame(points=c.frames[0][0], pose=c.frames[0][1])
+        first = integrate_frame(g, bank, f, prm)
+        again = integrate_frame(g, bank, f, prm)
+        assert first.voxels_written > 0 and again.voxels_written == 0
+
+    def test_env_default(self, monkeypatch):
+        monkeypatch.setenv("DBT_EXACT_VOXELS_WRITTEN", "1")
+        assert IntegrationParams().exact_voxels_written
+        monkeypatch.delenv("DBT_EXACT_VOXELS_WRITTEN")
+        assert not IntegrationParams().exact_voxels_written
+
+    def test_sharded_grid_rejected(self):
+        from paper_2509_20081_b200.grid import VoxelGrid
+
+        c = next(c for c in SMALL if c.name == "frame500_default")
+        g = VoxelGrid(c.dims, c.voxel_size, c.origin, slab=(0, 20))
+        with pytest.raises(ConfigurationError):
+            integrate_frame(g, build_kernel_bank(**c.bank), ScanFrame(points=c.frames[0][0], pose=c.frames[0][1]),
+                            IntegrationParams(exact_voxels_written=True))
