@@ -14,8 +14,8 @@
 //    lexicographic (cx, cy, cz) order — rows (cx, cy) ascending, cz ascending;
 //  * a stamp changes v iff (m & k) != m for the running mask m, starting from
 //    v's mask before the launch.
-// One warp per touched cell: lanes take kernel rows, an AND-scan across lanes
-// gives each row its incoming mask, each lane replays its row in z order.
+// One lane per touched cell replays the centres of its box in that order
+// from a centre bitmap (exact_count_kernel).
 // Costs ~ms per scan (every cell of every new centre's box is visited), so it
 // is opt-in; the default path reports the concurrent change count.
 #include "engine.cuh"
@@ -42,7 +42,7 @@ __device__ __forceinline__ uint32_t run_mask(int len) { return len >= 32 ? 0xFFF
 __device__ __forceinline__ uint32_t bits_at(const uint32_t* __restrict__ bm, int64_t b, int w) {
   const int64_t q = b >> 5;
   const int s = (int)(b & 31);
-  const uint64_t v = (uint64_t)__ldcg(bm + q) | ((uint64_t)__ldcg(bm + q + 1) << 32);
+  const uint64_t v = (uint64_t)bm[q] | ((uint64_t)bm[q + 1] << 32);
   return (uint32_t)(v >> s) & (w >= 32 ? 0xFFFFFFFFu : ((1u << w) - 1u));
 }
 
@@ -81,66 +81,17 @@ __global__ void exact_clear_kernel(ExactArgs a) {
   }
 }
 
-// serial change count of cell v (whole warp; returns the count on every lane)
-__device__ __forceinline__ unsigned cell_changes(const ExactArgs& a, int64_t v) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = v / a.nzp, z = v - row * a.nzp;
-  const int64_t x = row / a.ny, y = row - x * a.ny;
-  uint32_t carry = a.cells[v].x;  // mask before this launch
-  if (carry == 0u) return 0u;     // nothing left to clear
-  const int K = a.K, R = a.R, KK = K * K;
-  const int64_t zlo = z - R < 0 ? 0 : z - R;
-  const int64_t zhi = z + R > a.nz - 1 ? a.nz - 1 : z + R;
-  const int w = (int)(zhi - zlo + 1);
-  unsigned cnt = 0;
-  for (int r0 = 0; r0 < KK; r0 += 32) {
-    const int r = r0 + lane;
-    uint32_t win = 0;
-    int kbase = 0;
-    if (r < KK) {
-      const int ia = r / K, ib = r - ia * K;  // centre row (x - R + ia, y - R + ib)
-      const int64_t cx = x - R + ia, cy = y - R + ib;
-      if (cx >= 0 && cy >= 0 && cx < a.nx && cy < a.ny) {
-        win = bits_at(a.cbits, (cx * a.ny + cy) * a.nzp + zlo, w);
-        // kernel offset v - c = (R - ia, R - ib, z - cz): row index (2R-ia, 2R-ib)
-        kbase = ((2 * R - ia) * K + (2 * R - ib)) * K;
-      }
-    }
-    // pass 1: AND of this row's kernel masks
-    uint32_t prod = 0xFFFFFFFFu;
-    for (uint32_t b = win; b; b &= b - 1) {
-      const int64_t cz = zlo + (__ffs(b) - 1);
-      prod &= run_mask(a.len[kbase + (int)(z - cz + R)]);
-    }
-    // exclusive AND-scan across lanes (row order)
-    uint32_t incl = prod;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl &= t;
-    }
-    uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) excl = 0xFFFFFFFFu;
-    // pass 2: replay the row from its incoming mask
-    uint32_t m = carry & excl;
-    for (uint32_t b = win; b; b &= b - 1) {
-      const int64_t cz = zlo + (__ffs(b) - 1);
-      const uint32_t k = run_mask(a.len[kbase + (int)(z - cz + R)]);
-      if ((m & k) != m) {
-        ++cnt;
-        m &= k;
-      }
-    }
-    carry &= __shfl_sync(0xffffffffu, incl, 31);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  return cnt;
-}
-
-// warps walk the touched bitmap 32 words at a time (clearing it) and count
-// every set cell; one atomic per block
+// Warps walk the touched bitmap 32 words at a time (clearing it); every
+// non-zero word is then processed with one lane per cell: each lane replays
+// the kernel rows (cx, cy) of its box in lexicographic order and the centres
+// of each row in z order from the centre bitmap, keeping its running mask.
+// Lanes of a word share most row windows (same (x, y), z one apart), so the
+// bitmap loads are L1 broadcasts. Run lengths live in shared memory.
 __global__ void exact_count_kernel(ExactArgs a) {
+  extern __shared__ uint8_t s_len[];
+  const int K = a.K, R = a.R, K3 = K * K * K;
+  for (int i = threadIdx.x; i < K3; i += blockDim.x) s_len[i] = a.len[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   unsigned long long tot = 0;
@@ -153,12 +104,42 @@ __global__ void exact_count_kernel(ExactArgs a) {
     }
     for (unsigned todo = __ballot_sync(0xffffffffu, word != 0); todo; todo &= todo - 1) {
       const int src = __ffs(todo) - 1;
-      for (uint32_t bits = __shfl_sync(0xffffffffu, word, src); bits; bits &= bits - 1) {
-        const int64_t v = (w0 + src) * 32 + (__ffs(bits) - 1);
-        tot += cell_changes(a, v);
+      const uint32_t bits = __shfl_sync(0xffffffffu, word, src);
+      if (!((bits >> lane) & 1u)) continue;
+      const int64_t v = (w0 + src) * 32 + lane;
+      uint32_t m = a.cells[v].x;  // mask before this launch
+      if (m == 0u) continue;      // nothing left to clear
+      const int64_t row = v / a.nzp, z = v - row * a.nzp;
+      const int64_t x = row / a.ny, y = row - x * a.ny;
+      const int64_t zlo = z - R < 0 ? 0 : z - R;
+      const int64_t zhi = z + R > a.nz - 1 ? a.nz - 1 : z + R;
+      const int w = (int)(zhi - zlo + 1);
+      const int zoff = (int)(z - zlo);  // window bit j is centre z = zlo + j: kernel z index R + zoff - j
+      unsigned cnt = 0;
+      for (int ia = 0; ia < K && m; ++ia) {
+        const int64_t cx = x - R + ia;
+        if (cx < 0 || cx >= a.nx) continue;
+        for (int ib = 0; ib < K; ++ib) {
+          const int64_t cy = y - R + ib;
+          if (cy < 0 || cy >= a.ny) continue;
+          uint32_t win = bits_at(a.cbits, (cx * a.ny + cy) * a.nzp + zlo, w);
+          if (!win) continue;
+          // kernel offset v - c = (R - ia, R - ib, z - cz)
+          const uint8_t* lrow = s_len + ((2 * R - ia) * K + (2 * R - ib)) * K + R + zoff;
+          for (; win; win &= win - 1) {
+            const uint32_t k = run_mask(lrow[-(__ffs(win) - 1)]);
+            if ((m & k) != m) {
+              ++cnt;
+              m &= k;
+            }
+          }
+        }
       }
+      tot += cnt;
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   __shared__ unsigned long long s[32];
   if (lane == 0) s[threadIdx.x >> 5] = tot;
   __syncthreads();
@@ -202,7 +183,7 @@ int launch_exact_written(dbt_grid* g, const dbt_bank* b, cudaStream_t st) {
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("exact_mark_kernel");
   prof_begin(g, "exact_count_kernel", st, &tok);
-  exact_count_kernel<<<148 * 8, 256, 0, st>>>(a);
+  exact_count_kernel<<<148 * 8, 256, (size_t)b->K * b->K * b->K, st>>>(a);
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("exact_count_kernel");
   exact_clear_kernel<<<148 * 4, 256, 0, st>>>(a);
