@@ -115,6 +115,9 @@ SIGNATURES = {
     "dbt_mesh_from_host": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.POINTER(_vp)]),
     "dbt_mesh_normals": (ctypes.c_int, [_vp]),
     "dbt_mesh_download_normals": (ctypes.c_int, [_vp, _vp]),
+    "dbt_replica_mark": (ctypes.c_int, [_vp]),
+    "dbt_replica_pack": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "dbt_replica_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
     "dbt_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
     "dbt_host_free": (ctypes.c_int, [_vp]),
 }

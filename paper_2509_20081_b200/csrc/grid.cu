@@ -229,11 +229,13 @@ namespace {
 // after host data replaced the records: rebuild the distance cache, drop
 // every stamp certificate (host writes carry no stamp history)
 int finish_host_write(dbt_grid* g) {
+  g->base_valid = false;  // replica base: host data replaced the records
   rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
+  g->base_valid = false;
   return DBT_OK;
 }
 
@@ -356,7 +358,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   for (auto e : g->event_pool) cudaEventDestroy(e);
   void* dev[] = {g->cells,  g->dist,  g->stamped, g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_scan_off,
-                 g->d_lcnt, g->d_stage, g->d_rowoff, g->d_exact_bits};
+                 g->d_lcnt, g->d_stage, g->d_rowoff, g->d_exact_bits, g->d_base_hits};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {g->h_lcnt, g->h_meta};

@@ -15,6 +15,12 @@ counts are summed with one all-reduce.
 
 The functions below take a ``torch.distributed`` process group and work with
 any backend (NCCL on the GPU box, gloo in the CPU tests).
+
+``ReplicatedGrid`` is the data-parallel alternative for grids that fit one
+GPU (config 2's is 87 MB of masks, even config 4's 51 GB fits 180 GB): each
+rank integrates its own scans into a whole replica with no per-scan
+collective, and an exact merge (three all-reduces) combines the replicas
+when the global map is needed.
 """
 
 from __future__ import annotations
@@ -24,6 +30,7 @@ import ctypes
 import numpy as np
 
 from . import _native
+from .errors import ConfigurationError
 from .grid import VoxelGrid
 from .integrator import FrameStats, IntegrationParams
 from .kernels import KernelBank
@@ -140,3 +147,100 @@ class ShardedGrid:
         out = (_native.Stats * self._last_scans)()
         _native.check(_native.lib().dbt_stats_read(self.local.handle, out, self._last_scans))
         return [FrameStats.from_native(out[i]) for i in range(self._last_scans)]
+
+
+class ReplicatedGrid:
+    """Data-parallel replicas: every rank holds the whole grid (device
+    resident) and integrates its OWN scans — no collective per scan. ``merge``
+    makes all replicas equal to the grid that every rank's scans produce
+    together (exact: see csrc/replica.cu), with three all-reduces over the
+    packed grid (MIN of the mask keys, MIN of the signs, SUM of the hit
+    deltas, 9 B per voxel). Until then each replica holds a valid partial
+    map; reads that need the global map merge first.
+
+    The scans between two merges must share (h_max, t_occ), as the hit-count
+    combine depends on them."""
+
+    def __init__(self, dims, voxel_size, origin, dist, group=None, device: int | None = None):
+        self.dims = tuple(int(d) for d in dims)
+        self.dist, self.group = dist, group
+        self.local = VoxelGrid(self.dims, voxel_size, origin, device=device)
+        self._params = None
+        self._bufs = None
+        self.mark()
+
+    def mark(self):
+        """Start a merge interval from the current records (after creation,
+        reset or any host write)."""
+        self.local.push_host()
+        _native.check(_native.lib().dbt_replica_mark(self.local.handle))
+        self._params = None
+
+    def reset(self):
+        _native.check(_native.lib().dbt_grid_reset(self.local.handle))
+        self.mark()
+
+    def _note_params(self, params: IntegrationParams):
+        key = (params.h_max, params.t_occ)
+        if self._params is None:
+            self._params = key
+        elif self._params != key:
+            raise ConfigurationError("replica scans between two merges must share h_max and t_occ")
+
+    def integrate_device(self, bank: KernelBank, points, counts, poses, params: IntegrationParams, stream=None):
+        """Stamp this rank's scans (device tensor) into its replica,
+        asynchronously on ``stream`` (torch.cuda.Stream or None = current)."""
+        import torch
+
+        self._note_params(params)
+        dtype = _native.DBT_F32 if points.dtype == torch.float32 else _native.DBT_F64
+        counts = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+        poses = np.ascontiguousarray(np.asarray(poses, dtype=np.float64).reshape(-1))
+        st = torch.cuda.current_stream() if stream is None else stream
+        prm = params.native()
+        self._last_scans = len(counts)
+        _native.check(_native.lib().dbt_integrate_device(
+            self.local.handle, bank.device_handle(self.local.device), ctypes.c_void_p(points.data_ptr()), dtype,
+            counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
+            ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm), ctypes.c_void_p(st.cuda_stream)))
+
+    def integrate_frame(self, bank: KernelBank, scan, params: IntegrationParams) -> FrameStats:
+        """integrate_frame on this rank's replica (synchronous; local stats)."""
+        from .integrator import integrate_frame
+
+        self._note_params(params)
+        return integrate_frame(self.local, bank, scan, params)
+
+    def stats(self) -> list:
+        out = (_native.Stats * self._last_scans)()
+        _native.check(_native.lib().dbt_stats_read(self.local.handle, out, self._last_scans))
+        return [FrameStats.from_native(out[i]) for i in range(self._last_scans)]
+
+    def merge(self, stream=None):
+        """All ranks: combine the replicas (collective). Returns when the
+        merged records are enqueued on ``stream`` (current torch stream by
+        default)."""
+        import torch
+
+        n = self.dims[0] * self.dims[1] * self.dims[2]
+        dev = torch.device("cuda", self.local.device)
+        if self._bufs is None:
+            self._bufs = (torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
+                          torch.empty(n, dtype=torch.int32, device=dev))
+        mk, sg, dl = self._bufs
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        L = _native.lib()
+        self.local.push_host()
+        _native.check(L.dbt_replica_pack(self.local.handle, ctypes.c_void_p(mk.data_ptr()),
+                                         ctypes.c_void_p(sg.data_ptr()), ctypes.c_void_p(dl.data_ptr()),
+                                         ctypes.c_void_p(st.cuda_stream)))
+        with torch.cuda.stream(st):
+            self.dist.all_reduce(mk, op=self.dist.ReduceOp.MIN, group=self.group)
+            self.dist.all_reduce(sg, op=self.dist.ReduceOp.MIN, group=self.group)
+            self.dist.all_reduce(dl, op=self.dist.ReduceOp.SUM, group=self.group)
+        h_max, t_occ = self._params if self._params is not None else (255, 2)
+        _native.check(L.dbt_replica_apply(self.local.handle, ctypes.c_void_p(mk.data_ptr()),
+                                          ctypes.c_void_p(sg.data_ptr()), ctypes.c_void_p(dl.data_ptr()),
+                                          int(h_max), int(t_occ), ctypes.c_void_p(st.cuda_stream)))
+        self.local.pull_host()
+        self._params = None

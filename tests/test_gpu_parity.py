@@ -763,3 +763,97 @@ class TestExactVoxelsWritten:
         with pytest.raises(ConfigurationError):
             integrate_frame(g, build_kernel_bank(**c.bank), ScanFrame(points=c.frames[0][0], pose=c.frames[0][1]),
                             IntegrationParams(exact_voxels_written=True))
+
+
+class TestReplicaMerge:
+    """Data-parallel replicas (sharded.ReplicatedGrid): each replica
+    integrates a subset of the scans; dbt_replica_pack -> MIN/MIN/SUM across
+    replicas (torch ops standing in for the NCCL all-reduces) ->
+    dbt_replica_apply must give every replica the reference's final grid."""
+
+    @staticmethod
+    def merge(grids):
+        import ctypes
+
+        import torch
+
+        L = _native.lib()
+        n = int(np.prod(grids[0].dims))
+        packs = []
+        for g in grids:
+            mk = torch.empty(n, dtype=torch.int32, device="cuda")
+            sg = torch.empty(n, dtype=torch.uint8, device="cuda")
+            dl = torch.empty(n, dtype=torch.int32, device="cuda")
+            _native.check(L.dbt_replica_pack(g.handle, ctypes.c_void_p(mk.data_ptr()), ctypes.c_void_p(sg.data_ptr()),
+                                             ctypes.c_void_p(dl.data_ptr()), None))
+            packs.append((mk, sg, dl))
+        torch.cuda.synchronize()
+        mk = torch.stack([p[0] for p in packs]).amin(0).contiguous()
+        sg = torch.stack([p[1] for p in packs]).amin(0).contiguous()
+        dl = torch.stack([p[2] for p in packs]).sum(0, dtype=torch.int32).contiguous()
+        torch.cuda.synchronize()  # apply runs on the grids' own streams
+        return mk, sg, dl
+
+    @staticmethod
+    def apply(grids, red, params):
+        import ctypes
+
+        import torch
+
+        L = _native.lib()
+        mk, sg, dl = red
+        for g in grids:
+            _native.check(L.dbt_replica_apply(g.handle, ctypes.c_void_p(mk.data_ptr()), ctypes.c_void_p(sg.data_ptr()),
+                                              ctypes.c_void_p(dl.data_ptr()), params.h_max, params.t_occ, None))
+            g.synchronize()
+        torch.cuda.synchronize()
+
+    def run(self, c, n_rep, intervals=1):
+        bank = build_kernel_bank(**c.bank)
+        grids = []
+        for _ in range(n_rep):
+            g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 42)
+            if c.init is not None:
+                g.mask[...], g.sign[...], g.hits[...] = c.init
+                g.release_host()
+            _native.check(_native.lib().dbt_replica_mark(g.handle))
+            grids.append(g)
+        params = IntegrationParams(**c.params)
+        frames = [ScanFrame(points=p, pose=pose) for p, pose in c.frames]
+        chunks = np.array_split(np.arange(len(frames)), intervals)
+        for chunk in chunks:
+            for j, k in enumerate(chunk):
+                integrate_frame(grids[j % n_rep], bank, frames[k], params)
+            self.apply(grids, self.merge(grids), params)
+        return grids
+
+    @pytest.mark.parametrize("name,n_rep,intervals", [
+        ("cfg2_scans0-2", 2, 1), ("cfg2_scans0-2", 3, 1), ("yaw_frames_f32", 3, 2), ("yaw_frames_f32", 4, 1),
+        ("nonfresh_hemisphere_h7_t3", 2, 1), ("nonfresh_cone_h200_t2", 3, 1), ("nonfresh_hemisphere_h255_t1", 2, 2),
+        ("arbitrary_state", 2, 1)])
+    def test_merged_replicas_match_reference(self, name, n_rep, intervals, golden):
+        c = next(c for c in SMALL + CONFIG if c.name == name)
+        ref = golden["cases"][name]
+        for g in self.run(c, n_rep, intervals):
+            m, s, h = g.download_range(0, c.dims[0])
+            assert cases.sha(m) == ref["mask"], "mask differs from the reference"
+            assert cases.sha(s) == ref["sign"], "sign differs from the reference"
+            assert cases.sha(h) == ref["hits"], "hits differ from the reference"
+
+    def test_merge_without_work_is_identity(self, golden):
+        c = next(c for c in SMALL if c.name == "arbitrary_state")
+        g = new_grid(c.dims, c.voxel_size, c.origin)
+        g.mask[...], g.sign[...], g.hits[...] = c.init
+        g.release_host()
+        _native.check(_native.lib().dbt_replica_mark(g.handle))
+        self.apply([g], self.merge([g]), IntegrationParams(h_max=250, t_occ=4))
+        m, s, h = g.download_range(0, c.dims[0])
+        assert np.array_equal(m, c.init[0]) and np.array_equal(s, c.init[1]) and np.array_equal(h, c.init[2])
+
+    def test_pack_needs_mark(self):
+        import ctypes
+
+        g = new_grid((16, 16, 16), 0.1)
+        with pytest.raises(ConfigurationError):
+            _native.check(_native.lib().dbt_replica_pack(g.handle, ctypes.c_void_p(0), ctypes.c_void_p(0),
+                                                         ctypes.c_void_p(0), None))

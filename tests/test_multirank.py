@@ -109,3 +109,65 @@ def test_slab_bounds_partition():
             assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
             assert max(x1 - x0 for x0, x1 in b) - min(x1 - x0 for x0, x1 in b) <= 1
             assert owner_of(nx - 1, nx, world) == world - 1
+
+
+def _replica_worker(rank, world, port, case_name, out_path):
+    """Data-parallel replica protocol (sharded.ReplicatedGrid / csrc/replica.cu)
+    over gloo: each rank integrates the scans k with k % world == rank into a
+    whole replica (the oracle stands in for the engine), packs (mask key,
+    sign, hit delta against the shared base), and the three all-reduces plus
+    the combine rule must give the reference's grid."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import cases as C
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = next(x for x in C.small_cases() + C.config_cases(include_slow=False) if x.name == case_name)
+    g = oracle.OracleGrid(c.dims, c.voxel_size, c.origin)
+    if c.init is not None:
+        g.mask[...], g.sign[...], g.hits[...] = c.init
+    base = g.hits.copy()
+    p = dict(h_max=255, t_occ=2)
+    p.update(c.params)
+    ob = oracle.OracleBank.build(**c.bank)
+    for k, (pts, pose) in enumerate(c.frames):
+        if k % world == rank:
+            oracle.integrate_frame(g, ob, pts, pose, h_max=p["h_max"], t_occ=p["t_occ"], threads=2)
+    # pack (replica_pack_kernel) and reduce
+    mk = torch.from_numpy((g.mask.ravel() ^ np.uint32(0x80000000)).view(np.int32).copy())
+    sg = torch.from_numpy(g.sign.ravel().copy())
+    dl = torch.from_numpy(g.hits.ravel().astype(np.int32) - base.ravel().astype(np.int32))
+    dist.all_reduce(mk, op=dist.ReduceOp.MIN)
+    dist.all_reduce(sg, op=dist.ReduceOp.MIN)
+    dist.all_reduce(dl, op=dist.ReduceOp.SUM)
+    # combine (replica_apply_kernel)
+    h0 = base.ravel().astype(np.int32)
+    d = dl.numpy()
+    h = np.where(h0 >= p["h_max"], h0, np.minimum(h0 + d, p["h_max"]))
+    sign = np.where((d > 0) & (h >= p["t_occ"]), 0, sg.numpy())
+    mask = mk.numpy().view(np.uint32) ^ np.uint32(0x80000000)
+    if rank == 0:
+        np.savez(out_path, mask_sha=C.sha(mask.reshape(c.dims)), sign_sha=C.sha(sign.astype(np.uint8).reshape(c.dims)),
+                 hits_sha=C.sha(h.astype(np.uint8).reshape(c.dims)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case_name,world", [("cfg2_scans0-2", 2), ("yaw_frames_f32", 3),
+                                             ("nonfresh_cone_h200_t2", 2), ("arbitrary_state", 2)])
+def test_replica_merge_reproduces_reference(case_name, world, golden, tmp_path):
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "r0.npz"
+    mp.spawn(_replica_worker, args=(world, _free_port(), case_name, str(out)), nprocs=world, join=True)
+    r = np.load(out)
+    ref = golden["cases"][case_name]
+    assert str(r["mask_sha"]) == ref["mask"]
+    assert str(r["sign_sha"]) == ref["sign"]
+    assert str(r["hits_sha"]) == ref["hits"]
