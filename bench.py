@@ -215,7 +215,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(w, batch, interleave=0):
+def config_desc(w, batch, interleave=0, replica=False):
     scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
     return {"workload": f"config {w.config}: {scene}, {w.n_scans}-scan trajectory, {w.beams}x{w.n_az} float32 "
                         f"returns/scan, {w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]}"
@@ -224,7 +224,10 @@ def config_desc(w, batch, interleave=0):
             "scans_per_step": batch,
             "step": f"{batch} scan(s) integrated into the trajectory grid in one launch",
             "l2": "flushed between steps (256 MB write)",
-            "parallelism": (f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks)"
+            "parallelism": ("data-parallel whole-grid replicas: each rank integrates its own scans (consecutive "
+                            "trajectory scans dealt round-robin), one exact merge (MIN/MIN/SUM all-reduces) at the "
+                            "end of the timed region" if replica else
+                            f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks)"
                             if interleave else
                             "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU")}
 
@@ -241,7 +244,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     ap.add_argument("--interleave", type=int, default=None,
-                    help="x-block width of interleaved sharding (default 64 when N > 1, contiguous at N = 1)")
+                    help="slab mode: x-block width of interleaved sharding (default 64)")
+    ap.add_argument("--multi", default="replica", choices=["replica", "slab"],
+                    help="N > 1: data-parallel whole-grid replicas with one exact merge at the end of the "
+                         "timed region (default), or x-sharded slabs with a per-step point broadcast")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -256,14 +262,22 @@ def main():
     from paper_2509_20081_b200 import _native
     from paper_2509_20081_b200 import (IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame,
                                        integrate_frames, new_grid)
-    from paper_2509_20081_b200.sharded import ShardedGrid
+    from paper_2509_20081_b200.sharded import ReplicatedGrid, ShardedGrid
 
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        # functional checks of the N > 1 host logic on a box with fewer GPUs
+        # than ranks (host-staged collectives; not a timing configuration)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workloads.get(args.config)
     B = max(1, args.batch)
     need = (args.warmup + args.steps) * B
@@ -278,26 +292,48 @@ def main():
     dev = f"cuda:{local}"
 
     # ---------------- device-resident value --------------------------------
-    ilv = args.interleave if args.interleave is not None else (64 if world > 1 else 0)
-    sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local, interleave=ilv or None)
+    multi = args.multi if world > 1 else "single"
+    replica = multi == "replica"
+    W = world if replica else 1  # step-batches consumed per step (all ranks)
+    if replica:
+        ilv = 0
+        sg = ReplicatedGrid(w.dims, w.voxel_size, w.origin, dist, device=local)
+    else:
+        ilv = args.interleave if args.interleave is not None else (64 if world > 1 else 0)
+        sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local, interleave=ilv or None)
     # one device buffer per step-batch (concatenated scans), built before timing
     batches = []
     for j in range(steps_per_pass):
         idx = list(range(j * B, (j + 1) * B))
         counts = [len(scans[k]) for k in idx]
         poses = np.stack([w.poses[k] for k in idx])
-        pts = torch.from_numpy(np.concatenate([scans[k] for k in idx])).to(dev) if rank == 0 else None
+        pts = torch.from_numpy(np.concatenate([scans[k] for k in idx])).to(dev) if (rank == 0 or replica) else None
         batches.append((pts, counts, poses))
+
+    def batch_of(s):
+        """Step-batch this rank integrates at step s (replicas: ranks take
+        consecutive batches of the trajectory, round-robin)."""
+        return (s * W + rank) % steps_per_pass
+
+    def new_pass(s):
+        return s == 0 or (s * W) // steps_per_pass != ((s - 1) * W) // steps_per_pass
+
+    def reset_grid():
+        if replica:
+            sg.reset()
+        else:
+            L.dbt_grid_reset(sg.local.handle)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
     torch.cuda.set_stream(stream)
 
-    def do_step(s):
-        pts, counts, poses = batches[s % steps_per_pass]
-        if rank != 0:
-            pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
-        if dist is not None:
-            dist.broadcast(pts, 0)
+    def do_step(s, j=None):
+        pts, counts, poses = batches[batch_of(s) if j is None else j]
+        if not replica:
+            if rank != 0:
+                pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
+            if dist is not None:
+                dist.broadcast(pts, 0)
         sg.integrate_device(bank, pts, counts, poses, params, stream=stream)
 
     # applied returns of every distinct batch (discards do not depend on the
@@ -305,8 +341,8 @@ def main():
     applied_of = []
     for j in range(steps_per_pass):
         if j == 0:
-            L.dbt_grid_reset(sg.local.handle)
-        do_step(j)
+            reset_grid()
+        do_step(0, j)
         applied_of.append(sum(x.points_in - x.points_discarded for x in sg.stats()))
 
     def run_pass(timed):
@@ -314,10 +350,10 @@ def main():
         inside the region (launches queue ahead), else per-step stats and
         per-kernel CUDA events."""
         L.dbt_profile_enable(sg.local.handle, 0 if timed else 1)
-        L.dbt_grid_reset(sg.local.handle)
+        reset_grid()
         for s in range(args.warmup):
-            if s and s % steps_per_pass == 0:
-                L.dbt_grid_reset(sg.local.handle)
+            if s and new_pass(s):
+                reset_grid()
             do_step(s)
         torch.cuda.synchronize()
         L.dbt_profile_reset(sg.local.handle)
@@ -329,33 +365,49 @@ def main():
         launches0 = L.dbt_launch_count()
         for i in range(args.steps):
             s = args.warmup + i
-            if s % steps_per_pass == 0:
-                L.dbt_grid_reset(sg.local.handle)
+            if new_pass(s):
+                reset_grid()
             if not args.no_flush:
                 flush.zero_()
             ev[i][0].record(stream)
             do_step(s)
             ev[i][1].record(stream)
-            cnt["applied"] += applied_of[s % steps_per_pass]
+            cnt["applied"] += applied_of[batch_of(s)]
             if not timed:
                 sts = sg.stats()
                 cnt["swept"] += sts[0].unique_centers
                 cnt["written"] += sts[0].voxels_written
                 cnt["skipped"] += sts[0].centers_skipped
                 cnt["rows"] += sts[0].rows_swept
+        merge_ms = 0.0
+        if replica:
+            # the replicas' partial maps become the global map: one exact
+            # merge (three all-reduces over the packed grid), timed
+            em = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            em[0].record(stream)
+            sg.merge(stream=stream)
+            em[1].record(stream)
+            torch.cuda.synchronize()
+            merge_ms = em[0].elapsed_time(em[1])
         torch.cuda.synchronize()
         launches = L.dbt_launch_count() - launches0
-        dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+        dev_ms = sum(a.elapsed_time(b) for a, b in ev) + merge_ms
+        cnt["merge_ms"] = merge_ms
         return dev_ms, launches, cnt
 
     with ClockSampler(local) as clk:
         dev_ms, launches, cnt = run_pass(timed=True)
+    applied = cnt["applied"]
+    local_applied = applied
     if dist is not None:
         t = torch.tensor([dev_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
+        if replica:  # every rank integrated its own scans
+            a = torch.tensor([applied], dtype=torch.int64, device=dev)
+            dist.all_reduce(a)
+            applied = int(a.item())
         dist.barrier()
-    applied = cnt["applied"]
     value = applied / (dev_ms / 1e3)
 
     # per-kernel device time: a second, identical pass with CUDA events around
@@ -375,8 +427,9 @@ def main():
 
     sweep = kernels.get("sweep_kernel", {"avg_us": float("nan"), "launches": 0})
     peak, peak_src = measured_peaks()
-    applied_per_launch = applied / max(args.steps, 1)
-    alg_bytes = b_alg(shadow_cells) * applied_per_launch / max(world, 1)
+    # per launch of THIS rank: its own scans (replicas) or its slab's share
+    applied_per_launch = local_applied / max(args.steps, 1)
+    alg_bytes = b_alg(shadow_cells) * applied_per_launch / (1 if replica else max(world, 1))
     achieved = alg_bytes / (sweep["avg_us"] * 1e-6) / 1e9
     # bytes the sweep actually touches (device counters): one 32-byte sector of
     # the 1-byte distance cache per kernel row it read after culling (a row's
@@ -402,8 +455,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w, B, ilv),
+        "scaling": "weak" if replica else "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": config_desc(w, B, ilv, replica=replica),
         "gpu_launches": int(launches),
         "kernels": kernels,
         "profiled_step_ms": prof_ms / args.steps,
@@ -411,6 +464,7 @@ def main():
                   "applied returns per scan from an untimed counting pass; kernel times from a second "
                   "identical pass with per-kernel CUDA events",
         "clocks": clk.summary(),
+        **({"merge_ms": cnt["merge_ms"]} if replica else {}),
         "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes,
@@ -439,9 +493,16 @@ def main():
                      "ncu_per_launch": lts},
     }
 
-    # ---------------- e2e through the public API (N=1) ----------------------
-    if world == 1:
-        g = new_grid(w.dims, w.voxel_size, w.origin, memory_cap=1 << 42, device=local)
+    # ---------------- e2e through the public API ----------------------------
+    # N = 1: integrate_frame(s) on pinned host scans; replicas: every rank
+    # the same on its own scans, then the merge (collective), max over ranks
+    if world == 1 or replica:
+        if replica:
+            rg = ReplicatedGrid(w.dims, w.voxel_size, w.origin, dist, device=local)
+            rg._note_params(params)
+            g = rg.local
+        else:
+            g = new_grid(w.dims, w.voxel_size, w.origin, memory_cap=1 << 42, device=local)
         pinned = []
         for s in scans:
             buf = ctypes.c_void_p()
@@ -450,10 +511,15 @@ def main():
             arr[...] = s
             pinned.append((buf, arr))
         e_el, e_pts, h2d = 0.0, 0, 0
+        if dist is not None:
+            dist.barrier()
         for s in range(args.warmup + args.steps):
-            j = s % steps_per_pass
-            if j == 0:
-                L.dbt_grid_reset(g.handle)
+            j = batch_of(s)
+            if new_pass(s):
+                if replica:
+                    rg.reset()
+                else:
+                    L.dbt_grid_reset(g.handle)
             ks = range(j * B, (j + 1) * B)
             if s >= args.warmup:
                 flush.zero_()
@@ -469,11 +535,23 @@ def main():
                 e_el += dt
                 e_pts += sum(x.points_in - x.points_discarded for x in sts)
                 h2d += sum(pinned[k][1].nbytes for k in ks)
+        if replica:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rg.merge()
+            torch.cuda.synchronize()
+            e_el += time.perf_counter() - t0
+            t = torch.tensor([e_el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            a = torch.tensor([e_pts, h2d], dtype=torch.int64, device=dev)
+            dist.all_reduce(a)
+            e_el, e_pts, h2d = float(t.item()), int(a[0].item()), int(a[1].item())
         line["e2e"] = {"value": e_pts / e_el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                        "d2h_bytes_per_step": 32 + 32 * B, "ms_per_step": e_el / args.steps * 1e3,
                        "api": ("paper_2509_20081_b200.integrate_frame (dbt_integrate_frame)" if B == 1 else
                                "paper_2509_20081_b200.integrate_frames (dbt_integrate_batch)")
-                              + ", pinned float32 scans"}
+                              + ", pinned float32 scans"
+                              + (", every rank its own scans, then ReplicatedGrid.merge" if replica else "")}
         for buf, _ in pinned:
             L.dbt_host_free(buf)
     if rank == 0:
