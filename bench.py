@@ -244,7 +244,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     ap.add_argument("--interleave", type=int, default=None,
-                    help="slab mode: x-block width of interleaved sharding (default 64)")
+                    help="slab mode: x-block width of interleaved sharding (default 64, at most nx / 2N)")
     ap.add_argument("--multi", default="replica", choices=["replica", "slab"],
                     help="N > 1: data-parallel whole-grid replicas with one exact merge at the end of the "
                          "timed region (default), or x-sharded slabs with a per-step point broadcast")
@@ -299,7 +299,9 @@ def main():
         ilv = 0
         sg = ReplicatedGrid(w.dims, w.voxel_size, w.origin, dist, device=local)
     else:
-        ilv = args.interleave if args.interleave is not None else (64 if world > 1 else 0)
+        # 64-plane blocks, narrower when the grid has too few for every rank
+        ilv = args.interleave if args.interleave is not None else (
+            min(64, max(1, w.dims[0] // (2 * world))) if world > 1 else 0)
         sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local, interleave=ilv or None)
     # one device buffer per step-batch (concatenated scans), built before timing
     batches = []
@@ -310,13 +312,20 @@ def main():
         pts = torch.from_numpy(np.concatenate([scans[k] for k in idx])).to(dev) if (rank == 0 or replica) else None
         batches.append((pts, counts, poses))
 
+    # Replicas: every pass over the trajectory is split into W contiguous
+    # segments, one per rank (each scan integrated once per pass, and a
+    # rank's consecutive scans overlap like the single-GPU sequence); a pass
+    # ends with the merge (the pass's global map), then a reset.
+    seg = (rank * steps_per_pass // W, (rank + 1) * steps_per_pass // W)
+    P = -(-steps_per_pass // W)  # steps per pass (longest segment)
+
     def batch_of(s):
-        """Step-batch this rank integrates at step s (replicas: ranks take
-        consecutive batches of the trajectory, round-robin)."""
-        return (s * W + rank) % steps_per_pass
+        """Step-batch this rank integrates at step s, or None (short segment)."""
+        i = s % P
+        return seg[0] + i if seg[0] + i < seg[1] else None
 
     def new_pass(s):
-        return s == 0 or (s * W) // steps_per_pass != ((s - 1) * W) // steps_per_pass
+        return s % P == 0
 
     def reset_grid():
         if replica:
@@ -328,7 +337,10 @@ def main():
     torch.cuda.set_stream(stream)
 
     def do_step(s, j=None):
-        pts, counts, poses = batches[batch_of(s) if j is None else j]
+        j = batch_of(s) if j is None else j
+        if j is None:
+            return
+        pts, counts, poses = batches[j]
         if not replica:
             if rank != 0:
                 pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
@@ -353,6 +365,8 @@ def main():
         reset_grid()
         for s in range(args.warmup):
             if s and new_pass(s):
+                if replica:
+                    sg.merge(stream=stream)
                 reset_grid()
             do_step(s)
         torch.cuda.synchronize()
@@ -363,36 +377,44 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = L.dbt_launch_count()
+        merges = []
+
+        def timed_merge():
+            # the replicas' partial maps become the pass's global map: one
+            # exact merge (three all-reduces over the packed grid), timed
+            em = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            em[0].record(stream)
+            sg.merge(stream=stream)
+            em[1].record(stream)
+            merges.append(em)
+
         for i in range(args.steps):
             s = args.warmup + i
             if new_pass(s):
+                if replica and i > 0:
+                    timed_merge()
                 reset_grid()
             if not args.no_flush:
                 flush.zero_()
             ev[i][0].record(stream)
             do_step(s)
             ev[i][1].record(stream)
-            cnt["applied"] += applied_of[batch_of(s)]
+            if batch_of(s) is not None:
+                cnt["applied"] += applied_of[batch_of(s)]
             if not timed:
                 sts = sg.stats()
                 cnt["swept"] += sts[0].unique_centers
                 cnt["written"] += sts[0].voxels_written
                 cnt["skipped"] += sts[0].centers_skipped
                 cnt["rows"] += sts[0].rows_swept
-        merge_ms = 0.0
         if replica:
-            # the replicas' partial maps become the global map: one exact
-            # merge (three all-reduces over the packed grid), timed
-            em = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            em[0].record(stream)
-            sg.merge(stream=stream)
-            em[1].record(stream)
-            torch.cuda.synchronize()
-            merge_ms = em[0].elapsed_time(em[1])
+            timed_merge()  # the last (possibly partial) pass
         torch.cuda.synchronize()
         launches = L.dbt_launch_count() - launches0
+        merge_ms = sum(a.elapsed_time(b) for a, b in merges)
         dev_ms = sum(a.elapsed_time(b) for a, b in ev) + merge_ms
         cnt["merge_ms"] = merge_ms
+        cnt["merges"] = len(merges)
         return dev_ms, launches, cnt
 
     with ClockSampler(local) as clk:
@@ -464,7 +486,7 @@ def main():
                   "applied returns per scan from an untimed counting pass; kernel times from a second "
                   "identical pass with per-kernel CUDA events",
         "clocks": clk.summary(),
-        **({"merge_ms": cnt["merge_ms"]} if replica else {}),
+        **({"merge_ms": cnt["merge_ms"], "merges": cnt["merges"]} if replica else {}),
         "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes,
@@ -514,12 +536,20 @@ def main():
         if dist is not None:
             dist.barrier()
         for s in range(args.warmup + args.steps):
-            j = batch_of(s)
             if new_pass(s):
                 if replica:
+                    if s > args.warmup:  # the pass's global map, timed
+                        torch.cuda.synchronize()
+                        t0 = time.perf_counter()
+                        rg.merge()
+                        torch.cuda.synchronize()
+                        e_el += time.perf_counter() - t0
                     rg.reset()
                 else:
                     L.dbt_grid_reset(g.handle)
+            j = batch_of(s)
+            if j is None:
+                continue
             ks = range(j * B, (j + 1) * B)
             if s >= args.warmup:
                 flush.zero_()

@@ -253,16 +253,17 @@ DBT_API int dbt_mesh_destroy(dbt_mesh* m);
 /* Each rank integrates its own scans into a whole-grid replica; a merge makes
  * every replica equal to the grid all those scans produce together:
  *   mark  : snapshot the base (after create/reset/upload and after a merge)
- *   pack  : n = nx*ny*nz C-order device buffers: mask_key (int32, mask ^
- *           0x80000000), sign (u8), delta (int32, hits - base hits)
- *   (caller: all-reduce MIN mask_key, MIN sign, SUM delta over the replicas)
+ *   pack  : n = nx*ny*nz C-order device buffers: mask_len (u8, bit length of
+ *           the mask), sign (u8), delta_f16 (IEEE half, hits - base hits)
+ *   (caller: all-reduce MIN mask_len, MIN sign, SUM delta_f16 over replicas)
  *   apply : combine the reduced buffers into the records (h_max, t_occ = the
  *           parameters the replicas integrated with) and re-mark.
- * pack/apply are asynchronous on `stream` (NULL: the grid's stream). */
+ * 4 bytes per voxel; pack/apply are asynchronous on `stream` (NULL: the
+ * grid's stream). */
 DBT_API int dbt_replica_mark(dbt_grid* g);
-DBT_API int dbt_replica_pack(dbt_grid* g, int32_t* mask_key, uint8_t* sign, int32_t* delta, void* stream);
-DBT_API int dbt_replica_apply(dbt_grid* g, const int32_t* mask_key_min, const uint8_t* sign_min,
-                      const int32_t* delta_sum, int32_t h_max, int32_t t_occ, void* stream);
+DBT_API int dbt_replica_pack(dbt_grid* g, uint8_t* mask_len, uint8_t* sign, uint16_t* delta_f16, void* stream);
+DBT_API int dbt_replica_apply(dbt_grid* g, const uint8_t* mask_len_min, const uint8_t* sign_min,
+                      const uint16_t* delta_sum_f16, int32_t h_max, int32_t t_occ, void* stream);
 
 /* pinned host buffers for callers without a CUDA runtime of their own */
 DBT_API int dbt_host_alloc(int64_t bytes, void** out);

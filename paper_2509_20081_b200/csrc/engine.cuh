@@ -169,6 +169,7 @@ struct dbt_grid {
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
   uint32_t* d_exact_bits = nullptr;         // centre + touched bitmaps (exact.cu), lazily
   uint8_t* d_base_hits = nullptr;           // replica mode: hits at the last merge (replica.cu)
+  uint32_t* d_base_mask = nullptr;          // replica mode: masks at the last merge
   bool base_valid = false;                  // d_base_hits describes the current records' base
   int64_t n_cells = 0;                      // lx*ny*nzp
   cudaStream_t stream = nullptr;

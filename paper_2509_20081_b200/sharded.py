@@ -154,8 +154,8 @@ class ReplicatedGrid:
     resident) and integrates its OWN scans — no collective per scan. ``merge``
     makes all replicas equal to the grid that every rank's scans produce
     together (exact: see csrc/replica.cu), with three all-reduces over the
-    packed grid (MIN of the mask keys, MIN of the signs, SUM of the hit
-    deltas, 9 B per voxel). Until then each replica holds a valid partial
+    packed grid (MIN of the mask bit lengths, MIN of the signs, float16 SUM
+    of the hit deltas: 4 B per voxel). Until then each replica holds a valid partial
     map; reads that need the global map merge first.
 
     The scans between two merges must share (h_max, t_occ), as the hit-count
@@ -225,8 +225,8 @@ class ReplicatedGrid:
         n = self.dims[0] * self.dims[1] * self.dims[2]
         dev = torch.device("cuda", self.local.device)
         if self._bufs is None:
-            self._bufs = (torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
-                          torch.empty(n, dtype=torch.int32, device=dev))
+            self._bufs = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
+                          torch.empty(n, dtype=torch.float16, device=dev))
         mk, sg, dl = self._bufs
         st = torch.cuda.current_stream(dev) if stream is None else stream
         L = _native.lib()

@@ -781,16 +781,16 @@ class TestReplicaMerge:
         n = int(np.prod(grids[0].dims))
         packs = []
         for g in grids:
-            mk = torch.empty(n, dtype=torch.int32, device="cuda")
+            mk = torch.empty(n, dtype=torch.uint8, device="cuda")
             sg = torch.empty(n, dtype=torch.uint8, device="cuda")
-            dl = torch.empty(n, dtype=torch.int32, device="cuda")
+            dl = torch.empty(n, dtype=torch.float16, device="cuda")
             _native.check(L.dbt_replica_pack(g.handle, ctypes.c_void_p(mk.data_ptr()), ctypes.c_void_p(sg.data_ptr()),
                                              ctypes.c_void_p(dl.data_ptr()), None))
             packs.append((mk, sg, dl))
         torch.cuda.synchronize()
         mk = torch.stack([p[0] for p in packs]).amin(0).contiguous()
         sg = torch.stack([p[1] for p in packs]).amin(0).contiguous()
-        dl = torch.stack([p[2] for p in packs]).sum(0, dtype=torch.int32).contiguous()
+        dl = torch.stack([p[2] for p in packs]).sum(0).contiguous()  # float16, like NCCL
         torch.cuda.synchronize()  # apply runs on the grids' own streams
         return mk, sg, dl
 

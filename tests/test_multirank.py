@@ -133,6 +133,7 @@ def _replica_worker(rank, world, port, case_name, out_path):
     if c.init is not None:
         g.mask[...], g.sign[...], g.hits[...] = c.init
     base = g.hits.copy()
+    base_mask = g.mask.copy()
     p = dict(h_max=255, t_occ=2)
     p.update(c.params)
     ob = oracle.OracleBank.build(**c.bank)
@@ -140,18 +141,21 @@ def _replica_worker(rank, world, port, case_name, out_path):
         if k % world == rank:
             oracle.integrate_frame(g, ob, pts, pose, h_max=p["h_max"], t_occ=p["t_occ"], threads=2)
     # pack (replica_pack_kernel) and reduce
-    mk = torch.from_numpy((g.mask.ravel() ^ np.uint32(0x80000000)).view(np.int32).copy())
+    bits = g.mask.ravel().astype(np.uint64)
+    mlen = np.where(bits == 0, 0, np.floor(np.log2(np.maximum(bits, 1))).astype(np.int64) + 1).astype(np.uint8)
+    mk = torch.from_numpy(mlen)
     sg = torch.from_numpy(g.sign.ravel().copy())
-    dl = torch.from_numpy(g.hits.ravel().astype(np.int32) - base.ravel().astype(np.int32))
+    dl = torch.from_numpy((g.hits.ravel().astype(np.int32) - base.ravel().astype(np.int32)).astype(np.float16))
     dist.all_reduce(mk, op=dist.ReduceOp.MIN)
     dist.all_reduce(sg, op=dist.ReduceOp.MIN)
     dist.all_reduce(dl, op=dist.ReduceOp.SUM)
     # combine (replica_apply_kernel)
     h0 = base.ravel().astype(np.int32)
-    d = dl.numpy()
+    d = np.minimum(dl.numpy().astype(np.float32), 4096).astype(np.int32)
     h = np.where(h0 >= p["h_max"], h0, np.minimum(h0 + d, p["h_max"]))
     sign = np.where((d > 0) & (h >= p["t_occ"]), 0, sg.numpy())
-    mask = mk.numpy().view(np.uint32) ^ np.uint32(0x80000000)
+    keep = mk.numpy().astype(np.uint64)
+    mask = (base_mask.ravel().astype(np.uint64) & ((np.uint64(1) << keep) - np.uint64(1))).astype(np.uint32)
     if rank == 0:
         np.savez(out_path, mask_sha=C.sha(mask.reshape(c.dims)), sign_sha=C.sha(sign.astype(np.uint8).reshape(c.dims)),
                  hits_sha=C.sha(h.astype(np.uint8).reshape(c.dims)))
