@@ -60,7 +60,6 @@ struct MeshTab {
   uint16_t used[256];     // cube edges the present slots reference
   int8_t axis[12];
   int64_t eoff[12];       // storage offset of the edge's lower lattice point
-  int64_t coff[8];        // storage offset of each cube corner
 };
 
 // one warp per (x, y) row, 4 z per lane: 32-byte record loads, 4-byte flag stores
@@ -93,12 +92,13 @@ __global__ void mesh_flags_kernel(const uint2* __restrict__ cells, uint8_t* __re
 // the cell's triangles use (atomicOr; other lanes only read bits 0..1).
 struct RowGeom {
   int64_t nx, ny, nz, nzp;
-  int64_t roff[8];  // corner row offset (ox*ny + oy)*nzp
+  int64_t roff[4];  // the four corner rows (ox*ny + oy)*nzp, (ox, oy) in {0,1}^2
+  int crow[8];      // corner -> its row
   int oz[8];        // corner z offset
 };
 
 template <bool kEmit>
-__global__ void __launch_bounds__(256) mesh_active_kernel(uint8_t* __restrict__ flags, const MeshTab* __restrict__ t,
+__global__ void __launch_bounds__(256, 8) mesh_active_kernel(uint8_t* __restrict__ flags, const MeshTab* __restrict__ t,
                                                           RowGeom rg, unsigned long long* __restrict__ rowcnt,
                                                           int64_t* __restrict__ cell_out,
                                                           uint8_t* __restrict__ cube_out) {
@@ -119,31 +119,38 @@ __global__ void __launch_bounds__(256) mesh_active_kernel(uint8_t* __restrict__ 
   const int64_t rows = (rg.nx - 1) * rg.ny, zc = rg.nz - 1;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
-    const bool edge_row = (r % rg.ny) == rg.ny - 1;  // y = ny-1: no cells
+    // y = ny-1 holds no cells; the emit pass also skips rows the count pass
+    // found empty (scanned offsets equal)
+    const bool edge_row = (r % rg.ny) == rg.ny - 1 || (kEmit && rowcnt[r + 1] == rowcnt[r]);
     const int64_t base = r * rg.nzp;
     unsigned long long run = kEmit ? rowcnt[r] : 0ull;
     for (int64_t z0 = 0; z0 < zc && !edge_row; z0 += 128) {
       const int64_t z = z0 + 4 * lane;
       uint32_t amask = 0, cubes = 0;
       if (z < zc) {
-        uint64_t v[8];
+        // flag bytes z .. z+7 of the four corner rows
+        uint64_t row[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint8_t* q = flags + base + rg.roff[q4] + z;
+          row[q4] = (uint64_t)*reinterpret_cast<const uint32_t*>(q) |
+                    ((uint64_t)*reinterpret_cast<const uint32_t*>(q + 4) << 32);
+        }
+        // SWAR over the 4 cells: byte k of `cubes` collects bit c = inside
+        // flag of corner c of cell z+k, byte k of `obs` = all corners observed
+        uint32_t all = 0u, obs = 0x01010101u;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint8_t* q = flags + base + rg.roff[c] + z;
-          const uint64_t w = (uint64_t)*reinterpret_cast<const uint32_t*>(q) |
-                             ((uint64_t)*reinterpret_cast<const uint32_t*>(q + 4) << 32);
-          v[c] = w >> (8 * rg.oz[c]);
+          const int q = rg.crow[c];  // selects, not a dynamically indexed (local-memory) array
+          const uint64_t rw = q == 0 ? row[0] : q == 1 ? row[1] : q == 2 ? row[2] : row[3];
+          const uint32_t vc = (uint32_t)(rw >> (8 * rg.oz[c]));
+          all |= (vc & 0x01010101u) << c;
+          obs &= vc >> 1;
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          uint32_t cube = 0, obs = 1;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t b = (uint32_t)(v[c] >> (8 * k));
-            obs &= b >> 1;
-            cube |= (b & 1u) << c;
-          }
-          if (z + k < zc && obs && s_active[cube]) {
+          const uint32_t cube = (all >> (8 * k)) & 0xFFu;
+          if (z + k < zc && ((obs >> (8 * k)) & 1u) && s_active[cube]) {
             amask |= 1u << k;
             cubes |= cube << (8 * k);
           }
@@ -224,9 +231,12 @@ __global__ void mesh_vert_kernel(const uint2* __restrict__ cells, const uint64_t
                                  double* __restrict__ vert) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.n_words;
        w += (int64_t)gridDim.x * blockDim.x) {
+    // groups of 64 points without a referenced edge are skipped on their
+    // scanned counts (8 bytes per 8 words of flags)
+    int64_t r = (int64_t)pre[w >> 3];
+    if ((int64_t)pre[(w >> 3) + 1] == r) continue;
     uint64_t bits = fw[w] & kEdgeBits;
     if (!bits) continue;
-    int64_t r = (int64_t)pre[w >> 3];
     for (int64_t k = w & ~int64_t(7); k < w; ++k) r += __popcll(fw[k] & kEdgeBits);
     for (; bits; bits &= bits - 1, ++r) {
       const int pos = __ffsll((long long)bits) - 1;
@@ -448,12 +458,12 @@ int extract_into(dbt_grid* g, double iso, const dbt_mc_tables* tables, MeshTab& 
   const int64_t nx = g->nx, ny = g->ny, nz = g->nz, nzp = g->nzp;
   if (nx < 2 || ny < 2 || nz < 2) return DBT_OK;  // empty mesh (mesher.py:45-47)
   cudaStream_t st = g->stream;
-  RowGeom rg{nx, ny, nz, nzp, {}, {}};
+  RowGeom rg{nx, ny, nz, nzp, {}, {}, {}};
+  for (int q4 = 0; q4 < 4; ++q4) rg.roff[q4] = ((q4 >> 1) * ny + (q4 & 1)) * nzp;
   for (int c = 0; c < 8; ++c) {
     const int32_t* o = tables->corner_offsets + 3 * c;
-    rg.roff[c] = (o[0] * ny + o[1]) * nzp;
+    rg.crow[c] = o[0] * 2 + o[1];
     rg.oz[c] = o[2];
-    h.coff[c] = rg.roff[c] + o[2];
   }
   for (int e = 0; e < 12; ++e)
     h.eoff[e] = (tables->edge_base[3 * e] * ny + tables->edge_base[3 * e + 1]) * nzp + tables->edge_base[3 * e + 2];
