@@ -167,7 +167,8 @@ struct dbt_grid {
   uint2* cells = nullptr;                   // authoritative voxel records
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
-  uint32_t* d_exact_bits = nullptr;         // centre + touched bitmaps (exact.cu), lazily
+  uint32_t* d_exact_bits = nullptr;         // centre + touched + centre-row bitmaps (exact.cu), lazily
+  uint32_t* d_exact_m0 = nullptr;           // pre-launch masks of touched cells (exact.cu)
   uint8_t* d_base_hits = nullptr;           // replica mode: hits at the last merge (replica.cu)
   uint32_t* d_base_mask = nullptr;          // replica mode: masks at the last merge
   bool base_valid = false;                  // d_base_hits describes the current records' base
@@ -240,8 +241,10 @@ namespace dbt {
 
 // pending shadow visits (grid.cu): make the records final before a read
 int fold_pending(dbt_grid* g, cudaStream_t st);
-// serial voxels_written of a one-scan launch, between prep and sweep (exact.cu)
-int launch_exact_written(dbt_grid* g, const dbt_bank* b, cudaStream_t st);
+// serial voxels_written of a one-scan launch (exact.cu): pre before the
+// sweep, post after it
+int launch_exact_pre(dbt_grid* g, const dbt_bank* b, cudaStream_t st);
+int launch_exact_post(dbt_grid* g, const dbt_bank* b, cudaStream_t st);
 
 // error plumbing (abi.cu)
 int set_error(int code, const std::string& msg);

@@ -1186,8 +1186,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
 
   if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
     // the reference's serial count needs the masks before this launch's stamps
+    // (saved here for the touched cells; counted after the sweep)
     if (S != 1 || d_map_sensor) return set_error(DBT_ERR_CONFIG, "exact voxels_written needs one scan per launch");
-    rc = launch_exact_written(g, b, st);
+    rc = launch_exact_pre(g, b, st);
     if (rc) return rc;
   }
 
@@ -1224,6 +1225,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sweep_cull_kernel<<<blocks, kCullWarps * 32, smem, st>>>(wa);
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");
+    if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
+      rc = launch_exact_post(g, b, st);
+      if (rc) return rc;
+    }
     if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
     g->last_st = st;
     return DBT_OK;
@@ -1266,6 +1271,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   fn<<<blocks, 256, smem, st>>>(wa);
   prof_end(g, st, tok);
   DBT_CHECK_LAUNCH("sweep_kernel");
+  if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
+    rc = launch_exact_post(g, b, st);
+    if (rc) return rc;
+  }
   if (joined) DBT_CUDA(cudaStreamWaitEvent(st, g->ev_join, 0));
   g->last_st = st;
   return DBT_OK;
