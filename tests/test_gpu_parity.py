@@ -163,13 +163,14 @@ def test_slab_grids_reassemble_reference():
     assert np.array_equal(full[2], ref.hits)
 
 
+@pytest.fixture(scope="module")
+def bank():
+    return build_kernel_bank(shadow_radius=3)
+
+
 class TestReferenceBehaviours:
     """The reference's own integrator tests (test_integrator.py) re-expressed
     against the drop-in API."""
-
-    @pytest.fixture(scope="class")
-    def bank(self):
-        return build_kernel_bank(shadow_radius=3)
 
     def fresh(self, n=41):
         return new_grid((n, n, n), 0.1)
