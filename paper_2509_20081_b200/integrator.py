@@ -128,10 +128,16 @@ class FrameStats:
 
     @classmethod
     def from_native(cls, s: _native.Stats, elapsed_ms: float | None = None) -> "FrameStats":
-        return cls(int(s.points_in), int(s.points_discarded), int(s.voxels_written),
-                   float(s.elapsed_ms if elapsed_ms is None else elapsed_ms), int(s.points_applied),
-                   int(s.unique_centers), int(s.centers_skipped), int(s.bin_fallbacks), float(s.device_ms),
-                   int(s.rows_swept))
+        # ctypes int64 / double fields already read as Python int / float;
+        # filling __dict__ directly skips the dataclass __init__ (per-call cost)
+        o = object.__new__(cls)
+        o.__dict__.update(points_in=s.points_in, points_discarded=s.points_discarded,
+                          voxels_written=s.voxels_written,
+                          elapsed_ms=s.elapsed_ms if elapsed_ms is None else float(elapsed_ms),
+                          points_applied=s.points_applied, unique_centers=s.unique_centers,
+                          centers_skipped=s.centers_skipped, bin_fallbacks=s.bin_fallbacks,
+                          device_ms=s.device_ms, rows_swept=s.rows_swept)
+        return o
 
 
 def _scan_times(scan: ScanFrame) -> np.ndarray:
@@ -168,8 +174,8 @@ def motion_compensate(scan: ScanFrame, mode: str) -> ScanFrame:
 
 
 def _pose_arg(pose: np.ndarray):
-    p = np.ascontiguousarray(pose, dtype=np.float64).reshape(16)
-    return p, ctypes.c_void_p(p.ctypes.data)
+    p = pose if (pose.dtype == np.float64 and pose.flags.c_contiguous) else np.ascontiguousarray(pose, np.float64)
+    return p, _native.ptr(p)
 
 
 def integrate_point(grid: VoxelGrid, bank: KernelBank, p_map, sensor_pos, params: IntegrationParams) -> str:
