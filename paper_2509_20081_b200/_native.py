@@ -173,9 +173,13 @@ def default_device() -> int:
 _params_cache: dict = {}
 
 
+# measurement-only engine flags OR-ed into every launch (A/B runs, e.g. DBT_EXTRA_FLAGS=16)
+_EXTRA_FLAGS = int(os.environ.get("DBT_EXTRA_FLAGS", "0"), 0)
+
+
 def make_params(h_max=255, t_occ=2, downsample=1, first_return=False, flags=0) -> Params:
     """dbt_params for these values (cached: the struct is read-only for the engine)."""
-    key = (int(h_max), int(t_occ), int(downsample), int(bool(first_return)), int(flags))
+    key = (int(h_max), int(t_occ), int(downsample), int(bool(first_return)), int(flags) | _EXTRA_FLAGS)
     p = _params_cache.get(key)
     if p is None:
         p = _params_cache[key] = Params(*key, 0)
