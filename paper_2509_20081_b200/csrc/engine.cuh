@@ -218,7 +218,9 @@ struct dbt_grid {
   std::vector<std::string> prof_names;
   std::vector<double> prof_ms;
   std::vector<int64_t> prof_launches;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // device_ms of the last call
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // device_ms of the last call (timed calls)
+  cudaEvent_t ev_done = nullptr;               // completion of a synchronous call (no timing)
+  bool time_calls = false;                     // $DBT_DEVICE_MS: device_ms on every synchronous call
   cudaEvent_t ev_meta = nullptr;               // pinned metadata consumed by the stream
   cudaStream_t aux = nullptr;                  // shadow kernel, concurrent with the sweep
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

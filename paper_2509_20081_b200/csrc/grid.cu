@@ -1,5 +1,6 @@
 // grid.cu — device voxel store: allocation, host sync, DBTSDF01 records and
 // the distance readout kernels (reference: grid.py:39-202).
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 
@@ -288,6 +289,8 @@ static int create_grid(const int64_t dims[3], double voxel_size, const double or
   cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
   cudaEventCreate(&g->ev_a);
   cudaEventCreate(&g->ev_b);
+  cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming);
+  g->time_calls = getenv("DBT_DEVICE_MS") != nullptr;
   cudaEventCreateWithFlags(&g->ev_meta, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming);
@@ -366,6 +369,7 @@ int dbt_grid_destroy(dbt_grid* g) {
     if (p) cudaFreeHost(p);
   if (g->ev_a) cudaEventDestroy(g->ev_a);
   if (g->ev_b) cudaEventDestroy(g->ev_b);
+  if (g->ev_done) cudaEventDestroy(g->ev_done);
   if (g->ev_meta) cudaEventDestroy(g->ev_meta);
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);
   if (g->ev_join) cudaEventDestroy(g->ev_join);

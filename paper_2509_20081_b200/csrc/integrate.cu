@@ -1323,6 +1323,26 @@ cudaError_t wait_event(cudaEvent_t ev) {
   return e;
 }
 
+// Synchronous calls: device_ms (two timing events + cudaEventElapsedTime,
+// ~4 us of host time) only when profiling or $DBT_DEVICE_MS asks for it;
+// otherwise one timing-free completion event.
+void call_begin(dbt_grid* g, cudaStream_t st, bool timed) {
+  if (timed) cudaEventRecord(g->ev_a, st);
+}
+
+int call_end(dbt_grid* g, cudaStream_t st, bool timed, double* device_ms) {
+  cudaEvent_t e = timed ? g->ev_b : g->ev_done;
+  DBT_CUDA(cudaEventRecord(e, st));
+  DBT_CUDA(wait_event(e));
+  *device_ms = 0.0;
+  if (timed) {
+    float dms = 0.f;
+    cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
+    *device_ms = dms;
+  }
+  return DBT_OK;
+}
+
 double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -1356,7 +1376,8 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
     else
       cudaGetLastError();  // pageable pointers report an error on some drivers
   }
-  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  const bool timed = g->time_calls || g->profiling;
+  call_begin(g, st, timed);
   if (!d_src) {
     rc = stage_raw(g, total * (int64_t)esz);
     if (rc) return rc;
@@ -1367,11 +1388,10 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
   if (rc) return rc;
   rc = fetch_counters(g, st);
   if (rc) return rc;
-  DBT_CUDA(cudaEventRecord(g->ev_b, st));
-  DBT_CUDA(wait_event(g->ev_b));
+  double dms = 0.0;
+  rc = call_end(g, st, timed, &dms);
+  if (rc) return rc;
   fill_stats(g, p, out, S);
-  float dms = 0.f;
-  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
   out[0].device_ms = dms;
   out[0].elapsed_ms = now_ms() - t0;
   return DBT_OK;
@@ -1412,7 +1432,8 @@ int integrate_scans_host(dbt_grid* g, const dbt_bank* b, const void* const* poin
   }
   for (int s = 0; s < S; ++s)
     if (!dptr[s]) staged += counts[s];
-  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  const bool timed = g->time_calls || g->profiling;
+  call_begin(g, st, timed);
   if (staged) {
     rc = stage_raw(g, staged * (int64_t)esz);
     if (rc) return rc;
@@ -1432,11 +1453,10 @@ int integrate_scans_host(dbt_grid* g, const dbt_bank* b, const void* const* poin
   if (rc) return rc;
   rc = fetch_counters(g, st);
   if (rc) return rc;
-  DBT_CUDA(cudaEventRecord(g->ev_b, st));
-  DBT_CUDA(wait_event(g->ev_b));
+  double dms = 0.0;
+  rc = call_end(g, st, timed, &dms);
+  if (rc) return rc;
   fill_stats(g, p, out, S);
-  float dms = 0.f;
-  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
   out[0].device_ms = dms;
   out[0].elapsed_ms = now_ms() - t0;
   return DBT_OK;
@@ -1479,7 +1499,8 @@ int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map
   if (!rc && outcome) rc = grow((void**)&g->d_outcome, &g->cap_outcome, n, 1);
   if (rc) return rc;
   cudaStream_t st = g->stream;
-  DBT_CUDA(cudaEventRecord(g->ev_a, st));
+  const bool timed = g->time_calls || g->profiling;
+  call_begin(g, st, timed);
   DBT_CUDA(cudaMemcpyAsync(g->d_raw, p_map, n * 24, cudaMemcpyHostToDevice, st));
   DBT_CUDA(cudaMemcpyAsync(g->d_sensor, sensor, n * 24, cudaMemcpyHostToDevice, st));
   rc = launch_integrate(g, b, g->d_raw, DBT_F64, &n, 1, nullptr, &q, g->d_sensor,
@@ -1488,11 +1509,10 @@ int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map
   rc = fetch_counters(g, st);
   if (rc) return rc;
   if (outcome) DBT_CUDA(cudaMemcpyAsync(outcome, g->d_outcome, n, cudaMemcpyDeviceToHost, st));
-  DBT_CUDA(cudaEventRecord(g->ev_b, st));
-  DBT_CUDA(wait_event(g->ev_b));
+  double dms = 0.0;
+  rc = call_end(g, st, timed, &dms);
+  if (rc) return rc;
   fill_stats(g, &q, out, 1);
-  float dms = 0.f;
-  cudaEventElapsedTime(&dms, g->ev_a, g->ev_b);
   out->device_ms = dms;
   out->elapsed_ms = now_ms() - t0;
   return DBT_OK;

@@ -1,5 +1,7 @@
 """Batched e2e (config-5 shape): 32 pinned scans per dbt_integrate_scans call,
 zero-copy reads in preprocessing vs one DMA copy per scan (FLAG_STAGE_COPY)."""
+import os
+os.environ.setdefault("DBT_DEVICE_MS", "1")  # FrameStats.device_ms on every call (timing events)
 import ctypes
 import sys
 import time

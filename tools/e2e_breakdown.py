@@ -2,6 +2,8 @@
 scans, L2 flushed between steps like bench.py): Python ScanFrame
 construction, the C call (host wall, elapsed_ms) and the device span from
 the H2D copy to the counter read-back (device_ms)."""
+import os
+os.environ.setdefault("DBT_DEVICE_MS", "1")  # FrameStats.device_ms on every call (timing events)
 import ctypes
 import sys
 import time

@@ -1,3 +1,5 @@
+import os
+os.environ.setdefault("DBT_DEVICE_MS", "1")  # FrameStats.device_ms on every call (timing events)
 import ctypes, sys, time
 import numpy as np, torch
 sys.path.insert(0, ".")

@@ -1,5 +1,7 @@
 """Cost of DBT_FLAG_EXACT_WRITTEN (the reference's serial voxels_written) on a
 config's trajectory: device ms per scan with and without it, per kernel."""
+import os
+os.environ.setdefault("DBT_DEVICE_MS", "1")  # FrameStats.device_ms on every call (timing events)
 import ctypes, json, sys
 import numpy as np
 sys.path.insert(0, ".")
