@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import CODE_TO_ERROR, BitsdfError
 
-LIB_PATH = Path(__file__).resolve().parent / "libdbtsdf.so"
+# $DBT_LIB: another build of the engine (same-box A/B measurements only)
+LIB_PATH = Path(os.environ.get("DBT_LIB") or Path(__file__).resolve().parent / "libdbtsdf.so")
 
 DBT_F32 = 0
 DBT_F64 = 1

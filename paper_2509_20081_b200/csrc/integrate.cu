@@ -170,6 +170,11 @@ __device__ __forceinline__ bool floor_index(double v, double o, double vs, long 
 constexpr int kPrepThreads = 256;
 
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
+  // the sweep (programmatic dependent launch) may be scheduled once every
+  // prep block has started; it waits for this grid's completion before
+  // reading anything (griddepcontrol.wait), so only its launch latency
+  // overlaps preprocessing
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool live = i < a.n;
@@ -567,6 +572,8 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
 }
 
 __global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a) {
+  // launched programmatically behind prep_kernel: wait for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw);  // kCullWarps * K * K
   __shared__ int q_n;
@@ -1037,7 +1044,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, bytes, cudaMemcpyHostToDevice, st));
     DBT_CUDA(cudaEventRecord(g->ev_meta, st));
   }
-  // launch + per-scan counters: one contiguous block, one memset
+  // launch + per-scan counters: one contiguous block, one memset (zeroing
+  // them behind the previous launch's read-back instead measured 2 us per
+  // step slower device-resident)
   DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
   if (n == 0) return DBT_OK;
   // pending shadow visits were counted under other (h_max, T): fold them first
@@ -1222,7 +1231,24 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     // persistent blocks fetching kCullWarps centres at a time
     unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 2 * kCullWarps - 1) / (2 * kCullWarps)));
     prof_begin(g, "sweep_kernel", st, &tok);
-    sweep_cull_kernel<<<blocks, kCullWarps * 32, smem, st>>>(wa);
+    if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
+      // exact_pre sits between prep and the sweep: plain stream order
+      sweep_cull_kernel<<<blocks, kCullWarps * 32, smem, st>>>(wa);
+    } else {
+      // programmatic dependent launch: the sweep's launch latency overlaps
+      // the tail of preprocessing (the kernel waits for prep's completion)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(blocks);
+      cfg.blockDim = dim3(kCullWarps * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      DBT_CUDA(cudaLaunchKernelEx(&cfg, sweep_cull_kernel, wa));
+    }
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");
     if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
