@@ -571,7 +571,13 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
   return (uint64_t)(rbase >> 3) | ((uint64_t)c0 << 37) | ((uint64_t)c1 << 39) | ((uint64_t)drow << 41);
 }
 
-__global__ void __launch_bounds__(kCullWarps * 32) sweep_cull_kernel(CullArgs a) {
+// 8 resident blocks per SM (64 registers, 24 B spilled): same-box A/B vs 7
+// (72 registers): config 2 +2.7 %, config 1 +5 %, config 3 neutral; 9 or 10
+// blocks (56 / 48 registers) spill more and are slower
+#ifndef DBT_CULL_MIN_BLOCKS
+#define DBT_CULL_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cull_kernel(CullArgs a) {
   // launched programmatically behind prep_kernel: wait for its results
   asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_raw[];
