@@ -516,8 +516,11 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
             const uint32_t d = (((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF) - 1u;
             atomicAnd(&a.cells[off[k] + b].x, run_mask_of((int)d));  // RED.AND, fire and forget
             ++changed;
-            a.dist[off[k] + b] = (uint8_t)d;
           }
+          // the chunk's cache word in one store (see sweep_cull_kernel)
+          const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
+          *reinterpret_cast<uint2*>(a.dist + off[k]) = make_uint2((w[k].x & ~bm0) | ((d8[k].x - 0x01010101u) & bm0),
+                                                                (w[k].y & ~bm1) | ((d8[k].y - 0x01010101u) & bm1));
         }
       }
     }
@@ -835,8 +838,15 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
               const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
               atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
               ++changed;
-              a.dist[off + b] = (uint8_t)d;
             }
+            // the chunk's cache word in one store: lowered bytes take d (the
+            // table byte - 1, never borrows), the others the value read above.
+            // A concurrent lowering overwritten here only leaves its byte
+            // stale-high (>= the record's bit length): a redundant AND later.
+            const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
+            *reinterpret_cast<uint2*>(a.dist + off) =
+                make_uint2((w[r][j].x & ~bm0) | ((d8[r][j].x - 0x01010101u) & bm0),
+                           (w[r][j].y & ~bm1) | ((d8[r][j].y - 0x01010101u) & bm1));
           }
         }
     }
