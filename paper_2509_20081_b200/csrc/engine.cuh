@@ -181,6 +181,7 @@ struct dbt_grid {
   int64_t cap_raw_bytes = 0;    // raw input staging
   void* d_raw = nullptr;
   uint64_t* d_center = nullptr; // packed centre per point (kEmptyKey = not ok)
+  double* d_ray = nullptr;       // map-frame ray per point (binned by the shadow kernel)
   uint16_t* d_bin = nullptr;
   uint32_t* d_slot = nullptr;
   uint64_t* d_uniq = nullptr;   // unique packed centres

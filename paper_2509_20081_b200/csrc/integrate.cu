@@ -89,6 +89,8 @@ struct PrepArgs {
   // certificate bits instead of the hash table
   int claim;
   uint32_t* stamped;
+  int bins;     // direction bins here (else rays out, binned in shadow_bin_kernel)
+  double* ray;  // n x 3 map-frame rays (bins == 0)
 };
 
 constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
@@ -169,6 +171,58 @@ __device__ __forceinline__ bool floor_index(double v, double o, double vs, long 
 
 constexpr int kPrepThreads = 256;
 
+// Return i in the map frame (integrator.py:223-232): the source point
+// (downsampled index, per-scan offsets), and m = p @ R.T + t with the sensor
+// position t (map mode: given per point). Shared by prep and the shadow
+// kernel's bin phase, so both see the same doubles.
+__device__ __forceinline__ void map_point(const PrepArgs& a, int64_t i, int& s, double& m0, double& m1, double& m2,
+                                          double& t0, double& t1, double& t2) {
+  int64_t src;
+  s = 0;
+  if (a.inline_meta) {
+    src = i * a.ds;
+  } else {
+    s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+    src = (a.scan_ptr ? 0 : a.src_off[s]) + (i - a.scan_off[s]) * a.ds;
+  }
+  const void* pts = a.scan_ptr && !a.inline_meta ? (const void*)a.scan_ptr[s] : a.pts;
+  double p0, p1, p2;
+  if (a.dtype == DBT_F32) {
+    const float* q = (const float*)pts + 3 * src;
+    p0 = q[0];
+    p1 = q[1];
+    p2 = q[2];
+  } else {
+    const double* q = (const double*)pts + 3 * src;
+    p0 = q[0];
+    p1 = q[1];
+    p2 = q[2];
+  }
+  if (a.map_mode) {
+    m0 = p0;
+    m1 = p1;
+    m2 = p2;
+    t0 = a.sensor[3 * src];
+    t1 = a.sensor[3 * src + 1];
+    t2 = a.sensor[3 * src + 2];
+  } else {
+    const double* P = a.inline_meta ? a.pose0 : a.poses + 12 * s;
+    t0 = P[9];
+    t1 = P[10];
+    t2 = P[11];
+    // pts @ R.T + t: OpenBLAS dgemm accumulates k = 0,1,2 with FMA
+    // (probed on both the build and the GPU-box hosts), then numpy adds t.
+    m0 = __dadd_rn(__fma_rn(p2, P[2], __fma_rn(p1, P[1], __dmul_rn(p0, P[0]))), t0);
+    m1 = __dadd_rn(__fma_rn(p2, P[5], __fma_rn(p1, P[4], __dmul_rn(p0, P[3]))), t1);
+    m2 = __dadd_rn(__fma_rn(p2, P[8], __fma_rn(p1, P[7], __dmul_rn(p0, P[6]))), t2);
+  }
+}
+
+// np.linalg.norm(rays, axis=1): sqrt((x*x + y*y) + z*z), no FMA
+__device__ __forceinline__ double ray_norm(double rx, double ry, double rz) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
+}
+
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   // the sweep (programmatic dependent launch) may be scheduled once every
   // prep block has started; it waits for this grid's completion before
@@ -184,48 +238,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   bool claimed = false; // centre stamp already applied / claimed: no sweep
   uint64_t packed = kEmptyKey;
   if (live) {
-    int64_t src;
-    if (a.inline_meta) {
-      src = i * a.ds;
-    } else {
-      s = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
-      src = (a.scan_ptr ? 0 : a.src_off[s]) + (i - a.scan_off[s]) * a.ds;
-    }
-    const void* pts = a.scan_ptr && !a.inline_meta ? (const void*)a.scan_ptr[s] : a.pts;
-    double p0, p1, p2;
-    if (a.dtype == DBT_F32) {
-      const float* q = (const float*)pts + 3 * src;
-      p0 = q[0];
-      p1 = q[1];
-      p2 = q[2];
-    } else {
-      const double* q = (const double*)pts + 3 * src;
-      p0 = q[0];
-      p1 = q[1];
-      p2 = q[2];
-    }
     double m0, m1, m2, t0, t1, t2;
-    if (a.map_mode) {
-      m0 = p0;
-      m1 = p1;
-      m2 = p2;
-      t0 = a.sensor[3 * src];
-      t1 = a.sensor[3 * src + 1];
-      t2 = a.sensor[3 * src + 2];
-    } else {
-      const double* P = a.inline_meta ? a.pose0 : a.poses + 12 * s;
-      t0 = P[9];
-      t1 = P[10];
-      t2 = P[11];
-      // pts @ R.T + t: OpenBLAS dgemm accumulates k = 0,1,2 with FMA
-      // (probed on both the build and the GPU-box hosts), then numpy adds t.
-      m0 = __dadd_rn(__fma_rn(p2, P[2], __fma_rn(p1, P[1], __dmul_rn(p0, P[0]))), t0);
-      m1 = __dadd_rn(__fma_rn(p2, P[5], __fma_rn(p1, P[4], __dmul_rn(p0, P[3]))), t1);
-      m2 = __dadd_rn(__fma_rn(p2, P[8], __fma_rn(p1, P[7], __dmul_rn(p0, P[6]))), t2);
-    }
+    map_point(a, i, s, m0, m1, m2, t0, t1, t2);
     double rx = __dsub_rn(m0, t0), ry = __dsub_rn(m1, t1), rz = __dsub_rn(m2, t2);
-    // np.linalg.norm(rays, axis=1): sqrt((x*x + y*y) + z*z), no FMA
-    double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
+    double nrm = ray_norm(rx, ry, rz);
     ok = a.skip_norm ? 1 : (nrm >= a.vs);
     long long cx, cy, cz;
     bool fx = floor_index(m0, a.ox, a.vs, cx);
@@ -234,9 +250,17 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
     ok = ok && fx && fy && fz && cx >= a.R && cy >= a.R && cz >= a.R && cx <= a.nx - 1 - a.R &&
          cy <= a.ny - 1 - a.R && cz <= a.nz - 1 - a.R;
     if (ok) {
-      int ba, be;
-      bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
-      a.bin[i] = (uint16_t)(ba * a.b_el + be);
+      int ba = 0, be = 0;
+      if (a.bins) {
+        bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
+        a.bin[i] = (uint16_t)(ba * a.b_el + be);
+      } else {
+        // the shadow kernel bins the return from its ray (off the sweep's
+        // critical path, and without re-reading a zero-copy host scan)
+        a.ray[3 * i] = rx;
+        a.ray[3 * i + 1] = ry;
+        a.ray[3 * i + 2] = rz;
+      }
       packed = pack_center(cx, cy, cz);
       if (a.claim) {
         // claim the stamp certificate of the centre (one atomicOr): a bit
@@ -380,6 +404,10 @@ struct ShadowArgs {
   const int64_t* scan_off;
   ScanCounters* sc;
   LaunchCounters* lc;
+  // shadow_bin_kernel: rays from prep, bin table geometry
+  const double* ray;
+  int b_az, b_el;
+  const uint16_t* seeds;
 };
 
 __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
@@ -410,6 +438,64 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     if (lgx < 0) continue;
     shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
                (uint32_t)a.t_occ);
+  }
+}
+
+// Shadow update with the direction bins computed here (prep skips them, so
+// the sweep starts earlier; this kernel runs beside the sweep). A block takes
+// tiles of 256 >> log2s returns: phase 1, one thread per return, bins the
+// ray prep stored (bin_dev on the same doubles) and applies the first-return
+// choice; phase 2, one thread per (return, shadow offset), counts the visit
+// as shadow_kernel does.
+__global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
+  __shared__ uint64_t s_c[256];
+  __shared__ uint16_t s_b[256];
+  const int per = 256 >> a.log2s;
+  const int smask = (1 << a.log2s) - 1;
+  const int64_t tiles = (a.n + per - 1) / per;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * per;
+    if ((int)threadIdx.x < per) {
+      const int64_t i = r0 + threadIdx.x;
+      uint64_t c = i < a.n ? a.center[i] : kEmptyKey;
+      if (c != kEmptyKey && a.first_return) {
+        if (a.hmin[a.slot[i]] != (uint32_t)i) {
+          c = kEmptyKey;
+        } else {
+          // one atomic per group of lanes counting the same scan
+          const int sc = a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0;
+          const unsigned grp = __match_any_sync(__activemask(), sc);
+          if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&a.sc[sc].n_applied, (unsigned long long)__popc(grp));
+        }
+      }
+      uint16_t bin = 0;
+      if (c != kEmptyKey) {
+        const double rx = a.ray[3 * i], ry = a.ray[3 * i + 1], rz = a.ray[3 * i + 2];
+        int ba, be, fb;
+        bin_dev(rx, ry, rz, ray_norm(rx, ry, rz), a.b_az, a.b_el, a.seeds, ba, be, fb);
+        bin = (uint16_t)(ba * a.b_el + be);
+        if (fb) atomicAdd(&a.sc[a.S > 1 ? find_scan(a.scan_off, a.S, i) : 0].n_fallback, 1ull);  // rare
+      }
+      s_c[threadIdx.x] = c;
+      s_b[threadIdx.x] = bin;
+    }
+    __syncthreads();
+    const int j = threadIdx.x >> a.log2s, k = threadIdx.x & smask;
+    const uint64_t c = j < per ? s_c[j] : kEmptyKey;
+    if (c != kEmptyKey) {
+      const int b = s_b[j];
+      const int st = a.sstart[b];
+      if (k < a.sstart[b + 1] - st) {
+        const char4 o = reinterpret_cast<const char4*>(a.sxyz)[st + k];
+        int64_t cx, cy, cz;
+        unpack_center(c, cx, cy, cz);
+        const int64_t lgx = a.xm.local(cx + o.x);
+        if (lgx >= 0)
+          shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+                     (uint32_t)a.t_occ);
+      }
+    }
+    __syncthreads();  // s_c / s_b are rewritten by the next tile
   }
 }
 
@@ -938,7 +1024,7 @@ int grow(void** p, int64_t* cap, int64_t need, size_t elem) {
 int ensure_points(dbt_grid* g, int64_t n) {
   if (n <= g->cap_pts) return DBT_OK;
   int64_t c = std::max<int64_t>(n, g->cap_pts + g->cap_pts / 2);
-  void* ptrs[] = {g->d_center, g->d_bin, g->d_slot};
+  void* ptrs[] = {g->d_center, g->d_bin, g->d_slot, g->d_ray};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->d_uniq) cudaFree(g->d_uniq);
@@ -946,11 +1032,13 @@ int ensure_points(dbt_grid* g, int64_t n) {
   g->d_bin = nullptr;
   g->d_slot = nullptr;
   g->d_uniq = nullptr;
+  g->d_ray = nullptr;
   g->cap_pts = 0;
   DBT_CUDA(cudaMalloc(&g->d_center, c * sizeof(uint64_t)));
   DBT_CUDA(cudaMalloc(&g->d_bin, c * sizeof(uint16_t)));
   DBT_CUDA(cudaMalloc(&g->d_slot, c * sizeof(uint32_t)));
   DBT_CUDA(cudaMalloc(&g->d_uniq, c * sizeof(uint64_t)));
+  DBT_CUDA(cudaMalloc(&g->d_ray, c * 3 * sizeof(double)));
   g->cap_pts = c;
   return DBT_OK;
 }
@@ -1103,6 +1191,11 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   // it into preprocessing is kept as a measurement option
   const bool fuse_shadow =
       !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && (p->flags & DBT_FLAG_FUSE_SHADOW);
+  int shadow_l2 = 0;
+  while ((1 << shadow_l2) < b->max_shadow) ++shadow_l2;
+  // bins in the shadow kernel (off the critical path) when a tile of 256
+  // threads still bins >= 32 returns; otherwise (|S| > 8) in prep
+  const bool shadow_bins = b->max_shadow > 0 && !fuse_shadow && shadow_l2 <= 3;
 
   PrepArgs pa;
   pa.pts = d_pts;
@@ -1162,6 +1255,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.sc = g->d_scnt;
   pa.outcome = d_outcome;
   pa.seeds = device_seeds(g->device, &rc);
+  pa.bins = shadow_bins ? 0 : 1;
+  pa.ray = g->d_ray;
   if (rc) return rc;
   int tok;
   prof_begin(g, "prep_kernel", st, &tok);
@@ -1180,8 +1275,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sa.sxyz = b->d_shadow_xyz;
     sa.sstart = b->d_shadow_start;
     sa.n = n;
-    int l2 = 0;
-    while ((1 << l2) < b->max_shadow) ++l2;
+    const int l2 = shadow_l2;
     sa.log2s = l2;
     sa.x0 = g->x0;
     sa.x1 = g->x1;
@@ -1202,7 +1296,16 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     DBT_CUDA(cudaEventRecord(g->ev_fork, st));
     DBT_CUDA(cudaStreamWaitEvent(g->aux, g->ev_fork, 0));
     prof_begin(g, "shadow_kernel", g->aux, &tok);
-    shadow_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+    if (shadow_bins) {
+      const int64_t tiles = (n + (256 >> l2) - 1) >> (8 - l2);
+      sa.ray = g->d_ray;
+      sa.b_az = b->b_az;
+      sa.b_el = b->b_el;
+      sa.seeds = pa.seeds;
+      shadow_bin_kernel<<<(unsigned)std::min<int64_t>(tiles, 148 * 64), 256, 0, g->aux>>>(sa);
+    } else {
+      shadow_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+    }
     prof_end(g, g->aux, tok);
     DBT_CHECK_LAUNCH("shadow_kernel");
     DBT_CUDA(cudaEventRecord(g->ev_join, g->aux));
