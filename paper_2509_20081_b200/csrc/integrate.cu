@@ -660,6 +660,260 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
   return (uint64_t)(rbase >> 3) | ((uint64_t)c0 << 37) | ((uint64_t)c1 << 39) | ((uint64_t)drow << 41);
 }
 
+// Phase A of the culling sweep for one centre (one warp): neighbour
+// certificates -> per-lane dy interval and per-row dz interval -> the
+// surviving row tasks, reserved as one range of `total` slots through *q_n
+// (lane 0) and written with put(slot, task) (kEmptyKey for a row whose dz
+// interval is empty).
+template <typename Put>
+__device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put) {
+  const int R = a.R, K = a.K;
+  const int64_t sx = a.ny * a.nzp;
+  const uint16_t* rowd = a.rowd;
+  int64_t cx, cy, cz;
+  unpack_center(centre, cx, cy, cz);
+  // neighbour certificates: 27 bits, bit (a+1)*9 + (b+1)*3 + (c+1)
+  uint32_t nb3 = 0;
+  if (lane < 9) {
+    const int na = lane / 3 - 1, nbb = lane % 3 - 1;
+    const int64_t lgx = a.xm.local(cx + na);
+    if (lgx >= 0) {
+      const int64_t idx = (lgx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
+      const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+      const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+      nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
+    }
+  }
+  // axis neighbours at distance k = 2..5 (sparse returns: the next beam
+  // or azimuth step is often several voxels away): c + k e_x (lanes
+  // 9-16), c + k e_y (lanes 17-24), c + k e_z (lane 25: the centre row's
+  // bits cz-5 .. cz+5). Each cuts the half-space 2 k o_axis > k^2, i.e.
+  // o_axis >= k/2 + 1 on its side (inside its window: o_axis >= k - R).
+  // Bits: 4 per direction (k = 2..5): x+ 0-3, x- 4-7, y+ 8-11, y- 12-15,
+  // z+ 16-19, z- 20-23.
+  uint32_t ax = 0;
+  if (lane >= 9 && lane < 25) {
+    const int j = (lane - 9) & 7, k = 2 + (j & 3), sg = j < 4 ? 1 : -1;
+    const bool along_x = lane < 17;
+    const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
+    const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(qx) : -1;
+    if (lq >= 0) {
+      const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+      ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
+    }
+  } else if (lane == 25 && cz >= 5 && cz + 5 < a.nzp) {  // padding bits are never set
+    const int64_t lq = a.xm.local(cx);
+    if (lq >= 0) {
+      const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 5);
+      const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+      const uint32_t w1 = ((idx & 31) > 21) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+      const uint32_t b11 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7FFu;  // bit i: cz - 5 + i
+      const uint32_t up = (b11 >> 7) & 0xFu;                                // cz+2 .. cz+5
+      const uint32_t dn = __brev(b11 & 0xFu) >> 28;                         // cz-2 .. cz-5
+      ax = (up << 16) | (dn << 20);
+    }
+  }
+  const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
+  const uint32_t axm = __reduce_or_sync(0xffffffffu, ax);
+  // sparse neighbourhood (few of the 26 adjacent centres certified): also
+  // gather the norm-2 plane neighbours below (a second round of loads,
+  // skipped for dense surfaces where they add little)
+  uint32_t plm = 0;
+  if (__popc(nb) < kPlaneGatherBelow) {
+    // plane neighbours of norm 2 with one zero coordinate besides the
+    // axes: (a, b, 0) (lanes 0-11, bit cz) and (a, 0, c) (lanes 12-15: rows
+    // cx+1, cx-1, cx+2, cx-2 at bits cz-2 .. cz+2). Their cuts are
+    // constant per lane (a dy interval or a dz threshold). Index i of
+    // either list: |a|,|b| = (2,1) for i < 4, (1,2) for i < 8, (2,2) else;
+    // first sign + for even i>>1, second sign + for even i.
+    uint32_t plb = 0;
+    if (lane < 12) {
+      const int g = lane >> 2, sa = (lane & 2) ? -1 : 1, sb = (lane & 1) ? -1 : 1;
+      const int pa = sa * (g == 1 ? 1 : 2), pb = sb * (g == 0 ? 1 : 2);
+      const int64_t qy = cy + pb;
+      const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(cx + pa) : -1;
+      if (lq >= 0) {
+        const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+        plb = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
+      }
+    } else if (lane < 16 && cz >= 2 && cz + 2 < a.nzp) {
+      const int pa = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
+      const int64_t lq = a.xm.local(cx + pa);
+      if (lq >= 0) {
+        const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 2);
+        const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
+        const uint32_t w1 = ((idx & 31) > 27) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+        const uint32_t b5 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x1Fu;  // bit i: cz - 2 + i
+        const uint32_t cp1 = (b5 >> 3) & 1u, cm1 = (b5 >> 1) & 1u, cp2 = (b5 >> 4) & 1u, cm2 = b5 & 1u;
+        uint32_t xz = 0;
+        if (lane == 12) xz = (cp2 << 4) | (cm2 << 5);
+        if (lane == 13) xz = (cp2 << 6) | (cm2 << 7);
+        if (lane == 14) xz = cp1 | (cm1 << 1) | (cp2 << 8) | (cm2 << 9);
+        if (lane == 15) xz = (cp1 << 2) | (cm1 << 3) | (cp2 << 10) | (cm2 << 11);
+        plb = xz << 12;
+      }
+    }
+    plm = __reduce_or_sync(0xffffffffu, plb);
+  }
+#define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
+  // per lane: kernel x-offset dx, its dy interval and z-cut terms
+  const int dx = lane - R;
+  const int64_t lgx = lane < K ? a.xm.local(cx + dx) : -1;
+  bool dead = lgx < 0;
+  const int64_t xbase = dead ? 0 : lgx * sx;  // storage offset of this lane's x-plane
+  int ylo = -R, yhi = R;
+  int mp[3] = {kFar, kFar, kFar}, mm[3] = {-kFar, -kFar, -kFar};  // index b + 1
+#pragma unroll
+  for (int na = -1; na <= 1; ++na) {
+    const bool xw = na == 0 || (na > 0 ? dx >= -R + 1 : dx <= R - 1);  // v in e's x-window
+    if (!xw) continue;
+    const int s = na * dx;
+    if (na != 0 && NB(na, 0, 0) && s >= 1) dead = true;  // delta_z = 0: whole rows
+    const int t2 = na == 0 ? 1 : 2;                     // floor(|delta|^2 / 2) + 1
+    if (NB(na, 1, 0)) yhi = min(yhi, max(t2 - s, -R + 1) - 1);
+    if (NB(na, -1, 0)) ylo = max(ylo, min(s - t2, R - 1) + 1);
+#pragma unroll
+    for (int b = -1; b <= 1; ++b) {
+      const int t3 = (na * na + b * b + 1) / 2 + 1;
+      if (NB(na, b, 1)) mp[b + 1] = min(mp[b + 1], t3 - s);
+      if (NB(na, b, -1)) mm[b + 1] = max(mm[b + 1], s - t3);
+    }
+  }
+#undef NB
+  // axis neighbours: per direction the nearest present k gives the cut
+  // threshold thr = max(k / 2 + 1, k - R) (0 when none)
+  int thr[6];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const uint32_t bits = (axm >> (4 * d)) & 0xFu;
+    const int k = bits ? 2 + (__ffs(bits) - 1) : 0;
+    thr[d] = k ? max(k / 2 + 1, k - R) : 0;
+  }
+  if (thr[0] && dx >= thr[0]) dead = true;
+  if (thr[1] && dx <= -thr[1]) dead = true;
+  if (thr[2]) yhi = min(yhi, thr[2] - 1);
+  if (thr[3]) ylo = max(ylo, 1 - thr[3]);
+  if (thr[4]) mp[1] = min(mp[1], thr[4]);   // dz >= thr culled
+  if (thr[5]) mm[1] = max(mm[1], -thr[5]);  // dz <= -thr culled
+  // plane neighbours: (a, b, 0) cut b dy >= T - a dx, (a, 0, c) cut
+  // c dz >= T - a dx, T = |delta|^2 / 2 + 1, each inside its window
+  if (plm) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int g = i >> 2, s1 = (i & 2) ? -1 : 1, s2 = (i & 1) ? -1 : 1;
+      const int pa = s1 * (g == 1 ? 1 : 2), q = s2 * (g == 0 ? 1 : 2);
+      const bool xw = dx - pa <= R && pa - dx <= R;  // v inside e's x-window
+      const int num = (g == 2 ? 5 : 3) - pa * dx;
+      const int cdiv = g == 0 ? num : (num + 1) >> 1;  // ceil(num / |q|)
+      if (xw && ((plm >> i) & 1u)) {  // (pa, q, 0): dy cut
+        if (q > 0) yhi = min(yhi, max(cdiv, q - R) - 1);
+        else ylo = max(ylo, min(-cdiv, R + q) + 1);
+      }
+      if (xw && ((plm >> (12 + i)) & 1u)) {  // (pa, 0, q): dz cut
+        if (q > 0) mp[1] = min(mp[1], max(cdiv, q - R));
+        else mm[1] = max(mm[1], min(-cdiv, R + q));
+      }
+    }
+  }
+  const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
+  int pre = cnt;  // inclusive scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, pre, 31);
+  pre -= cnt;  // exclusive
+  const int64_t zs = cz - R;
+  const int sh = (int)(zs & 7);
+  const int64_t zb = zs >> 3;  // chunk index of the kernel's first chunk
+  const int64_t cbase = cy * a.nzp + (zb << 3);
+  // each lane writes its own column's rows at its prefix offset (no owner
+  // search, no per-row shuffles); a row with an empty dz interval fills
+  // its reserved slot with kEmptyKey
+  int qb = 0;
+  if (lane == 0 && total) qb = atomicAdd(q_n, total);
+  qb = __shfl_sync(0xffffffffu, qb, 0);
+  const int zhi0 = min(R, max(mp[1], -R + 1) - 1), zlo0 = max(-R, min(mm[1], R - 1) + 1);
+  const int drow0 = sh * a.nd * a.CH;
+  const uint16_t* rowd_dx = rowd + (dx + R) * K + R;
+  for (int k = 0; k < cnt; ++k) {
+    const int rdy = ylo + k;
+    // dz interval: delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1),
+    // delta_z = -1 ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only
+    // when v is in their y-window)
+    int zhi = zhi0, zlo = zlo0;
+    if (rdy <= R - 1) {  // b = -1
+      zhi = min(zhi, max(mp[0] + rdy, -R + 1) - 1);
+      zlo = max(zlo, min(mm[0] - rdy, R - 1) + 1);
+    }
+    if (rdy >= -R + 1) {  // b = +1
+      zhi = min(zhi, max(mp[2] - rdy, -R + 1) - 1);
+      zlo = max(zlo, min(mm[2] + rdy, R - 1) + 1);
+    }
+    uint64_t task = kEmptyKey;
+    if (zlo <= zhi) {
+      const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
+      task = pack_task(xbase + cbase + rdy * a.nzp, c0, c1, drow0 + __ldg(rowd_dx + rdy));
+    }
+    put(qb + pre + k, task);
+  }
+}
+
+// Phase B of the culling sweep: one thread, two row tasks (kEmptyKey = none)
+// with their chunk loads in flight together; a cached byte above the row's
+// run length marks a voxel this centre lowers: RED.AND into the record, and
+// the chunk's cache word written back once.
+__device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t tasks[2], unsigned long long& changed,
+                                            unsigned long long& rows_done) {
+  const uint2* dtab = a.dtab;
+  uint2 w[2][4], d8[2][4];
+  int64_t rb[2];
+  int cb[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint64_t task = tasks[r];
+    rows_done += task != kEmptyKey;
+    rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
+    const int c0 = (int)((task >> 37) & 3), c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
+    cb[r] = c0;
+    const uint2* drow = dtab + (int)(task >> 41);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool act = c0 + j <= c1;
+      d8[r][j] = act ? __ldg(drow + c0 + j) : make_uint2(0x40404040u, 0x40404040u);
+      // inactive chunks read one shared dummy sector
+      w[r][j] = *reinterpret_cast<const uint2*>(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t lt0 = ((w[r][j].x | 0x80808080u) - d8[r][j].x) & 0x80808080u;
+      const uint32_t lt1 = ((w[r][j].y | 0x80808080u) - d8[r][j].y) & 0x80808080u;
+      if (lt0 | lt1) {
+        const int64_t off = rb[r] + 8 * (cb[r] + j);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const uint32_t lt = b < 4 ? lt0 : lt1;
+          if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
+          const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
+          atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
+          ++changed;
+        }
+        // the chunk's cache word in one store: lowered bytes take d (the
+        // table byte - 1, never borrows), the others the value read above.
+        // A concurrent lowering overwritten here only leaves its byte
+        // stale-high (>= the record's bit length): a redundant AND later.
+        const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
+        *reinterpret_cast<uint2*>(a.dist + off) =
+            make_uint2((w[r][j].x & ~bm0) | ((d8[r][j].x - 0x01010101u) & bm0),
+                       (w[r][j].y & ~bm1) | ((d8[r][j].y - 0x01010101u) & bm1));
+      }
+    }
+}
+
 // 8 resident blocks per SM (64 registers, 24 B spilled): same-box A/B vs 7
 // (72 registers): config 2 +2.7 %, config 1 +5 %, config 3 neutral; 9 or 10
 // blocks (56 / 48 registers) spill more and are slower
@@ -674,14 +928,10 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
   __shared__ int q_n;
   __shared__ long long batch0, batch_next;
   // the d-table (17 KB for K = 21) is read through L1 (__ldg), not staged
-  const uint2* dtab = a.dtab;
-  const uint16_t* rowd = a.rowd;
   if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int R = a.R, K = a.K;
   const int64_t n_items = (int64_t)a.lc->n_unique;
-  const int64_t sx = a.ny * a.nzp;
   unsigned long long changed = 0, rows_done = 0;
   while (true) {
     if (threadIdx.x == 0) {
@@ -692,195 +942,7 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
     const int64_t item = batch0 + warp;
     if (batch0 >= n_items) break;
     if (item < n_items) {
-      // ===== phase A: this warp's centre -> surviving row tasks =====
-      int64_t cx, cy, cz;
-      unpack_center(a.uniq[item], cx, cy, cz);
-      // neighbour certificates: 27 bits, bit (a+1)*9 + (b+1)*3 + (c+1)
-      uint32_t nb3 = 0;
-      if (lane < 9) {
-        const int na = lane / 3 - 1, nbb = lane % 3 - 1;
-        const int64_t lgx = a.xm.local(cx + na);
-        if (lgx >= 0) {
-          const int64_t idx = (lgx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
-          const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-          const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
-          nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
-        }
-      }
-      // axis neighbours at distance k = 2..5 (sparse returns: the next beam
-      // or azimuth step is often several voxels away): c + k e_x (lanes
-      // 9-16), c + k e_y (lanes 17-24), c + k e_z (lane 25: the centre row's
-      // bits cz-5 .. cz+5). Each cuts the half-space 2 k o_axis > k^2, i.e.
-      // o_axis >= k/2 + 1 on its side (inside its window: o_axis >= k - R).
-      // Bits: 4 per direction (k = 2..5): x+ 0-3, x- 4-7, y+ 8-11, y- 12-15,
-      // z+ 16-19, z- 20-23.
-      uint32_t ax = 0;
-      if (lane >= 9 && lane < 25) {
-        const int j = (lane - 9) & 7, k = 2 + (j & 3), sg = j < 4 ? 1 : -1;
-        const bool along_x = lane < 17;
-        const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
-        const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(qx) : -1;
-        if (lq >= 0) {
-          const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
-          ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
-        }
-      } else if (lane == 25 && cz >= 5 && cz + 5 < a.nzp) {  // padding bits are never set
-        const int64_t lq = a.xm.local(cx);
-        if (lq >= 0) {
-          const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 5);
-          const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-          const uint32_t w1 = ((idx & 31) > 21) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
-          const uint32_t b11 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7FFu;  // bit i: cz - 5 + i
-          const uint32_t up = (b11 >> 7) & 0xFu;                                // cz+2 .. cz+5
-          const uint32_t dn = __brev(b11 & 0xFu) >> 28;                         // cz-2 .. cz-5
-          ax = (up << 16) | (dn << 20);
-        }
-      }
-      const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
-      const uint32_t axm = __reduce_or_sync(0xffffffffu, ax);
-      // sparse neighbourhood (few of the 26 adjacent centres certified): also
-      // gather the norm-2 plane neighbours below (a second round of loads,
-      // skipped for dense surfaces where they add little)
-      uint32_t plm = 0;
-      if (__popc(nb) < kPlaneGatherBelow) {
-        // plane neighbours of norm 2 with one zero coordinate besides the
-        // axes: (a, b, 0) (lanes 0-11, bit cz) and (a, 0, c) (lanes 12-15: rows
-        // cx+1, cx-1, cx+2, cx-2 at bits cz-2 .. cz+2). Their cuts are
-        // constant per lane (a dy interval or a dz threshold). Index i of
-        // either list: |a|,|b| = (2,1) for i < 4, (1,2) for i < 8, (2,2) else;
-        // first sign + for even i>>1, second sign + for even i.
-        uint32_t plb = 0;
-        if (lane < 12) {
-          const int g = lane >> 2, sa = (lane & 2) ? -1 : 1, sb = (lane & 1) ? -1 : 1;
-          const int pa = sa * (g == 1 ? 1 : 2), pb = sb * (g == 0 ? 1 : 2);
-          const int64_t qy = cy + pb;
-          const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(cx + pa) : -1;
-          if (lq >= 0) {
-            const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
-            plb = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
-          }
-        } else if (lane < 16 && cz >= 2 && cz + 2 < a.nzp) {
-          const int pa = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
-          const int64_t lq = a.xm.local(cx + pa);
-          if (lq >= 0) {
-            const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 2);
-            const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-            const uint32_t w1 = ((idx & 31) > 27) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
-            const uint32_t b5 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x1Fu;  // bit i: cz - 2 + i
-            const uint32_t cp1 = (b5 >> 3) & 1u, cm1 = (b5 >> 1) & 1u, cp2 = (b5 >> 4) & 1u, cm2 = b5 & 1u;
-            uint32_t xz = 0;
-            if (lane == 12) xz = (cp2 << 4) | (cm2 << 5);
-            if (lane == 13) xz = (cp2 << 6) | (cm2 << 7);
-            if (lane == 14) xz = cp1 | (cm1 << 1) | (cp2 << 8) | (cm2 << 9);
-            if (lane == 15) xz = (cp1 << 2) | (cm1 << 3) | (cp2 << 10) | (cm2 << 11);
-            plb = xz << 12;
-          }
-        }
-        plm = __reduce_or_sync(0xffffffffu, plb);
-      }
-#define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
-      // per lane: kernel x-offset dx, its dy interval and z-cut terms
-      const int dx = lane - R;
-      const int64_t lgx = lane < K ? a.xm.local(cx + dx) : -1;
-      bool dead = lgx < 0;
-      const int64_t xbase = dead ? 0 : lgx * sx;  // storage offset of this lane's x-plane
-      int ylo = -R, yhi = R;
-      int mp[3] = {kFar, kFar, kFar}, mm[3] = {-kFar, -kFar, -kFar};  // index b + 1
-#pragma unroll
-      for (int na = -1; na <= 1; ++na) {
-        const bool xw = na == 0 || (na > 0 ? dx >= -R + 1 : dx <= R - 1);  // v in e's x-window
-        if (!xw) continue;
-        const int s = na * dx;
-        if (na != 0 && NB(na, 0, 0) && s >= 1) dead = true;  // delta_z = 0: whole rows
-        const int t2 = na == 0 ? 1 : 2;                     // floor(|delta|^2 / 2) + 1
-        if (NB(na, 1, 0)) yhi = min(yhi, max(t2 - s, -R + 1) - 1);
-        if (NB(na, -1, 0)) ylo = max(ylo, min(s - t2, R - 1) + 1);
-#pragma unroll
-        for (int b = -1; b <= 1; ++b) {
-          const int t3 = (na * na + b * b + 1) / 2 + 1;
-          if (NB(na, b, 1)) mp[b + 1] = min(mp[b + 1], t3 - s);
-          if (NB(na, b, -1)) mm[b + 1] = max(mm[b + 1], s - t3);
-        }
-      }
-#undef NB
-      // axis neighbours: per direction the nearest present k gives the cut
-      // threshold thr = max(k / 2 + 1, k - R) (0 when none)
-      int thr[6];
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        const uint32_t bits = (axm >> (4 * d)) & 0xFu;
-        const int k = bits ? 2 + (__ffs(bits) - 1) : 0;
-        thr[d] = k ? max(k / 2 + 1, k - R) : 0;
-      }
-      if (thr[0] && dx >= thr[0]) dead = true;
-      if (thr[1] && dx <= -thr[1]) dead = true;
-      if (thr[2]) yhi = min(yhi, thr[2] - 1);
-      if (thr[3]) ylo = max(ylo, 1 - thr[3]);
-      if (thr[4]) mp[1] = min(mp[1], thr[4]);   // dz >= thr culled
-      if (thr[5]) mm[1] = max(mm[1], -thr[5]);  // dz <= -thr culled
-      // plane neighbours: (a, b, 0) cut b dy >= T - a dx, (a, 0, c) cut
-      // c dz >= T - a dx, T = |delta|^2 / 2 + 1, each inside its window
-      if (plm) {
-#pragma unroll
-        for (int i = 0; i < 12; ++i) {
-          const int g = i >> 2, s1 = (i & 2) ? -1 : 1, s2 = (i & 1) ? -1 : 1;
-          const int pa = s1 * (g == 1 ? 1 : 2), q = s2 * (g == 0 ? 1 : 2);
-          const bool xw = dx - pa <= R && pa - dx <= R;  // v inside e's x-window
-          const int num = (g == 2 ? 5 : 3) - pa * dx;
-          const int cdiv = g == 0 ? num : (num + 1) >> 1;  // ceil(num / |q|)
-          if (xw && ((plm >> i) & 1u)) {  // (pa, q, 0): dy cut
-            if (q > 0) yhi = min(yhi, max(cdiv, q - R) - 1);
-            else ylo = max(ylo, min(-cdiv, R + q) + 1);
-          }
-          if (xw && ((plm >> (12 + i)) & 1u)) {  // (pa, 0, q): dz cut
-            if (q > 0) mp[1] = min(mp[1], max(cdiv, q - R));
-            else mm[1] = max(mm[1], min(-cdiv, R + q));
-          }
-        }
-      }
-      const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
-      int pre = cnt;  // inclusive scan
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, pre, 31);
-      pre -= cnt;  // exclusive
-      const int64_t zs = cz - R;
-      const int sh = (int)(zs & 7);
-      const int64_t zb = zs >> 3;  // chunk index of the kernel's first chunk
-      const int64_t cbase = cy * a.nzp + (zb << 3);
-      // each lane writes its own column's rows at its prefix offset (no owner
-      // search, no per-row shuffles); a row with an empty dz interval fills
-      // its reserved slot with kEmptyKey
-      int qb = 0;
-      if (lane == 0 && total) qb = atomicAdd(&q_n, total);
-      qb = __shfl_sync(0xffffffffu, qb, 0);
-      const int zhi0 = min(R, max(mp[1], -R + 1) - 1), zlo0 = max(-R, min(mm[1], R - 1) + 1);
-      const int drow0 = sh * a.nd * a.CH;
-      const uint16_t* rowd_dx = rowd + (dx + R) * K + R;
-      for (int k = 0; k < cnt; ++k) {
-        const int rdy = ylo + k;
-        // dz interval: delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1),
-        // delta_z = -1 ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only
-        // when v is in their y-window)
-        int zhi = zhi0, zlo = zlo0;
-        if (rdy <= R - 1) {  // b = -1
-          zhi = min(zhi, max(mp[0] + rdy, -R + 1) - 1);
-          zlo = max(zlo, min(mm[0] - rdy, R - 1) + 1);
-        }
-        if (rdy >= -R + 1) {  // b = +1
-          zhi = min(zhi, max(mp[2] - rdy, -R + 1) - 1);
-          zlo = max(zlo, min(mm[2] + rdy, R - 1) + 1);
-        }
-        uint64_t task = kEmptyKey;
-        if (zlo <= zhi) {
-          const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
-          task = pack_task(xbase + cbase + rdy * a.nzp, c0, c1, drow0 + __ldg(rowd_dx + rdy));
-        }
-        queue[qb + pre + k] = task;
-      }
+      cull_centre(a, a.uniq[item], lane, &q_n, [&](int i, uint64_t t) { queue[i] = t; });
     }
     __syncthreads();
     // next batch index: its atomic overlaps phase B
@@ -889,52 +951,9 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
     // two rows' chunk loads in flight per thread =====
     const int nq = q_n;
     for (int i = threadIdx.x; i < nq; i += 2 * blockDim.x) {
-      uint2 w[2][4], d8[2][4];
-      int64_t rb[2];
-      int cb[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int qi = i + r * blockDim.x;
-        const uint64_t task = qi < nq ? queue[qi] : kEmptyKey;
-        rows_done += task != kEmptyKey;
-        rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
-        const int c0 = (int)((task >> 37) & 3), c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
-        cb[r] = c0;
-        const uint2* drow = dtab + (int)(task >> 41);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool act = c0 + j <= c1;
-          d8[r][j] = act ? __ldg(drow + c0 + j) : make_uint2(0x40404040u, 0x40404040u);
-          // inactive chunks read one shared dummy sector
-          w[r][j] = *reinterpret_cast<const uint2*>(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t lt0 = ((w[r][j].x | 0x80808080u) - d8[r][j].x) & 0x80808080u;
-          const uint32_t lt1 = ((w[r][j].y | 0x80808080u) - d8[r][j].y) & 0x80808080u;
-          if (lt0 | lt1) {
-            const int64_t off = rb[r] + 8 * (cb[r] + j);
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              const uint32_t lt = b < 4 ? lt0 : lt1;
-              if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
-              const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-              atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
-              ++changed;
-            }
-            // the chunk's cache word in one store: lowered bytes take d (the
-            // table byte - 1, never borrows), the others the value read above.
-            // A concurrent lowering overwritten here only leaves its byte
-            // stale-high (>= the record's bit length): a redundant AND later.
-            const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
-            *reinterpret_cast<uint2*>(a.dist + off) =
-                make_uint2((w[r][j].x & ~bm0) | ((d8[r][j].x - 0x01010101u) & bm0),
-                           (w[r][j].y & ~bm1) | ((d8[r][j].y - 0x01010101u) & bm1));
-          }
-        }
+      const uint64_t tasks[2] = {i < nq ? queue[i] : kEmptyKey,
+                                 i + (int)blockDim.x < nq ? queue[i + blockDim.x] : kEmptyKey};
+      sweep_rows2(a, tasks, changed, rows_done);
     }
     __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
