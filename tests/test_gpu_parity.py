@@ -858,3 +858,31 @@ class TestReplicaMerge:
         with pytest.raises(ConfigurationError):
             _native.check(_native.lib().dbt_replica_pack(g.handle, ctypes.c_void_p(0), ctypes.c_void_p(0),
                                                          ctypes.c_void_p(0), None))
+
+
+@pytest.mark.parametrize("shadow_radius", [1, 2])
+def test_bin_fallback_counted_per_scan(shadow_radius):
+    """A ray component below 2^-1020 takes SVML's scalar helper, which is not
+    restated: the engine bins that ray with CUDA's atan2 and counts it in the
+    scan's bin_fallbacks. r_s = 1 (|S| = 4) bins in shadow_bin_kernel, r_s = 2
+    (|S| = 17) in prep; a two-scan launch attributes the count to its scan.
+    The azimuth of (2, 1e-308) is bin 0 either way, so the grid still equals
+    the oracle's."""
+    bank = build_kernel_bank(shadow_radius=shadow_radius)
+    dims, vs, org = (64, 64, 64), 0.1, (-3.2, -3.2, -3.2)
+    pts_a = np.array([[2.0, 0.5, 0.3], [1.0, -1.0, 0.5]])
+    pts_b = np.array([[2.0, 1e-308, 0.3], [-1.5, 0.7, -0.2]])
+    eye = np.eye(4)
+    g = new_grid(dims, vs, org)
+    sts = integrate_frames(g, bank, [ScanFrame(points=pts_a, pose=eye), ScanFrame(points=pts_b, pose=eye)],
+                           IntegrationParams())
+    assert [s.bin_fallbacks for s in sts] == [0, 1]
+    assert [s.points_in - s.points_discarded for s in sts] == [2, 2]
+    st = integrate_frame(new_grid(dims, vs, org), bank, ScanFrame(points=pts_b, pose=eye), IntegrationParams())
+    assert st.bin_fallbacks == 1
+    og = oracle.OracleGrid(dims, vs, org)
+    ob = oracle.OracleBank.from_bank(bank)
+    oracle.integrate_frame(og, ob, pts_a, eye)
+    oracle.integrate_frame(og, ob, pts_b, eye)
+    m, s, h = g.download_range(0, dims[0])
+    assert np.array_equal(m, og.mask) and np.array_equal(s, og.sign) and np.array_equal(h, og.hits)
