@@ -1212,9 +1212,12 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
       !p->first_return && b->max_shadow > 0 && b->max_shadow <= 8 && (p->flags & DBT_FLAG_FUSE_SHADOW);
   int shadow_l2 = 0;
   while ((1 << shadow_l2) < b->max_shadow) ++shadow_l2;
-  // bins in the shadow kernel (off the critical path) when a tile of 256
-  // threads still bins >= 32 returns; otherwise (|S| > 8) in prep
-  const bool shadow_bins = b->max_shadow > 0 && !fuse_shadow && shadow_l2 <= 3;
+  // bins in the shadow kernel (off the critical path) for a single-scan
+  // sized launch whose tile of 256 threads still bins >= 32 returns; big
+  // batched launches keep them in prep, where the latency-bound shadow tile
+  // loop would become the critical path (same-box A/B, config 5: 8 scans per
+  // launch +7 %, 32 scans +16 % with the bins in prep)
+  const bool shadow_bins = b->max_shadow > 0 && !fuse_shadow && shadow_l2 <= 3 && n <= (1 << 19);
 
   PrepArgs pa;
   pa.pts = d_pts;
