@@ -92,7 +92,9 @@ typedef struct dbt_stats {
   int64_t bin_fallbacks;    /* returns binned outside the SVML restatement (a nonzero ray
                                component below 2^-1020 or above 2^993); 0 in practice */
   double elapsed_ms;        /* host wall clock around the call (integrator.py:217,286) */
-  double device_ms;         /* CUDA-event time of the device work (H2D .. stats D2H) */
+  double device_ms;         /* CUDA-event time of the device work (H2D .. stats D2H); only measured
+                               under dbt_profile_enable or with $DBT_DEVICE_MS set when the grid was
+                               created (the two timing events cost ~4 us per call), else 0 */
   int64_t rows_swept;       /* kernel z-rows the sweep read (after neighbour culling);
                                launch-wide, reported on the first scan */
 } dbt_stats;
