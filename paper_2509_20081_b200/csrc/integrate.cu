@@ -652,7 +652,13 @@ struct CullArgs {
 
 constexpr int kFar = 1 << 20;
 constexpr int kPlaneGatherBelow = 8;  // certified adjacent centres below which plane neighbours are read
-constexpr int kCullWarps = 4;  // centres per block batch (one per warp; 4 measured best of 1/2/4/8)
+// centres per block batch (one warp each). Same-box A/B at 64 registers
+// (4 resident blocks of 8 warps): 8 vs 4 config 2 +8.5 %, config 3 +11 %,
+// config 1 +2 %, config 4 +1.6 %, config 5 +1 %; 2, 12 and 16 are slower
+#ifndef DBT_CULL_WARPS
+#define DBT_CULL_WARPS 8
+#endif
+constexpr int kCullWarps = DBT_CULL_WARPS;
 
 // row task: bits 0-36 row start / 8 (cells), 37-38 first chunk, 39-40 last
 // chunk, 41-54 d-table row offset
@@ -914,11 +920,11 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
     }
 }
 
-// 8 resident blocks per SM (64 registers, 24 B spilled): same-box A/B vs 7
-// (72 registers): config 2 +2.7 %, config 1 +5 %, config 3 neutral; 9 or 10
-// blocks (56 / 48 registers) spill more and are slower
+// 32 resident warps per SM (64 registers, a few bytes spilled): same-box A/B
+// vs 28 (72 registers): config 2 +2.7 %, config 1 +5 %, config 3 neutral;
+// 36 or 40 warps (56 / 48 registers) spill more and are slower
 #ifndef DBT_CULL_MIN_BLOCKS
-#define DBT_CULL_MIN_BLOCKS 8
+#define DBT_CULL_MIN_BLOCKS (32 / DBT_CULL_WARPS)
 #endif
 __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cull_kernel(CullArgs a) {
   // launched programmatically behind prep_kernel: wait for its results
