@@ -1,30 +1,37 @@
 """Benchmark: LiDAR points integrated per second (BASELINE.json metric).
 
-Default workload (configs[1] of BASELINE.json, the single-GPU config the
-metric is quoted on): config 2 — 100-scan trajectory in the synthetic box
-room, 64 beams x 1024 azimuths (65 536 float32 returns per scan), 0.05 m
-voxels on the 400x400x100 room padded by 11 voxels (422x422x122; the literal
-grid discards every wall return), K=21 kernel, 40x40 bins, shadow radius 1.
-`--config N` selects another BASELINE config (3: street 2000x2000x100 @ 0.1 m,
-4: 4000x4000x400 @ 0.02 m, 5: config-3 scans, `--batch S` per launch).
+Default workload: BASELINE config 4, the largest configuration that fits one
+B200 — the config-3 street scene and 128x2048-beam sensor at 0.02 m voxels on
+the full 4000x4000x400 grid (6.4e9 voxels, 58 GB of device state), K=21
+kernel, 40x40 bins, shadow radius 2. `--config N` selects another BASELINE
+config (1: room scan, 2: room trajectory, 3: street 2000x2000x100 @ 0.1 m,
+5: config-3 scans, `--batch S` per launch).
 
-A step integrates the next scan (or the next S scans, one launch) of the
-trajectory into the grid that holds all previous scans (the grid is reset
-when the trajectory wraps, outside the timed region). L2 is flushed (256 MB
-write) between timed steps.
+Fixed scan window (independent of --steps / --warmup): the grid first holds
+the trajectory's scans 0-9 (prefill, untimed); a step integrates the next
+scan (the next S scans for --batch S, one launch) of the window, scans 10-29
+(batches: max(2, 128 // S) batches from scan 10). After the last window
+batch the grid is reset and refilled (untimed, between the step events), so
+every pass over the window times the same grid states. Warm-up steps run the
+same window, then the grid is reset and refilled before the timed region.
+Config 1 has one scan: every step integrates it into a fresh grid. L2 is
+flushed (256 MB write) before every step; the config-4 grid is 58 GB anyway.
 
   value : applied returns / device seconds, scans resident in HBM, CUDA
           events on the launch stream around each step (launch sequence incl.
-          the concurrent shadow stream and the counter copy), summed over K
-          steps, max over ranks.
+          the concurrent shadow stream), max over ranks.
   e2e   : same metric through the public API (integrate_frame /
-          integrate_frames over PINNED host float32 scans): validation, H2D,
-          launches, D2H of the FrameStats counters, host wall clock per call.
+          integrate_frames) with PINNED host float32 scans: validation, the
+          scan's host->device transfer, launches, the FrameStats read-back,
+          host wall clock per call. `e2e_pageable` repeats it with the plain
+          numpy scans a stock caller passes.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                [--config 2] [--batch 1]
-Under torchrun (N>1) every rank owns an x-slab of the grid; rank 0 holds the
-scans and broadcasts each step's points over NCCL inside the timed region.
+                [--config 4] [--batch 1] [--multi slab|replica]
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one process per GPU). N > 1 default: interleaved x-slabs, every rank stamps
+only the part of each return's cube inside its planes; rank 0 holds the scans
+and broadcasts each step's points over NCCL inside the timed region.
 """
 
 from __future__ import annotations
@@ -33,6 +40,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -49,6 +57,8 @@ import workloads  # noqa: E402
 METRIC = "LiDAR points integrated/sec (device-timed)"
 UNIT = "points/s"
 K_EDGE = 21
+PREFILL = 10   # trajectory scans in the grid before the window
+WINDOW = 20    # window scans (single-scan steps)
 
 
 def b_alg(shadow_cells: float) -> float:
@@ -62,8 +72,38 @@ def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def plan(w, batch: int):
+    """(prefill scan ids, window batches as lists of scan ids)."""
+    if w.n_scans == 1:
+        return [], [[0]]
+    if batch == 1:
+        return list(range(PREFILL)), [[PREFILL + j] for j in range(WINDOW)]
+    nb = max(2, 128 // batch)
+    return list(range(PREFILL)), [list(range(PREFILL + j * batch, PREFILL + (j + 1) * batch)) for j in range(nb)]
+
+
+def window_desc(w, batch):
+    pre, win = plan(w, batch)
+    if not pre:
+        return "scan 0 into a fresh grid every step"
+    return (f"grid holds scans 0-{pre[-1]} (prefill, untimed); step j integrates window batch j mod {len(win)} "
+            f"(scans {win[0][0]}-{win[-1][-1]}, {batch} scan(s) per launch); reset + prefill after every pass "
+            f"(untimed) — independent of --steps/--warmup")
 
 
 class ClockSampler:
@@ -131,13 +171,14 @@ def _scan_job(args):
     return workloads.get(config).scan(k)
 
 
-def gen_scans(w, n):
-    """Scans 0..n-1 of the trajectory (ray casting in a process pool for the
-    street scenes, ~2.6 s per config-3 scan)."""
-    if w.config <= 2 or n <= 2:
-        return [w.scan(k) for k in range(n)]
-    with ProcessPoolExecutor(max_workers=min(n, os.cpu_count() or 1)) as ex:
-        return list(ex.map(_scan_job, [(w.config, k) for k in range(n)]))
+def gen_scans(w, ids):
+    """{scan id: float32 points} (ray casting in a process pool for the street
+    scenes, ~2.6 s per config-3 scan)."""
+    ids = sorted(set(ids))
+    if w.config <= 2 or len(ids) <= 2:
+        return {k: w.scan(k) for k in ids}
+    with ProcessPoolExecutor(max_workers=min(len(ids), os.cpu_count() or 1)) as ex:
+        return dict(zip(ids, ex.map(_scan_job, [(w.config, k) for k in ids])))
 
 
 def cpu_grid_for(w):
@@ -150,108 +191,147 @@ def cpu_grid_for(w):
     return w.dims, w.origin, "same grid"
 
 
-def cpu_baseline(w, scans, budget_s=12.0, threads=None):
+def cpu_baseline(w, batch, scans, budget_s=12.0, threads=None):
     """Oracle port (C preprocessing + C serial-order stamping, x-slab threads
-    over all host cores) on the first scans of the same trajectory until the
-    time budget is spent. Returns applied returns / s."""
+    over all host cores) on the prefill + window scans in trajectory order
+    until the time budget is spent. Returns applied returns / s."""
     import oracle
 
     threads = threads or oracle.os_threads()
     ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
     dims, origin, note = cpu_grid_for(w)
     g = oracle.OracleGrid(dims, w.voxel_size, origin)
+    pre, win = plan(w, batch)
+    order = pre + [k for b in win for k in b]
     applied = 0
     t0 = time.perf_counter()
-    k = 0
-    while k < len(scans):
+    n = 0
+    for k in order:
         st = oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
         applied += st.points_in - st.points_discarded
-        k += 1
+        n += 1
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return {"value": applied / el, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"config-{w.config} scans 0..{k - 1} ({k} scans, {applied} applied returns) in {el:.1f} s, "
-                      f"{note}, oracle C port (libm transcendentals), {threads} threads (x-slab stamping)"}
+    return {"value": applied / el, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"config-{w.config} scans {order[0]}..{order[n - 1]} ({n} scans, {applied} applied returns) "
+                      f"in {el:.1f} s, {note}, oracle C port of the reference integrate_frame (libm "
+                      f"transcendentals), {threads} threads (x-slab stamping) on {cpu_model()}"}
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (the
     oracle port of the Python reference, which cannot travel to the GPU box)
-    on the same workload, all host threads, one scan per step."""
+    on the same window, all host threads, one window batch per step."""
     if rank != 0:
         return
     import oracle
 
     w = workloads.get(args.config)
-    n = args.warmup + args.steps
-    scans = gen_scans(w, min(n, w.n_scans))
+    B = max(1, args.batch)
+    pre, win = plan(w, B)
+    scans = gen_scans(w, pre + [k for b in win for k in b])
     threads = oracle.os_threads()
     ob = oracle.OracleBank.build(size=K_EDGE, shadow_radius=w.shadow_radius)
     dims, origin, note = cpu_grid_for(w)
-    g = oracle.OracleGrid(dims, w.voxel_size, origin)
+
+    def fresh():
+        g = oracle.OracleGrid(dims, w.voxel_size, origin)
+        for k in pre:
+            oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
+        return g
+
+    g = fresh()
     applied, el = 0, 0.0
-    for s in range(n):
-        k = s % len(scans)
-        if k == 0 and s > 0:
-            g = oracle.OracleGrid(dims, w.voxel_size, origin)
+    for s in range(args.warmup + args.steps):
+        if s == args.warmup or (s and s % len(win) == 0):
+            g = fresh()
+        j = (s - args.warmup) % len(win) if s >= args.warmup else s % len(win)
         t0 = time.perf_counter()
-        st = oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
+        a = 0
+        for k in win[j]:
+            st = oracle.integrate_frame(g, ob, scans[k], w.poses[k], threads=threads, c_prep=True)
+            a += st.points_in - st.points_discarded
         dt = time.perf_counter() - t0
         if s >= args.warmup:
-            applied += st.points_in - st.points_discarded
+            applied += a
             el += dt
     value = applied / el
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} timed scans of config {args.config} (full scans, {note}), oracle "
-                                   f"C port of the reference integrate_frame, {threads} threads"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": config_desc(w, B),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} timed window steps of config {args.config} ({note}), oracle C "
+                                   f"port of the reference integrate_frame, {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_desc(w, batch, interleave=0, replica=False):
+def config_desc(w, batch, interleave=0, multi="single"):
     scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
-    return {"workload": f"config {w.config}: {scene}, {w.n_scans}-scan trajectory, {w.beams}x{w.n_az} float32 "
-                        f"returns/scan, {w.voxel_size} m voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]}"
+    par = {"single": "single GPU",
+           "replica": "data-parallel whole-grid replicas: each rank integrates a contiguous segment of the window, "
+                      "one exact merge (MIN/MIN/SUM all-reduces) at the end of every pass, timed",
+           "slab": f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks): every rank "
+                   "stamps only the part of each return's cube inside its planes; points broadcast from rank 0 "
+                   "over NCCL every step"}[multi]
+    return {"workload": f"config {w.config}: {scene}, {w.beams}x{w.n_az} float32 returns/scan, {w.voxel_size} m "
+                        f"voxels, grid {w.dims[0]}x{w.dims[1]}x{w.dims[2]}"
                         + (" (literal room grid padded by 11)" if w.config <= 2 else ""),
             "kernel": f"{K_EDGE}^3", "bins": "40x40", "shadow_radius": w.shadow_radius, "t_occ": 2, "h_max": 255,
-            "scans_per_step": batch,
-            "step": f"{batch} scan(s) integrated into the trajectory grid in one launch",
-            "l2": "flushed between steps (256 MB write)",
-            "parallelism": ("data-parallel whole-grid replicas: each rank integrates its own scans (consecutive "
-                            "trajectory scans dealt round-robin), one exact merge (MIN/MIN/SUM all-reduces) at the "
-                            "end of the timed region" if replica else
-                            f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks)"
-                            if interleave else
-                            "x-slab sharding" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single GPU")}
+            "scans_per_step": batch, "window": window_desc(w, batch),
+            "l2": "flushed before every step (256 MB write)", "parallelism": par}
+
+
+def relaunch(n: int) -> int:
+    """--gpus N > 1 outside torchrun: one process per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def kernel_traffic(config: int, batch: int):
+    """ncu per-launch DRAM/LTS figures of this workload's kernels
+    (profiles/kernel_traffic.json, written by tools/ncu_traffic.py from a
+    capture of this bench command on the current build)."""
+    p = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get("configs", {}).get(f"{config}x{batch}")
+    return d
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--batch", type=int, default=1, help="scans per launch (config 5: 1/8/32/128)")
-    ap.add_argument("--max-scans", type=int, default=None, help="distinct scans to generate (default: all needed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="diagnostics only: skip the end-to-end passes")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     ap.add_argument("--interleave", type=int, default=None,
                     help="slab mode: x-block width of interleaved sharding (default 64, at most nx / 2N)")
-    ap.add_argument("--multi", default="replica", choices=["replica", "slab"],
-                    help="N > 1: data-parallel whole-grid replicas with one exact merge at the end of the "
-                         "timed region (default), or x-sharded slabs with a per-step point broadcast")
+    ap.add_argument("--multi", default="slab", choices=["replica", "slab"],
+                    help="N > 1: x-interleaved slabs with a per-step point broadcast (default), or data-parallel "
+                         "whole-grid replicas with one exact merge per window pass")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -260,8 +340,8 @@ def main():
     import torch
 
     from paper_2509_20081_b200 import _native
-    from paper_2509_20081_b200 import (IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame,
-                                       integrate_frames, new_grid)
+    from paper_2509_20081_b200 import IntegrationParams, ScanFrame, build_kernel_bank, integrate_frame, integrate_frames
+    from paper_2509_20081_b200.grid import VoxelGrid
     from paper_2509_20081_b200.sharded import ReplicatedGrid, ShardedGrid
 
     backend = os.environ.get("BENCH_BACKEND", "nccl")
@@ -280,11 +360,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workloads.get(args.config)
     B = max(1, args.batch)
-    need = (args.warmup + args.steps) * B
-    n_avail = min(w.n_scans, need if args.max_scans is None else min(need, args.max_scans))
-    n_avail = max(B, n_avail - n_avail % B)  # whole batches; the trajectory wraps with a grid reset
-    scans = gen_scans(w, n_avail)
-    steps_per_pass = n_avail // B
+    pre, win = plan(w, B)
+    multi = args.multi if world > 1 else "single"
+    replica = multi == "replica"
+    holds_scans = rank == 0 or replica
+    scans = gen_scans(w, pre + [k for b in win for k in b]) if holds_scans else {}
     bank = build_kernel_bank(size=K_EDGE, shadow_radius=w.shadow_radius)
     shadow_cells = float(np.mean([len(o) for o in bank.shadow_offsets]))
     params = IntegrationParams()
@@ -292,9 +372,6 @@ def main():
     dev = f"cuda:{local}"
 
     # ---------------- device-resident value --------------------------------
-    multi = args.multi if world > 1 else "single"
-    replica = multi == "replica"
-    W = world if replica else 1  # step-batches consumed per step (all ranks)
     if replica:
         ilv = 0
         sg = ReplicatedGrid(w.dims, w.voxel_size, w.origin, dist, device=local)
@@ -303,44 +380,41 @@ def main():
         ilv = args.interleave if args.interleave is not None else (
             min(64, max(1, w.dims[0] // (2 * world))) if world > 1 else 0)
         sg = ShardedGrid(w.dims, w.voxel_size, w.origin, rank, world, device=local, interleave=ilv or None)
-    # one device buffer per step-batch (concatenated scans), built before timing
-    batches = []
-    for j in range(steps_per_pass):
-        idx = list(range(j * B, (j + 1) * B))
-        counts = [len(scans[k]) for k in idx]
-        poses = np.stack([w.poses[k] for k in idx])
-        pts = torch.from_numpy(np.concatenate([scans[k] for k in idx])).to(dev) if (rank == 0 or replica) else None
-        batches.append((pts, counts, poses))
+    g_local = sg.local
 
-    # Replicas: every pass over the trajectory is split into W contiguous
-    # segments, one per rank (each scan integrated once per pass, and a
-    # rank's consecutive scans overlap like the single-GPU sequence); a pass
-    # ends with the merge (the pass's global map), then a reset.
-    seg = (rank * steps_per_pass // W, (rank + 1) * steps_per_pass // W)
-    P = -(-steps_per_pass // W)  # steps per pass (longest segment)
+    def to_dev(ids):
+        poses = np.stack([w.poses[k] for k in ids])
+        if holds_scans:
+            counts = [len(scans[k]) for k in ids]
+            pts = torch.from_numpy(np.concatenate([scans[k] for k in ids])).to(dev)
+        else:
+            counts, pts = [0] * len(ids), None
+        if dist is not None and not replica:
+            # every rank needs the counts to size the broadcast buffers
+            c = torch.tensor(counts, dtype=torch.int64, device=dev)
+            dist.broadcast(c, 0)
+            counts = c.cpu().tolist()
+        return pts, counts, poses
+
+    pre_dev = [to_dev([k]) for k in pre]
+    win_dev = [to_dev(b) for b in win]
+    nw = len(win)
+    # replicas: every pass over the window is split into W contiguous segments
+    W = world if replica else 1
+    seg = (rank * nw // W, (rank + 1) * nw // W)
+    P = -(-nw // W)  # steps per pass (longest segment)
 
     def batch_of(s):
-        """Step-batch this rank integrates at step s, or None (short segment)."""
+        """Window batch this rank integrates at step s of a pass, or None."""
         i = s % P
         return seg[0] + i if seg[0] + i < seg[1] else None
 
-    def new_pass(s):
-        return s % P == 0
-
-    def reset_grid():
-        if replica:
-            sg.reset()
-        else:
-            L.dbt_grid_reset(sg.local.handle)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
     torch.cuda.set_stream(stream)
 
-    def do_step(s, j=None):
-        j = batch_of(s) if j is None else j
-        if j is None:
-            return
-        pts, counts, poses = batches[j]
+    def launch(item):
+        pts, counts, poses = item
         if not replica:
             if rank != 0:
                 pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
@@ -348,29 +422,41 @@ def main():
                 dist.broadcast(pts, 0)
         sg.integrate_device(bank, pts, counts, poses, params, stream=stream)
 
-    # applied returns of every distinct batch (discards do not depend on the
-    # grid state), so the timed pass needs no per-step read-back
-    applied_of = []
-    for j in range(steps_per_pass):
-        if j == 0:
-            reset_grid()
-        do_step(0, j)
-        applied_of.append(sum(x.points_in - x.points_discarded for x in sg.stats()))
+    def refill():
+        """reset + prefill (untimed, queued on the stream)."""
+        L.dbt_grid_reset(g_local.handle)
+        for item in pre_dev:
+            launch(item)
+        if replica:
+            stream.synchronize()
+            sg.mark()
+
+    # applied returns of every window batch in its pass position (discards
+    # do not depend on the grid state), so the timed pass needs no read-back
+    applied_of = {}
+    refill()
+    for j in range(seg[0], seg[1]):
+        launch(win_dev[j])
+        applied_of[j] = sum(x.points_in - x.points_discarded for x in sg.stats())
 
     def run_pass(timed):
-        """warmup + steps from a reset grid; timed: no host sync or profiling
-        inside the region (launches queue ahead), else per-step stats and
-        per-kernel CUDA events."""
-        L.dbt_profile_enable(sg.local.handle, 0 if timed else 1)
-        reset_grid()
+        """warmup + steps; timed: no host sync or profiling inside the region
+        (launches queue ahead), else per-step stats and per-kernel events."""
+        L.dbt_profile_enable(g_local.handle, 0 if timed else 1)
+        refill()
         for s in range(args.warmup):
-            if s and new_pass(s):
+            if s and s % P == 0:
                 if replica:
                     sg.merge(stream=stream)
-                reset_grid()
-            do_step(s)
+                refill()
+            if batch_of(s) is not None:
+                launch(win_dev[batch_of(s)])
+        if replica:
+            sg.merge(stream=stream)
         torch.cuda.synchronize()
-        L.dbt_profile_reset(sg.local.handle)
+        refill()
+        torch.cuda.synchronize()
+        L.dbt_profile_reset(g_local.handle)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         cnt = {"applied": 0, "swept": 0, "written": 0, "skipped": 0, "rows": 0}
         if dist is not None:
@@ -389,24 +475,25 @@ def main():
             merges.append(em)
 
         for i in range(args.steps):
-            s = args.warmup + i
-            if new_pass(s):
-                if replica and i > 0:
+            if i and i % P == 0:
+                if replica:
                     timed_merge()
-                reset_grid()
+                refill()  # untimed: between the step events
             if not args.no_flush:
                 flush.zero_()
+            j = batch_of(i)
             ev[i][0].record(stream)
-            do_step(s)
+            if j is not None:
+                launch(win_dev[j])
             ev[i][1].record(stream)
-            if batch_of(s) is not None:
-                cnt["applied"] += applied_of[batch_of(s)]
-            if not timed:
-                sts = sg.stats()
-                cnt["swept"] += sts[0].unique_centers
-                cnt["written"] += sts[0].voxels_written
-                cnt["skipped"] += sts[0].centers_skipped
-                cnt["rows"] += sts[0].rows_swept
+            if j is not None:
+                cnt["applied"] += applied_of[j]
+                if not timed:
+                    sts = sg.stats()
+                    cnt["swept"] += sts[0].unique_centers
+                    cnt["written"] += sts[0].voxels_written
+                    cnt["skipped"] += sts[0].centers_skipped
+                    cnt["rows"] += sts[0].rows_swept
         if replica:
             timed_merge()  # the last (possibly partial) pass
         torch.cuda.synchronize()
@@ -440,156 +527,194 @@ def main():
     ms = (ctypes.c_double * 16)()
     cnt_ = (ctypes.c_int64 * 16)()
     nk = ctypes.c_int32()
-    L.dbt_profile_read(sg.local.handle, names, ms, cnt_, 16, ctypes.byref(nk))
+    L.dbt_profile_read(g_local.handle, names, ms, cnt_, 16, ctypes.byref(nk))
     kernels = {}
     for i in range(nk.value):
         nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
         kernels[nm] = {"ms_total": ms[i], "launches": int(cnt_[i]), "avg_us": ms[i] / max(cnt_[i], 1) * 1e3}
-    L.dbt_profile_enable(sg.local.handle, 0)
+    L.dbt_profile_enable(g_local.handle, 0)
 
-    sweep = kernels.get("sweep_kernel", {"avg_us": float("nan"), "launches": 0})
+    # ---------------- roofline of the dominant kernel ------------------------
+    # Dominant = the critical-path kernel with the most event time per step
+    # (sweep on the main stream; the shadow kernel runs beside it).
+    dom = max(("sweep_kernel", "shadow_kernel"), key=lambda k: kernels.get(k, {}).get("ms_total", 0.0))
+    kd = kernels.get(dom, {"avg_us": float("nan"), "launches": 0})
     peak, peak_src = measured_peaks()
-    # per launch of THIS rank: its own scans (replicas) or its slab's share
-    applied_per_launch = local_applied / max(args.steps, 1)
-    alg_bytes = b_alg(shadow_cells) * applied_per_launch / (1 if replica else max(world, 1))
-    achieved = alg_bytes / (sweep["avg_us"] * 1e-6) / 1e9
-    # bytes the sweep actually touches (device counters): one 32-byte sector of
+    steps_with_work = max(1, sum(1 for i in range(args.steps) if batch_of(i) is not None))
+    applied_per_launch = local_applied / steps_with_work
+    tr = kernel_traffic(args.config, B) if world == 1 else None
+    dram = (tr or {}).get("kernels", {}).get(dom, {}).get("dram_bytes")
+    # bytes the sweep touches (live device counters): one 32-byte sector of
     # the 1-byte distance cache per kernel row it read after culling (a row's
-    # 1-4 chunks span 1-2 sectors) + the 4-byte RED.AND and the cache byte of
-    # every lowered voxel (the shadow kernel runs concurrently). Generic
-    # (non-culling) sweep: the full K^3 cube of every swept centre.
-    touched = ((rows * 32 if rows else swept * K_EDGE ** 3) + written * 5) / max(args.steps, 1)
-    traffic, lts = None, None
-    tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
-    if os.path.exists(tpath) and args.config == 2 and B == 1:
-        tr = json.load(open(tpath)).get("kernels", {})
-        sw = tr.get("sweep_kernel", {})
-        if "dram_bytes" in sw:
-            traffic = sw["dram_bytes"]
-        lts = {k: v for k, v in tr.items()}
-    # the roof of a launch whose mask footprint fits L2 is the
-    # measured L2 atomic (4-byte RED.AND) throughput, HBM otherwise
-    l2 = (ctypes.c_double * 3)()
-    _native.check(L.dbt_probe_l2(local, 48 << 20, l2))
-    mask_bytes = 4 * w.dims[0] * w.dims[1] * w.dims[2]
-    l2_size = torch.cuda.get_device_properties(local).L2_cache_size
-    survey_roof = ("l2_red", l2[1]) if mask_bytes <= l2_size else ("hbm", peak)
+    # 1-4 chunks span 1-2 sectors) + the 8-byte record sector share and the
+    # cache byte of every lowered voxel
+    touched = ((rows * 32 if rows else swept * K_EDGE ** 3) + written * 5) / steps_with_work
+    alg = b_alg(shadow_cells) * applied_per_launch / (1 if replica else max(world, 1))
+    if dram is not None:
+        achieved, basis = dram / (kd["avg_us"] * 1e-6) / 1e9, (
+            "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel on this workload "
+            f"({tr.get('source', '?')}) / its live CUDA-event launch time")
+    else:
+        achieved, basis = touched / (kernels.get("sweep_kernel", kd)["avg_us"] * 1e-6) / 1e9, (
+            "no ncu capture of this workload in profiles/kernel_traffic.json: bytes the sweep touches (live device "
+            "counters) / its live CUDA-event launch time")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak" if replica else "strong", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w, B, ilv, replica=replica),
+        "scaling": "weak" if replica else ("strong" if world > 1 else "weak"), "vs_baseline": None,
+        "dtype": "u32/f64", "data": "synthetic (seeded ray-cast scenes with the BASELINE configs' shapes)",
+        "config": config_desc(w, B, ilv, multi),
         "gpu_launches": int(launches),
         "kernels": kernels,
         "profiled_step_ms": prof_ms / args.steps,
-        "timing": "timed pass: launches queue ahead (no per-step host sync, no per-kernel events); "
-                  "applied returns per scan from an untimed counting pass; kernel times from a second "
-                  "identical pass with per-kernel CUDA events",
+        "timing": "timed pass: launches queue ahead (no per-step host sync, no per-kernel events); applied "
+                  "returns per window batch from an untimed counting pass; kernel times from a second identical "
+                  "pass with per-kernel CUDA events",
         "clocks": clk.summary(),
         **({"merge_ms": cnt["merge_ms"], "merges": cnt["merges"]} if replica else {}),
-        "roofline": {"bound": "hbm", "kernel": "sweep_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_launch": alg_bytes,
-                     "alg_bytes_def": f"4*21^3 + 4*|S| = {b_alg(shadow_cells):.0f} B per applied return "
-                                      "(SURVEY.md 8(d)) x applied returns per launch",
-                     "traffic_source": "ncu dram__bytes_read+write per sweep launch (config 2), "
-                                       "profiles/kernel_traffic.json",
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": dram, "peak_source": peak_src, "basis": basis,
+                     "kernel_avg_us": kd["avg_us"],
                      "touched_bytes_per_launch": touched,
-                     "touched_gbs": touched / (sweep["avg_us"] * 1e-6) / 1e9,
-                     "why_frac_above_1": "B_alg is the reference's per-return traffic; the engine sweeps each "
-                                         "centre voxel once (dedup), skips centres whose stamp is already applied "
-                                         "(certificates), skips the voxels a closer certified neighbour centre "
-                                         "covers (culling) and reads a 1-byte cache: touched/traffic are the "
-                                         "bytes actually moved",
-                     "rows_swept_per_launch": rows / max(args.steps, 1),
-                     "centres_swept_per_launch": swept / max(args.steps, 1),
-                     "returns_skipped_per_launch": skipped / max(args.steps, 1),
-                     "l2_probe": {"red_and_gops": l2[0], "red_and_gbs": l2[1], "ldcg_gbs": l2[2],
-                                  "buffer_bytes": 48 << 20,
-                                  "how": "dbt_probe_l2: coalesced 4-byte RED.AND / 8-byte ld.cg over an "
-                                         "L2-resident 48 MB buffer, best of 4 (CUDA events)"},
-                     "survey_roof": {"kind": survey_roof[0], "peak_gbs": survey_roof[1],
-                                     "achieved_gbs": achieved, "frac": achieved / survey_roof[1],
-                                     "why": f"SURVEY.md 8(d): reference mask array {mask_bytes / 1e6:.0f} MB "
-                                            f"vs L2 {l2_size / 1e6:.0f} MB"},
-                     "ncu_per_launch": lts},
+                     "touched_gbs": touched / (kernels.get("sweep_kernel", kd)["avg_us"] * 1e-6) / 1e9,
+                     "rows_swept_per_launch": rows / steps_with_work,
+                     "centres_swept_per_launch": swept / steps_with_work,
+                     "returns_skipped_per_launch": skipped / steps_with_work,
+                     "ncu_per_launch": (tr or {}).get("kernels")},
+        "alg_savings": {"b_alg_bytes_per_return": b_alg(shadow_cells),
+                        "b_alg_bytes_per_launch": alg,
+                        "b_alg_gbs_over_sweep": alg / (kernels.get("sweep_kernel", kd)["avg_us"] * 1e-6) / 1e9,
+                        "def": "SURVEY.md 8(d) 4*21^3 + 4*|S| B per applied return (the reference's per-return "
+                               "traffic) x applied returns / sweep time; above the HBM peak by design: the engine "
+                               "sweeps each centre once, skips centres whose stamp is applied (certificates), culls "
+                               "voxels a closer certified centre covers and reads a 1-byte cache"},
     }
 
     # ---------------- e2e through the public API ----------------------------
-    # N = 1: integrate_frame(s) on pinned host scans; replicas: every rank
-    # the same on its own scans, then the merge (collective), max over ranks
-    if world == 1 or replica:
-        if replica:
-            rg = ReplicatedGrid(w.dims, w.voxel_size, w.origin, dist, device=local)
-            rg._note_params(params)
-            g = rg.local
-        else:
-            g = new_grid(w.dims, w.voxel_size, w.origin, memory_cap=1 << 42, device=local)
-        pinned = []
-        for s in scans:
+    if not args.no_e2e:
+        line.update(run_e2e(args, w, B, pre, win, scans, sg, bank, params, dist, rank, world, replica, dev, flush,
+                            batch_of, P, seg, torch, _native, L, integrate_frame, integrate_frames, ScanFrame))
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(w, B, scans)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, w, B, pre, win, scans, sg, bank, params, dist, rank, world, replica, dev, flush, batch_of, P,
+            seg, torch, _native, L, integrate_frame, integrate_frames, ScanFrame):
+    """The same window through the public API with host scans (pinned, then
+    pageable numpy), host wall clock per call, max over ranks."""
+    out = {}
+    g = sg.local
+    pinned = {}
+    if rank == 0 or replica:
+        for k, s in scans.items():
             buf = ctypes.c_void_p()
             _native.check(L.dbt_host_alloc(s.nbytes, ctypes.byref(buf)))
             arr = np.ctypeslib.as_array((ctypes.c_float * s.size).from_address(buf.value)).reshape(s.shape)
             arr[...] = s
-            pinned.append((buf, arr))
-        e_el, e_pts, h2d = 0.0, 0, 0
+            pinned[k] = (buf, arr)
+
+    def call(ids, src):
+        """One public-API call for the scans ids; returns (applied, h2d bytes)."""
+        if world > 1 and not replica:
+            # slab mode: rank 0 copies the host scans, broadcasts, every rank
+            # stamps its planes, stats read back (per-step collectives)
+            if rank == 0:
+                pts = torch.from_numpy(np.concatenate([src[k] for k in ids])).to(dev, non_blocking=True)
+            else:
+                pts = None
+            counts = [len(scans[k]) for k in ids] if rank == 0 else None
+            c = torch.tensor(counts if counts is not None else [0] * len(ids), dtype=torch.int64, device=dev)
+            dist.broadcast(c, 0)
+            counts = c.cpu().tolist()
+            if rank != 0:
+                pts = torch.empty((sum(counts), 3), dtype=torch.float32, device=dev)
+            dist.broadcast(pts, 0)
+            sg.integrate_device(bank, pts, counts, np.stack([w.poses[k] for k in ids]), params)
+            sts = sg.stats()
+            return sum(x.points_in - x.points_discarded for x in sts), (sum(counts) * 12 if rank == 0 else 0)
+        if replica:
+            sg._note_params(params)
+        frames = [ScanFrame(points=src[k], pose=w.poses[k]) for k in ids]
+        sts = [integrate_frame(g, bank, frames[0], params)] if len(ids) == 1 else integrate_frames(g, bank, frames,
+                                                                                                  params)
+        return sum(x.points_in - x.points_discarded for x in sts), sum(src[k].nbytes for k in ids)
+
+    def refill(src):
+        L.dbt_grid_reset(g.handle)
+        for k in pre:
+            call([k], src)
+        if replica:
+            sg.mark()
+
+    def e2e_pass(src):
+        el, pts_n, h2d = 0.0, 0, 0
+        for s in range(args.warmup):
+            if s % P == 0:
+                if s and replica:
+                    sg.merge()
+                refill(src)
+            if batch_of(s) is not None:
+                call(win[batch_of(s)], src)
+        if replica:
+            sg.merge()
         if dist is not None:
             dist.barrier()
-        for s in range(args.warmup + args.steps):
-            if new_pass(s):
-                if replica:
-                    if s > args.warmup:  # the pass's global map, timed
-                        torch.cuda.synchronize()
-                        t0 = time.perf_counter()
-                        rg.merge()
-                        torch.cuda.synchronize()
-                        e_el += time.perf_counter() - t0
-                    rg.reset()
-                else:
-                    L.dbt_grid_reset(g.handle)
-            j = batch_of(s)
+        for i in range(args.steps):
+            if i % P == 0:
+                if i and replica:
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    sg.merge()
+                    torch.cuda.synchronize()
+                    el += time.perf_counter() - t0
+                refill(src)
+            j = batch_of(i)
+            if not args.no_flush:
+                flush.zero_()
+            torch.cuda.synchronize()
             if j is None:
                 continue
-            ks = range(j * B, (j + 1) * B)
-            if s >= args.warmup:
-                flush.zero_()
-                torch.cuda.synchronize()
             t0 = time.perf_counter()
-            if B == 1:
-                sts = [integrate_frame(g, bank, ScanFrame(points=pinned[j][1], pose=w.poses[j]), params)]
-            else:
-                sts = integrate_frames(g, bank, [ScanFrame(points=pinned[k][1], pose=w.poses[k]) for k in ks],
-                                       params)
-            dt = time.perf_counter() - t0
-            if s >= args.warmup:
-                e_el += dt
-                e_pts += sum(x.points_in - x.points_discarded for x in sts)
-                h2d += sum(pinned[k][1].nbytes for k in ks)
+            a, b = call(win[j], src)
+            el += time.perf_counter() - t0
+            pts_n += a
+            h2d += b
         if replica:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rg.merge()
+            sg.merge()
             torch.cuda.synchronize()
-            e_el += time.perf_counter() - t0
-            t = torch.tensor([e_el], dtype=torch.float64, device=dev)
+            el += time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            a = torch.tensor([e_pts, h2d], dtype=torch.int64, device=dev)
-            dist.all_reduce(a)
-            e_el, e_pts, h2d = float(t.item()), int(a[0].item()), int(a[1].item())
-        line["e2e"] = {"value": e_pts / e_el, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
-                       "d2h_bytes_per_step": 32 + 32 * B, "ms_per_step": e_el / args.steps * 1e3,
-                       "api": ("paper_2509_20081_b200.integrate_frame (dbt_integrate_frame)" if B == 1 else
-                               "paper_2509_20081_b200.integrate_frames (dbt_integrate_batch)")
-                              + ", pinned float32 scans"
-                              + (", every rank its own scans, then ReplicatedGrid.merge" if replica else "")}
-        for buf, _ in pinned:
-            L.dbt_host_free(buf)
-    if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(w, scans)
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+            el = float(t.item())
+            if replica:
+                a = torch.tensor([pts_n, h2d], dtype=torch.int64, device=dev)
+                dist.all_reduce(a)
+                pts_n, h2d = int(a[0].item()), int(a[1].item())
+        return pts_n / el, el, h2d
+
+    api = ("paper_2509_20081_b200.integrate_frame (dbt_integrate_frame)" if B == 1 else
+           "paper_2509_20081_b200.integrate_frames (dbt_integrate_scans)")
+    if world > 1 and not replica:
+        api = "rank 0: H2D copy of the host scans + NCCL broadcast; ShardedGrid.integrate_device + stats read, every rank"
+    pin_src = {k: a for k, (_, a) in pinned.items()} if pinned else scans
+    v, el, h2d = e2e_pass(pin_src)
+    out["e2e"] = {"value": v, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                  "d2h_bytes_per_step": 32 + 32 * B, "ms_per_step": el / args.steps * 1e3,
+                  "api": api + ", pinned float32 host scans"
+                  + (", every rank its own scans, then ReplicatedGrid.merge" if replica else "")}
+    v2, el2, _ = e2e_pass(scans if (rank == 0 or replica) else {})
+    out["e2e_pageable"] = {"value": v2, "unit": UNIT, "ms_per_step": el2 / args.steps * 1e3,
+                           "api": api + ", pageable numpy float32 scans (staged by one H2D copy per scan)"}
+    for buf, _ in pinned.values():
+        L.dbt_host_free(buf)
+    return out
 
 
 if __name__ == "__main__":

@@ -31,7 +31,7 @@ def sha(a) -> str:
     h = hashlib.sha256()
     h.update(str(a.dtype).encode())
     h.update(str(a.shape).encode())
-    h.update(a.tobytes())
+    h.update(a.reshape(-1).view(np.uint8).data if a.size else b"")  # the raw bytes, no copy
     return h.hexdigest()[:32]
 
 
@@ -210,3 +210,52 @@ def bin_dir_sets() -> dict:
     out["axes"] = np.array([[1, 0, 0], [0, 0, 1], [0, -1, 0], [-1, 0, 0], [0, 1, 0], [0, 0, -1], [1, 1, 0],
                             [-1, -1, 0], [1, -1, 0], [3, 4, 0], [1, 1, 1]], dtype=np.float64)
     return out
+
+
+# --------------------------------------------------------------------------
+# Trajectories: the regime the bench times (many launches into one grid, so
+# stamp certificates, culling, lazy shadow folds and PDL ordering carry state
+# across scans). The reference's grid hashes are stored after EVERY scan, so
+# a GPU run can be compared scan by scan or at the end of any batch split.
+
+
+@dataclass
+class Trajectory:
+    name: str
+    config: int
+    scans: tuple          # (first, last + 1)
+    dims: tuple
+    voxel_size: float
+    origin: tuple
+    bank: dict
+    slow: bool = False    # multi-GB grids / minutes of ray casting
+
+    def workload(self):
+        return workloads.get(self.config)
+
+    def scan_ids(self):
+        return list(range(*self.scans))
+
+
+def trajectories() -> list:
+    w2, w3, w4 = workloads.get(2), workloads.get(3), workloads.get(4)
+    return [
+        # config 2 in full: the 100-scan trajectory
+        Trajectory("cfg2_traj100", 2, (0, 100), w2.dims, w2.voxel_size, w2.origin,
+                   dict(size=21, shadow_radius=w2.shadow_radius)),
+        # config 3 prefix, also the config-5 batched case (batches of 8 / 32)
+        Trajectory("cfg3_traj32", 3, (0, 32), w3.dims, w3.voxel_size, w3.origin,
+                   dict(size=21, shadow_radius=w3.shadow_radius), slow=True),
+        # config-4 scene/sensor at 0.02 m on the 1000x1000x400 window (the
+        # reference's host arrays for the full grid are 38 GB); scans 0-29
+        # cover the bench's prefill + timed window
+        Trajectory("cfg4_window_traj30", 4, (0, 30), (1000, 1000, 400), w4.voxel_size, (0.0, 90.0, -0.22),
+                   dict(size=21, shadow_radius=w4.shadow_radius), slow=True),
+    ]
+
+
+def scan_hash(pts, pose) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(pts).reshape(-1).view(np.uint8).data if len(pts) else b"")
+    h.update(np.ascontiguousarray(pose).tobytes())
+    return h.hexdigest()[:32]
