@@ -394,6 +394,7 @@ int dbt_grid_reset(dbt_grid* g) {
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
+  g->base_valid = false;  // replica base: the records were rewritten (dbt_replica_mark again)
   return DBT_OK;
 }
 
@@ -628,6 +629,7 @@ int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, con
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
+  g->base_valid = false;  // replica base: the records were rewritten
   return DBT_OK;
 }
 

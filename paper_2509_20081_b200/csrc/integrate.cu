@@ -905,7 +905,9 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
           const uint32_t lt = b < 4 ? lt0 : lt1;
           if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
           const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
+#ifndef DBT_DIAG_NO_RED
           atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
+#endif
           ++changed;
         }
         // the chunk's cache word in one store: lowered bytes take d (the
@@ -913,9 +915,11 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
         // A concurrent lowering overwritten here only leaves its byte
         // stale-high (>= the record's bit length): a redundant AND later.
         const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
+#ifndef DBT_DIAG_NO_CACHE_STORE
         *reinterpret_cast<uint2*>(a.dist + off) =
             make_uint2((w[r][j].x & ~bm0) | ((d8[r][j].x - 0x01010101u) & bm0),
                        (w[r][j].y & ~bm1) | ((d8[r][j].y - 0x01010101u) & bm1));
+#endif
       }
     }
 }
@@ -1128,6 +1132,14 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   const int ds = d_map_sensor ? 1 : p->downsample;
   if (g->nx * g->ny * g->nz >= (1ll << 40))
     return set_error(DBT_ERR_CONFIG, "grid has 2^40 voxels or more (hash key width)");
+  if (g->last_st != st) {
+    // the per-grid scratch (counters, work list, hash, rays) may still be in
+    // use by a launch on another stream: order behind it. A device-wide sync
+    // (rare: only when the caller switches streams) rather than an event on
+    // the old stream, which the caller may have destroyed meanwhile.
+    DBT_CUDA(cudaDeviceSynchronize());
+    g->last_st = st;
+  }
   g->last_points_in.assign(S, 0);
   int64_t n = 0;
   for (int s = 0; s < S; ++s) {
@@ -1293,7 +1305,11 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   DBT_CHECK_LAUNCH("prep_kernel");
 
   bool joined = false;
+#ifdef DBT_DIAG_NO_SHADOW
+  if (false) {
+#else
   if (b->max_shadow > 0 && !fuse_shadow) {
+#endif
     ShadowArgs sa;
     sa.cells = g->cells;
     sa.center = g->d_center;

@@ -18,6 +18,9 @@
 // the caller decides; x == 0 or y == 0 is handled exactly like SVML's vector
 // special path. asin is restated for |x| <= 1 (the reference clips to
 // [-1, 1]).
+//
+// License: the restated routines are BSD-3 (Intel SVML via numpy); see
+// NOTICE.svml next to this file.
 #pragma once
 
 #include <stdint.h>

@@ -218,8 +218,10 @@ def integrate_points(grid: VoxelGrid, bank: KernelBank, p_map, sensor_pos, param
 
 def integrate_frame(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: IntegrationParams,
                     threads: int = 1) -> FrameStats:
-    """Fuse one scan (integrator.py:207-287): one H2D copy of the points, the
-    device launch sequence, one D2H copy of the counters."""
+    """Fuse one scan (integrator.py:207-287): the points cross the host link
+    once (pinned scans are read zero-copy by the preprocessing kernel,
+    pageable ones staged by one H2D copy), then the device launch sequence
+    and one D2H copy of the counters."""
     t0 = time.perf_counter()
     if scan.n_points == 0:
         return FrameStats()

@@ -6,11 +6,12 @@ cell in C order; float64 vertices with the reference's operation order). The
 work runs in libdbtsdf.so (csrc/mesh.cu) on the grid's device; only the
 finished arrays cross PCIe.
 
-The marching-cubes lookup tables are an input, not part of this package: they
-are read from the reference's own ``bitsdf._mc_tables`` (the package this one
-replaces), from an ``.npz`` named by ``$DBT_MC_TABLES``, or from any mapping /
-module passed as ``tables=`` holding EDGE_TABLE, TRI_TABLE, CORNER_OFFSETS,
-EDGE_BASE and EDGE_AXIS (_mc_tables.py:9-324).
+The marching-cubes lookup tables ship with the package
+(``data/mc_tables.npz``, the classic edge / triangle tables in the layout of
+_mc_tables.py:9-324); the engine takes them as an input, so an ``.npz`` named
+by ``$DBT_MC_TABLES`` or any mapping / module passed as ``tables=`` holding
+EDGE_TABLE, TRI_TABLE, CORNER_OFFSETS, EDGE_BASE and EDGE_AXIS replaces them.
+The reference package is not needed.
 """
 
 from __future__ import annotations
@@ -55,18 +56,16 @@ def empty_mesh() -> TriangleMesh:
     return TriangleMesh(vertices=np.zeros((0, 3)), triangles=np.zeros((0, 3), dtype=np.int64))
 
 
+_PKG_TABLES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "mc_tables.npz")
+
+
 def _table_source(source):
+    """Default: the tables shipped with the package (data/mc_tables.npz: the
+    classic Lorensen-Cline / Bourke marching-cubes edge and triangle tables in
+    the order the reference's _mc_tables.py:9-324 lists them, with its corner
+    and edge numbering); $DBT_MC_TABLES or tables= override them."""
     if source is None:
-        path = os.environ.get("DBT_MC_TABLES")
-        if path:
-            return np.load(path)
-        try:
-            from bitsdf import _mc_tables as ref_tables  # the reference package being replaced
-        except ImportError as e:
-            raise ConfigurationError(
-                "marching-cubes tables not found: pass tables=, set DBT_MC_TABLES to an .npz, or install the "
-                "reference bitsdf package (its _mc_tables module)") from e
-        return ref_tables
+        return np.load(os.environ.get("DBT_MC_TABLES") or _PKG_TABLES)
     if isinstance(source, (str, os.PathLike)):
         return np.load(source)
     return source

@@ -102,6 +102,20 @@ def reduce_stats(stats: list, dist, group=None, device=None) -> list:
     return out
 
 
+def _launch_device(grid: VoxelGrid, bank: KernelBank, points, dtype, counts, poses, prm, stream):
+    """dbt_integrate_device on ``grid`` (asynchronous on ``stream``). A host
+    mirror the caller may have written is uploaded first; afterwards it is
+    dropped (it would be stale, and a later push_host would overwrite the
+    device integration with it): the next read of grid.mask/sign/hits
+    downloads the current grid."""
+    grid.push_host()
+    grid._host = None
+    _native.check(_native.lib().dbt_integrate_device(
+        grid.handle, bank.device_handle(grid.device), ctypes.c_void_p(points.data_ptr()), dtype,
+        counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
+        ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream)))
+
+
 class ShardedGrid:
     """This rank's share of a globally-sized grid, device resident: the
     contiguous slab ``slab_bounds`` gives, or (interleave=width) the x-blocks
@@ -137,11 +151,7 @@ class ShardedGrid:
         st = torch.cuda.current_stream() if stream is None else stream
         prm = params.native()
         self._last_scans = len(counts)
-        _native.check(_native.lib().dbt_integrate_device(
-            self.local.handle, bank.device_handle(self.local.device), ctypes.c_void_p(points.data_ptr()), dtype,
-            counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
-            ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm),
-            ctypes.c_void_p(st.cuda_stream)))
+        _launch_device(self.local, bank, points, dtype, counts, poses, prm, st)
 
     def stats(self) -> list:
         out = (_native.Stats * self._last_scans)()
@@ -199,10 +209,7 @@ class ReplicatedGrid:
         st = torch.cuda.current_stream() if stream is None else stream
         prm = params.native()
         self._last_scans = len(counts)
-        _native.check(_native.lib().dbt_integrate_device(
-            self.local.handle, bank.device_handle(self.local.device), ctypes.c_void_p(points.data_ptr()), dtype,
-            counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(counts),
-            ctypes.c_void_p(poses.ctypes.data), ctypes.byref(prm), ctypes.c_void_p(st.cuda_stream)))
+        _launch_device(self.local, bank, points, dtype, counts, poses, prm, st)
 
     def integrate_frame(self, bank: KernelBank, scan, params: IntegrationParams) -> FrameStats:
         """integrate_frame on this rank's replica (synchronous; local stats)."""
@@ -215,6 +222,25 @@ class ReplicatedGrid:
         out = (_native.Stats * self._last_scans)()
         _native.check(_native.lib().dbt_stats_read(self.local.handle, out, self._last_scans))
         return [FrameStats.from_native(out[i]) for i in range(self._last_scans)]
+
+    def _agreed_params(self, dev):
+        """(h_max, t_occ) every rank that integrated since the last merge used
+        (collective). Ranks without scans take them from the others, so all
+        replicas fold the hit deltas identically; disagreement raises on
+        every rank."""
+        import torch
+
+        have = self._params is not None
+        h, t = self._params if have else (0, 0)
+        v = torch.tensor([h if have else 1 << 20, t if have else 1 << 20, -h if have else 1 << 20,
+                          -t if have else 1 << 20], dtype=torch.int64, device=dev)
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN, group=self.group)
+        lo_h, lo_t, hi_h, hi_t = (int(x) for x in v.tolist())
+        if lo_h == 1 << 20:  # no rank integrated: no deltas to fold
+            return 255, 2
+        if (lo_h, lo_t) != (-hi_h, -hi_t):
+            raise ConfigurationError("replica scans between two merges must share h_max and t_occ across ranks")
+        return lo_h, lo_t
 
     def merge(self, stream=None):
         """All ranks: combine the replicas (collective). Returns when the
@@ -238,7 +264,7 @@ class ReplicatedGrid:
             self.dist.all_reduce(mk, op=self.dist.ReduceOp.MIN, group=self.group)
             self.dist.all_reduce(sg, op=self.dist.ReduceOp.MIN, group=self.group)
             self.dist.all_reduce(dl, op=self.dist.ReduceOp.SUM, group=self.group)
-        h_max, t_occ = self._params if self._params is not None else (255, 2)
+        h_max, t_occ = self._agreed_params(dev)
         _native.check(L.dbt_replica_apply(self.local.handle, ctypes.c_void_p(mk.data_ptr()),
                                           ctypes.c_void_p(sg.data_ptr()), ctypes.c_void_p(dl.data_ptr()),
                                           int(h_max), int(t_occ), ctypes.c_void_p(st.cuda_stream)))

@@ -301,3 +301,15 @@ class TestDeviceMesh:
             t[key].ravel()[5] = val
             with pytest.raises(ConfigurationError):
                 extract_mesh(g, 0.0, tables=t)
+
+
+def test_packaged_tables_equal_the_reference_tables():
+    """The tables shipped in the package are the ones the reference meshes
+    were pinned with (tests/golden/mc_tables.npz, written from the
+    reference's _mc_tables by make_golden.py --only-mesh)."""
+    from paper_2509_20081_b200.mesher import _PKG_TABLES
+
+    a, b = np.load(_PKG_TABLES), np.load(TABLES)
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k

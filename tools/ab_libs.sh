@@ -12,8 +12,9 @@ for r in $(seq "$rounds"); do
 import json, sys
 try:
     d = json.loads(sys.argv[2])
-    print(f"{sys.argv[1]:40s} value {d['value'] / 1e6:8.1f}  e2e {d['e2e']['value'] / 1e6:7.1f}  step {d['ms_per_step'] * 1e3:6.1f} us "
-          f"e2e step {d['e2e']['ms_per_step'] * 1e3:6.1f} us  " + " ".join(f"{k} {v['avg_us']:.1f}" for k, v in d['kernels'].items()))
+    e = d.get('e2e', {'value': float('nan'), 'ms_per_step': float('nan')})
+    print(f"{sys.argv[1]:32s} value {d['value'] / 1e6:8.1f}  e2e {e['value'] / 1e6:7.1f}  step {d['ms_per_step'] * 1e3:6.1f} us "
+          f"e2e step {e['ms_per_step'] * 1e3:6.1f} us  " + " ".join(f"{k} {v['avg_us']:.1f}" for k, v in d['kernels'].items()), flush=True)
 except Exception as e:
     print(sys.argv[1], "failed", e, sys.argv[2][:200])
 PY
