@@ -27,7 +27,8 @@
 // AND) but never below the record: no update is ever lost.
 //
 // Stamp certificates: one bit per voxel, set when the full K^3 stamp centred
-// at that voxel is in the grid or claimed by a return of the running launch;
+// at that voxel (on a sharded grid: the part of it on this part's planes) is
+// in the grid or claimed by a return of the running launch;
 // the AND being idempotent, a later return centred there needs no sweep (its
 // shadow update still runs). Returns claim the bit with one atomicOr in
 // preprocessing. Cleared on reset/upload and when a launch uses a different
@@ -105,6 +106,19 @@ struct XMap {
     if (blk % p != r) return -1;
     return (blk / p) * w + (u - blk * w);
   }
+  // some owned plane lies in [lo, hi] (a return's K^3 cube [cx-R, cx+R]
+  // touches this part)
+  __host__ __device__ __forceinline__ bool touches(int64_t lo, int64_t hi) const {
+    lo = lo < x0 ? x0 : lo;
+    hi = hi >= x1 ? x1 - 1 : hi;
+    if (lo > hi) return false;
+    if (w == 0) return true;
+    const int64_t b0 = (lo - x0) / w, b1 = (hi - x0) / w;
+    if (b1 - b0 + 1 >= p) return true;
+    for (int64_t b = b0; b <= b1; ++b)
+      if (b % p == r) return true;
+    return false;
+  }
   __host__ int64_t planes() const {
     if (w == 0) return x1 - x0;
     int64_t n = 0;
@@ -166,7 +180,11 @@ struct dbt_grid {
   double vs = 0, org[3] = {0, 0, 0};
   uint2* cells = nullptr;                   // authoritative voxel records
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
-  uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel
+  uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel of the GLOBAL grid
+                                            // (index (x*ny + y)*nzp + z, x global): a part of a sharded
+                                            // grid certifies every centre whose cube touches its planes
+  int64_t n_cert = 0;                       // nx*ny*nzp certificate bits
+  uint32_t* diag_mask = nullptr;            // DBT_DIAG_RED_SPLIT builds only (A/B of a 4-byte mask array)
   uint32_t* d_exact_bits = nullptr;         // centre + touched + centre-row bitmaps (exact.cu), lazily
   uint32_t* d_exact_m0 = nullptr;           // pre-launch masks of touched cells (exact.cu)
   uint8_t* d_base_hits = nullptr;           // replica mode: hits at the last merge (replica.cu)

@@ -233,7 +233,7 @@ int finish_host_write(dbt_grid* g) {
   g->base_valid = false;  // replica base: host data replaced the records
   rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
-  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
   g->base_valid = false;
@@ -271,6 +271,7 @@ static int create_grid(const int64_t dims[3], double voxel_size, const double or
   g->vs = voxel_size;
   for (int i = 0; i < 3; ++i) g->org[i] = origin[i];
   g->n_cells = g->lx * g->ny * g->nzp;
+  g->n_cert = g->nx * g->ny * g->nzp;
   int rc = grid_set_device(g);
   if (rc) {
     delete g;
@@ -280,7 +281,11 @@ static int create_grid(const int64_t dims[3], double voxel_size, const double or
   // cells past the last row of the slab (never written).
   cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint2));
   if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
-  if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cells + 63) / 32) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cert + 63) / 32) * 4);
+#ifdef DBT_DIAG_RED_SPLIT
+  if (e == cudaSuccess) e = cudaMalloc(&g->diag_mask, (size_t)(g->n_cells + 64) * 4);
+  if (e == cudaSuccess) e = cudaMemset(g->diag_mask, 0xFF, (size_t)(g->n_cells + 64) * 4);
+#endif
   if (e != cudaSuccess) {
     if (g->cells) cudaFree(g->cells);
     delete g;
@@ -391,7 +396,7 @@ int dbt_grid_reset(dbt_grid* g) {
   g->pend = false;
   DBT_CHECK_LAUNCH("fill_cells_kernel");
   DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
-  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
   g->base_valid = false;  // replica base: the records were rewritten (dbt_replica_mark again)
@@ -405,7 +410,7 @@ int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* 
   dims[2] = g->nz;
   slab[0] = g->x0;
   slab[1] = g->x1;
-  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint2) + 1) + (g->n_cells + 63) / 32 * 4;
+  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint2) + 1) + (g->n_cert + 63) / 32 * 4;
   return DBT_OK;
 }
 
@@ -626,7 +631,7 @@ int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, con
         g->cells, g->dist, plane, g->nzp, z_begin, z_end);
     DBT_CHECK_LAUNCH("rebuild_dist_range_kernel");
   }
-  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, g->stream));
+  DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
   g->base_valid = false;  // replica base: the records were rewritten

@@ -94,6 +94,9 @@ struct PrepArgs {
 };
 
 constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
+// packed-centre flag (bit 63, above the 3 x 21 coordinate bits): the return
+// is applied but its cube misses this part's planes (sharded grids)
+constexpr uint64_t kRemote = 1ull << 63;
 constexpr int kEpochShift = 52;
 constexpr uint32_t kMaxEpoch = 4095;
 
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   int ok = 0, fallback = 0;
   bool append = false;  // this lane owns a new sweep work item (unique centre)
   bool claimed = false; // centre stamp already applied / claimed: no sweep
+  bool relevant = false; // the return's cube touches this part's planes
   uint64_t packed = kEmptyKey;
   if (live) {
     double m0, m1, m2, t0, t1, t2;
@@ -262,20 +266,19 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         a.ray[3 * i + 2] = rz;
       }
       packed = pack_center(cx, cy, cz);
-      if (a.claim) {
+      // a part of a sharded grid ignores returns whose cube misses its planes
+      // (still counted; the first-return choice below stays global)
+      relevant = a.xm.touches(cx - a.R, cx + a.R);
+      if (a.claim && relevant) {
         // claim the stamp certificate of the centre (one atomicOr): a bit
         // already set means the stamp is in the grid from an earlier launch
         // or owned by an earlier return of this launch; either way no sweep.
-        // A centre outside this rank's slab has no bit here: always swept.
-        const int64_t lcx = a.xm.local(cx);
-        if (lcx >= 0) {
-          const int64_t cidx = (lcx * a.ny + cy) * a.nzp + cz;
-          const uint32_t bit = 1u << (cidx & 31);
-          claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
-          append = !claimed;
-        } else {
-          append = true;
-        }
+        // Certificates are indexed by the global centre (a part certifies
+        // the centres whose cube touches its planes).
+        const int64_t cidx = (cx * a.ny + cy) * a.nzp + cz;
+        const uint32_t bit = 1u << (cidx & 31);
+        claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
+        append = !claimed;
       }
       // the hash table dedups centres for the sweep when certificates are not
       // used (measurement flags) and picks the first return per centre for
@@ -302,7 +305,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         h = (h + 1) & a.hmask;
         cur = __ldcg(&a.hkey[h]);
       }
-      if (a.fuse_shadow) {
+      append = append && relevant;
+      if (a.fuse_shadow && relevant) {
         // up to 8 shadow cells, their visits counted independently
         const int b0 = a.sstart[ba * a.b_el + be], nsh = a.sstart[ba * a.b_el + be + 1] - b0;
 #pragma unroll
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       }
       if (a.first_return) atomicMin(&a.hmin[h], (uint32_t)i);
       a.slot[i] = (uint32_t)h;
+      if (!relevant) packed |= kRemote;  // the shadow kernel counts it, visits nothing
     }
     a.center[i] = packed;
     if (a.outcome) a.outcome[i] = ok ? 1 : 0;
@@ -428,6 +433,7 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
         if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&a.sc[s].n_applied, (unsigned long long)__popc(grp));
       }
     }
+    if (c & kRemote) continue;
     int b = a.bin[i];
     int st = a.sstart[b];
     if (k >= a.sstart[b + 1] - st) continue;
@@ -469,6 +475,7 @@ __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
         }
       }
       uint16_t bin = 0;
+      if (c != kEmptyKey && (c & kRemote)) c = kEmptyKey;  // counted above; no visits here
       if (c != kEmptyKey) {
         const double rx = a.ray[3 * i], ry = a.ray[3 * i + 1], rz = a.ray[3 * i + 2];
         int ba, be, fb;
@@ -639,6 +646,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 // over the block instead of serialising one warp.
 struct CullArgs {
   uint2* cells;
+  uint32_t* dmask;  // DBT_DIAG_RED_SPLIT
   uint8_t* dist;
   const uint64_t* uniq;
   LaunchCounters* lc;
@@ -646,7 +654,7 @@ struct CullArgs {
   const uint16_t* rowd;  // [K*K] distinct id * CH
   const uint32_t* stamped;
   int K, R, nd, CH;
-  int64_t x0, x1, ny, nzp;
+  int64_t x0, x1, nx, ny, nzp;
   XMap xm;
 };
 
@@ -682,9 +690,9 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
   uint32_t nb3 = 0;
   if (lane < 9) {
     const int na = lane / 3 - 1, nbb = lane % 3 - 1;
-    const int64_t lgx = a.xm.local(cx + na);
-    if (lgx >= 0) {
-      const int64_t idx = (lgx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
+    const int64_t gx = cx + na;  // certificates: global planes (boundary discard keeps it in the grid)
+    {
+      const int64_t idx = (gx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
       const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
       const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
       nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
@@ -702,15 +710,13 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     const int j = (lane - 9) & 7, k = 2 + (j & 3), sg = j < 4 ? 1 : -1;
     const bool along_x = lane < 17;
     const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
-    const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(qx) : -1;
-    if (lq >= 0) {
-      const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+    if (qy >= 0 && qy < a.ny && qx >= 0 && qx < a.nx) {
+      const int64_t idx = (qx * a.ny + qy) * a.nzp + cz;
       ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
     }
   } else if (lane == 25 && cz >= 5 && cz + 5 < a.nzp) {  // padding bits are never set
-    const int64_t lq = a.xm.local(cx);
-    if (lq >= 0) {
-      const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 5);
+    {
+      const int64_t idx = (cx * a.ny + cy) * a.nzp + (cz - 5);
       const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
       const uint32_t w1 = ((idx & 31) > 21) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
       const uint32_t b11 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7FFu;  // bit i: cz - 5 + i
@@ -736,17 +742,16 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     if (lane < 12) {
       const int g = lane >> 2, sa = (lane & 2) ? -1 : 1, sb = (lane & 1) ? -1 : 1;
       const int pa = sa * (g == 1 ? 1 : 2), pb = sb * (g == 0 ? 1 : 2);
-      const int64_t qy = cy + pb;
-      const int64_t lq = qy >= 0 && qy < a.ny ? a.xm.local(cx + pa) : -1;
-      if (lq >= 0) {
-        const int64_t idx = (lq * a.ny + qy) * a.nzp + cz;
+      const int64_t qy = cy + pb, qx = cx + pa;
+      if (qy >= 0 && qy < a.ny && qx >= 0 && qx < a.nx) {
+        const int64_t idx = (qx * a.ny + qy) * a.nzp + cz;
         plb = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
       }
     } else if (lane < 16 && cz >= 2 && cz + 2 < a.nzp) {
       const int pa = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
-      const int64_t lq = a.xm.local(cx + pa);
-      if (lq >= 0) {
-        const int64_t idx = (lq * a.ny + cy) * a.nzp + (cz - 2);
+      const int64_t qx = cx + pa;
+      if (qx >= 0 && qx < a.nx) {
+        const int64_t idx = (qx * a.ny + cy) * a.nzp + (cz - 2);
         const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
         const uint32_t w1 = ((idx & 31) > 27) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
         const uint32_t b5 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x1Fu;  // bit i: cz - 2 + i
@@ -905,7 +910,9 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
           const uint32_t lt = b < 4 ? lt0 : lt1;
           if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
           const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-#ifndef DBT_DIAG_NO_RED
+#if defined(DBT_DIAG_RED_SPLIT)
+          atomicAnd(&a.dmask[off + b], run_mask_of((int)d));
+#elif !defined(DBT_DIAG_NO_RED)
           atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
 #endif
           ++changed;
@@ -1216,7 +1223,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   if (g->cert_dk != b->dk_hash) {
     // certificates of another distance kernel say nothing about this one
     if (g->cert_dk != 0)
-      DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cells + 63) / 32) * 4, st));
+      DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, st));
     g->cert_dk = b->dk_hash;
   }
   // claim mode: centre dedup and cross-launch skip through the certificates
@@ -1376,6 +1383,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     }
     CullArgs wa;
     wa.cells = g->cells;
+    wa.dmask = g->diag_mask;
     wa.dist = g->dist;
     wa.uniq = g->d_uniq;
     wa.lc = g->d_lcnt;
@@ -1389,6 +1397,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     wa.x0 = g->x0;
     wa.x1 = g->x1;
     wa.xm = g->xm;
+    wa.nx = g->nx;
     wa.ny = g->ny;
     wa.nzp = g->nzp;
     // persistent blocks fetching kCullWarps centres at a time
