@@ -99,12 +99,15 @@ struct XMap {
   int64_t x0 = 0, x1 = 0;
   int64_t w = 0;
   int32_t p = 1, r = 0;
+  // 32-bit arithmetic: planes are < 2^21 (kMaxDim), and int64 division is a
+  // long software sequence on the GPU
   __host__ __device__ __forceinline__ int64_t local(int64_t gx) const {
     if (gx < x0 || gx >= x1) return -1;
     if (w == 0) return gx - x0;
-    const int64_t u = gx - x0, blk = u / w;
-    if (blk % p != r) return -1;
-    return (blk / p) * w + (u - blk * w);
+    const uint32_t u = (uint32_t)(gx - x0), ww = (uint32_t)w, blk = u / ww;
+    const uint32_t q = blk / (uint32_t)p;
+    if (blk - q * (uint32_t)p != (uint32_t)r) return -1;
+    return (int64_t)(q * ww + (u - blk * ww));
   }
   // some owned plane lies in [lo, hi] (a return's K^3 cube [cx-R, cx+R]
   // touches this part)
@@ -113,10 +116,10 @@ struct XMap {
     hi = hi >= x1 ? x1 - 1 : hi;
     if (lo > hi) return false;
     if (w == 0) return true;
-    const int64_t b0 = (lo - x0) / w, b1 = (hi - x0) / w;
-    if (b1 - b0 + 1 >= p) return true;
-    for (int64_t b = b0; b <= b1; ++b)
-      if (b % p == r) return true;
+    const uint32_t ww = (uint32_t)w, b0 = (uint32_t)(lo - x0) / ww, b1 = (uint32_t)(hi - x0) / ww;
+    if (b1 - b0 + 1 >= (uint32_t)p) return true;
+    for (uint32_t b = b0; b <= b1; ++b)
+      if (b % (uint32_t)p == (uint32_t)r) return true;
     return false;
   }
   __host__ int64_t planes() const {

@@ -255,7 +255,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
          cy <= a.ny - 1 - a.R && cz <= a.nz - 1 - a.R;
     if (ok) {
       int ba = 0, be = 0;
-      if (a.bins) {
+      relevant = a.xm.touches(cx - a.R, cx + a.R);
+      if (!relevant) {
+        // a sharded part skips the bins of returns whose cube misses its
+        // planes (only the shadow update of a relevant return needs one)
+      } else if (a.bins) {
         bin_dev(rx, ry, rz, nrm, a.b_az, a.b_el, a.seeds, ba, be, fallback);
         a.bin[i] = (uint16_t)(ba * a.b_el + be);
       } else {
@@ -268,7 +272,6 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
       packed = pack_center(cx, cy, cz);
       // a part of a sharded grid ignores returns whose cube misses its planes
       // (still counted; the first-return choice below stays global)
-      relevant = a.xm.touches(cx - a.R, cx + a.R);
       if (a.claim && relevant) {
         // claim the stamp certificate of the centre (one atomicOr): a bit
         // already set means the stamp is in the grid from an earlier launch
@@ -989,6 +992,59 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
   if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
 }
 
+// Warp-independent variant of the culling sweep (A/B: -DDBT_SWEEP_WARP): each
+// warp fetches groups of centres and runs phase A and phase B for one centre
+// at a time on its own shared-memory queue, with no block barrier (a heavy
+// centre is swept by its own 32 lanes).
+__global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_warp_kernel(CullArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw) + warp * a.K * a.K;
+  __shared__ int q_n[kCullWarps];
+  const int64_t n_items = (int64_t)a.lc->n_unique;
+  unsigned long long changed = 0, rows_done = 0;
+  constexpr int G = 4;  // centres per work fetch
+  long long next = 0;
+  if (lane == 0) next = (long long)atomicAdd(&a.lc->work, (unsigned long long)G);
+  next = __shfl_sync(0xffffffffu, next, 0);
+  while (next < n_items) {
+    const long long cur = next;
+    if (lane == 0) next = (long long)atomicAdd(&a.lc->work, (unsigned long long)G);  // overlaps this group
+    for (int k = 0; k < G && cur + k < n_items; ++k) {
+      if (lane == 0) q_n[warp] = 0;
+      __syncwarp();
+      cull_centre(a, a.uniq[cur + k], lane, &q_n[warp], [&](int i, uint64_t t) { queue[i] = t; });
+      __syncwarp();
+      const int nq = q_n[warp];
+      for (int i = lane; i < nq; i += 64) {
+        const uint64_t tasks[2] = {queue[i], i + 32 < nq ? queue[i + 32] : kEmptyKey};
+        sweep_rows2(a, tasks, changed, rows_done);
+      }
+      __syncwarp();
+    }
+    next = __shfl_sync(0xffffffffu, next, 0);
+  }
+  __shared__ unsigned long long blk_changed, blk_rows;
+  if (threadIdx.x == 0) blk_changed = blk_rows = 0;
+  for (int o = 16; o; o >>= 1) {
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    rows_done += __shfl_xor_sync(0xffffffffu, rows_done, o);
+  }
+  __syncthreads();
+  if (lane == 0 && changed) atomicAdd(&blk_changed, changed);
+  if (lane == 0 && rows_done) atomicAdd(&blk_rows, rows_done);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_changed) atomicAdd(&a.lc->changed, blk_changed);
+  if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
+}
+
+#ifdef DBT_SWEEP_WARP
+#define DBT_ISO_SWEEP sweep_warp_kernel
+#else
+#define DBT_ISO_SWEEP sweep_cull_kernel
+#endif
+
 typedef void (*SweepFn)(SweepArgs);
 
 SweepFn sweep_fn(int CH) {
@@ -1374,9 +1430,9 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   if (b->iso && !(p->flags & DBT_FLAG_GENERIC_SWEEP)) {
     const size_t smem = (size_t)kCullWarps * b->K * b->K * sizeof(uint64_t);
     if (g->sweep_ch != -b->K) {
-      DBT_CUDA(cudaFuncSetAttribute(sweep_cull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      DBT_CUDA(cudaFuncSetAttribute(DBT_ISO_SWEEP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0, sms = 0;
-      DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_cull_kernel, kCullWarps * 32, smem));
+      DBT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, DBT_ISO_SWEEP, kCullWarps * 32, smem));
       DBT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
       g->sweep_blocks = std::max(per_sm, 1) * sms;
       g->sweep_ch = -b->K;
@@ -1405,7 +1461,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     prof_begin(g, "sweep_kernel", st, &tok);
     if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
       // exact_pre sits between prep and the sweep: plain stream order
-      sweep_cull_kernel<<<blocks, kCullWarps * 32, smem, st>>>(wa);
+      DBT_ISO_SWEEP<<<blocks, kCullWarps * 32, smem, st>>>(wa);
     } else {
       // programmatic dependent launch: the sweep's launch latency overlaps
       // the tail of preprocessing (the kernel waits for prep's completion)
@@ -1419,7 +1475,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      DBT_CUDA(cudaLaunchKernelEx(&cfg, sweep_cull_kernel, wa));
+      DBT_CUDA(cudaLaunchKernelEx(&cfg, DBT_ISO_SWEEP, wa));
     }
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("sweep_cull_kernel");

@@ -181,8 +181,11 @@ class ReplicatedGrid:
 
     def mark(self):
         """Start a merge interval from the current records (after creation,
-        reset or any host write)."""
+        reset or any host write). A host mirror is uploaded and then dropped:
+        a later upload of it would replace the records and void the merge
+        base (reading grid.mask/sign/hits again downloads a fresh one)."""
         self.local.push_host()
+        self.local._host = None
         _native.check(_native.lib().dbt_replica_mark(self.local.handle))
         self._params = None
 

@@ -16,7 +16,10 @@ import tempfile
 
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-lib = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2509_20081_b200", "libdbtsdf.so")
+# column to aggregate: stall samples (default) or e.g. "Instructions Executed"
+COL = os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)")
+lib = os.environ.get("DBT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..",
+                                                  "paper_2509_20081_b200", "libdbtsdf.so")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -29,13 +32,13 @@ for i, r in enumerate(rows):
         break
 hdr_i = next(i for i, r in enumerate(rows) if i > sec_start and "Address" in r and "Source" in r)
 hdr = rows[hdr_i]
-ia, isrc, ismp = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
+ia, isrc, ismp = hdr.index("Address"), hdr.index("Source"), hdr.index(COL)
 samples = []
 for r in rows[hdr_i + 1:]:
     if r and r[0] == "Kernel Name":
         break
     if len(r) == len(hdr):
-        samples.append((int(r[ia], 16), r[isrc].strip(), int(r[ismp] or 0)))
+        samples.append((int(r[ia], 16), r[isrc].strip(), int(float(r[ismp] or 0))))
 base = samples[0][0]
 rel = {a - base: (s, n) for a, s, n in samples}
 tmp = tempfile.mkdtemp()

@@ -1,6 +1,6 @@
 """Average per-launch ncu metrics per engine kernel -> profiles/kernel_traffic.json.
 
-usage: python tools/ncu_traffic.py <ncu --csv --print-units base log> [source description]
+usage: python tools/ncu_traffic.py <ncu --csv --print-units base log> <config>x<batch> [source description]
 The log comes from e.g.
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
       lts__t_sectors_op_red.sum,lts__t_sectors_op_atom.sum --clock-control none
@@ -14,7 +14,8 @@ import os
 import sys
 
 path = sys.argv[1]
-src = sys.argv[2] if len(sys.argv) > 2 else path
+cfg_key = sys.argv[2]
+src = sys.argv[3] if len(sys.argv) > 3 else path
 rows = [r for r in csv.reader(open(path)) if len(r) > 10]
 hdr = rows[0]
 ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
@@ -40,7 +41,10 @@ for k, mets in acc.items():
         o["launches"] = len(per)
     o["dram_bytes"] = o.get("dram__bytes_read.sum", 0.0) + o.get("dram__bytes_write.sum", 0.0)
     out[k] = o
-res = {"kernels": out, "source": src}
 dst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "kernel_traffic.json")
-json.dump(res, open(dst, "w"), indent=1)
-print(json.dumps(res, indent=1))
+allres = json.load(open(dst)) if os.path.exists(dst) else {}
+if "configs" not in allres:  # the round-1 file held one config-2 capture
+    allres = {"configs": {}}
+allres["configs"][cfg_key] = {"kernels": out, "source": src}
+json.dump(allres, open(dst, "w"), indent=1)
+print(json.dumps(allres["configs"][cfg_key], indent=1))

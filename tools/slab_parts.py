@@ -32,6 +32,7 @@ L.dbt_profile_enable  # noqa
 
 def run_part(g, timed_from=10):
     tot, prep = 0.0, 0.0
+    acc = np.zeros(4)
     L.dbt_profile_enable(g.handle, 1)
     for k in range(len(scans)):
         if k == timed_from:
@@ -49,6 +50,9 @@ def run_part(g, timed_from=10):
         torch.cuda.synchronize()
         if k >= timed_from:
             tot += a.elapsed_time(b)
+            st = (_native.Stats * 1)()
+            L.dbt_stats_read(g.handle, st, 1)
+            acc += [st[0].unique_centers, st[0].rows_swept, st[0].voxels_written, st[0].centers_skipped]
     names = ctypes.create_string_buffer(32 * 16)
     ms = (ctypes.c_double * 16)()
     cn = (ctypes.c_int64 * 16)()
@@ -57,6 +61,7 @@ def run_part(g, timed_from=10):
     ks = {names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): ms[i] / max(cn[i], 1) * 1e3 for i in range(nk.value)}
     L.dbt_profile_enable(g.handle, 0)
     n = len(scans) - timed_from
+    ks["counters"] = (acc / n).round().astype(int).tolist()  # centres swept, rows, REDs, skipped per scan
     return tot / n * 1e3, ks
 
 
@@ -68,7 +73,7 @@ for N in Ns:
         g = VoxelGrid(w.dims, w.voxel_size, w.origin, interleave=(width, N, r)) if N > 1 else \
             VoxelGrid(w.dims, w.voxel_size, w.origin)
         us, ks = run_part(g)
-        parts.append(round(us, 1))
+        parts.append((round(us, 1), ks["counters"]))
         if us > worst:
             worst, worst_k = us, ks
         del g
