@@ -27,6 +27,7 @@ int cuda_error(cudaError_t e, const char* what) {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static int prof_index(dbt_grid* g, const char* name) {
   for (size_t i = 0; i < g->prof_names.size(); ++i)

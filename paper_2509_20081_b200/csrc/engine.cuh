@@ -256,6 +256,15 @@ struct dbt_grid {
   // it on the host (an event recorded per launch costs ~7 us of pipelined
   // throughput on config 2)
   cudaStream_t last_st = nullptr;
+  // CUDA graph of the synchronous single-scan launch sequence (integrate.cu,
+  // integrate_host_graph): captured once per launch shape, replayed with
+  // updated prep / shadow kernel arguments
+  cudaGraph_t ggraph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphNode_t gprep = nullptr, gshadow = nullptr;
+  uint64_t gkey[12] = {};
+  int gkernels = 0;
+  bool gdisabled = false;                      // capture unsupported here, or $DBT_NO_GRAPH
   int sweep_ch = 0;                            // cached sweep launch shape
   int64_t sweep_blocks = 0;
   double last_device_ms = 0;
@@ -274,6 +283,7 @@ int launch_exact_post(dbt_grid* g, const dbt_bank* b, cudaStream_t st);
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* what);
 void count_launch();
+void add_launches(int64_t n);  // kernels run by a graph launch (or undo counts made under capture)
 
 #define DBT_CUDA(call)                                   \
   do {                                                   \

@@ -1182,10 +1182,26 @@ int validate_params(const dbt_params* p) {
 
 // Core launch sequence. Points are already on the device (d_pts). counts /
 // poses are host arrays. map_sensor (device) selects the map-frame mode.
+// Graph mode of a single-scan launch (integrate_host_graph): the host-side
+// bookkeeping and the conditional pre-steps (fold on a parameter change,
+// epoch wrap, certificate reset) always run here, issued directly; the core
+// sequence — counter memset, prep, shadow fork/join, PDL sweep — is captured
+// once into a CUDA graph (capture) and afterwards only the prep / shadow
+// kernel arguments of the instantiated graph change per call (replay).
+struct GraphCtl {
+  bool capture = false;  // issue the core under stream capture
+  bool replay = false;   // do not issue the core: fill the arguments below
+  PrepArgs pa;
+  ShadowArgs sa;
+  unsigned prep_blocks = 0, shadow_blocks = 0;
+  bool shadow_bin = false;  // shadow_bin_kernel (else shadow_kernel)
+  bool has_shadow = false;
+};
+
 int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtype,
                      const int64_t* counts, int S, const double* poses, const dbt_params* p,
                      const double* d_map_sensor, int8_t* d_outcome, cudaStream_t st,
-                     const void* const* scan_ptrs) {
+                     const void* const* scan_ptrs, GraphCtl* gc = nullptr) {
   if (S < 1 || S > kMaxScansPerLaunch) return set_error(DBT_ERR_CONFIG, "scan count per launch out of range");
   if (b->device != g->device) return set_error(DBT_ERR_CONFIG, "bank and grid live on different devices");
   if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
@@ -1248,11 +1264,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     DBT_CUDA(cudaMemcpyAsync(g->d_scan_off, h_scan, bytes, cudaMemcpyHostToDevice, st));
     DBT_CUDA(cudaEventRecord(g->ev_meta, st));
   }
-  // launch + per-scan counters: one contiguous block, one memset (zeroing
-  // them behind the previous launch's read-back instead measured 2 us per
-  // step slower device-resident)
-  DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
-  if (n == 0) return DBT_OK;
+  if (n == 0) {
+    DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
+    return DBT_OK;
+  }
   // pending shadow visits were counted under other (h_max, T): fold them first
   if (g->pend && (g->pend_h_max != p->h_max || g->pend_t_occ != p->t_occ)) {
     rc = fold_pending(g, st);
@@ -1282,6 +1297,13 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
       DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, st));
     g->cert_dk = b->dk_hash;
   }
+  // the core sequence starts here (graph mode: captured once, then replayed)
+  if (gc && gc->capture) DBT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const bool issue = !(gc && gc->replay);
+  // launch + per-scan counters: one contiguous block, one memset (zeroing
+  // them behind the previous launch's read-back instead measured 2 us per
+  // step slower device-resident)
+  if (issue) DBT_CUDA(cudaMemsetAsync(g->d_lcnt, 0, sizeof(LaunchCounters) + S * sizeof(ScanCounters), st));
   // claim mode: centre dedup and cross-launch skip through the certificates
   // (the stamp of a centre is the same for every return there, so this holds
   // in first-return mode too; the hash then only picks the shadow return)
@@ -1362,10 +1384,18 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.ray = g->d_ray;
   if (rc) return rc;
   int tok;
-  prof_begin(g, "prep_kernel", st, &tok);
-  prep_kernel<<<(unsigned)((n + kPrepThreads - 1) / kPrepThreads), kPrepThreads, 0, st>>>(pa);
-  prof_end(g, st, tok);
-  DBT_CHECK_LAUNCH("prep_kernel");
+  const unsigned prep_blocks = (unsigned)((n + kPrepThreads - 1) / kPrepThreads);
+  if (gc) {
+    gc->pa = pa;
+    gc->prep_blocks = prep_blocks;
+    gc->has_shadow = false;
+  }
+  if (issue) {
+    prof_begin(g, "prep_kernel", st, &tok);
+    prep_kernel<<<prep_blocks, kPrepThreads, 0, st>>>(pa);
+    prof_end(g, st, tok);
+    DBT_CHECK_LAUNCH("prep_kernel");
+  }
 
   bool joined = false;
 #ifdef DBT_DIAG_NO_SHADOW
@@ -1398,25 +1428,35 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     sa.lc = g->d_lcnt;
     int64_t total = n << l2;
     unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
-    // fork: aux waits for prep, runs the shadow kernel; joined before the
-    // counters are read back
-    DBT_CUDA(cudaEventRecord(g->ev_fork, st));
-    DBT_CUDA(cudaStreamWaitEvent(g->aux, g->ev_fork, 0));
-    prof_begin(g, "shadow_kernel", g->aux, &tok);
     if (shadow_bins) {
       const int64_t tiles = (n + (256 >> l2) - 1) >> (8 - l2);
       sa.ray = g->d_ray;
       sa.b_az = b->b_az;
       sa.b_el = b->b_el;
       sa.seeds = pa.seeds;
-      shadow_bin_kernel<<<(unsigned)std::min<int64_t>(tiles, 148 * 64), 256, 0, g->aux>>>(sa);
-    } else {
-      shadow_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+      blocks = (unsigned)std::min<int64_t>(tiles, 148 * 64);
     }
-    prof_end(g, g->aux, tok);
-    DBT_CHECK_LAUNCH("shadow_kernel");
-    DBT_CUDA(cudaEventRecord(g->ev_join, g->aux));
-    joined = true;
+    if (gc) {
+      gc->sa = sa;
+      gc->shadow_blocks = blocks;
+      gc->shadow_bin = shadow_bins;
+      gc->has_shadow = true;
+    }
+    if (issue) {
+      // fork: aux waits for prep, runs the shadow kernel; joined before the
+      // counters are read back
+      DBT_CUDA(cudaEventRecord(g->ev_fork, st));
+      DBT_CUDA(cudaStreamWaitEvent(g->aux, g->ev_fork, 0));
+      prof_begin(g, "shadow_kernel", g->aux, &tok);
+      if (shadow_bins)
+        shadow_bin_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+      else
+        shadow_kernel<<<blocks, 256, 0, g->aux>>>(sa);
+      prof_end(g, g->aux, tok);
+      DBT_CHECK_LAUNCH("shadow_kernel");
+      DBT_CUDA(cudaEventRecord(g->ev_join, g->aux));
+      joined = true;
+    }
   }
 
   if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
@@ -1456,8 +1496,15 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     wa.nx = g->nx;
     wa.ny = g->ny;
     wa.nzp = g->nzp;
-    // persistent blocks fetching kCullWarps centres at a time
-    unsigned blocks = (unsigned)std::min<int64_t>(g->sweep_blocks, std::max<int64_t>(1, (n + 2 * kCullWarps - 1) / (2 * kCullWarps)));
+    if (!issue) {
+      g->last_st = st;
+      return DBT_OK;
+    }
+    // persistent blocks fetching kCullWarps centres at a time (a graph keeps
+    // the full persistent grid: its shape cannot follow n)
+    unsigned blocks = gc ? (unsigned)g->sweep_blocks
+                         : (unsigned)std::min<int64_t>(g->sweep_blocks,
+                                                       std::max<int64_t>(1, (n + 2 * kCullWarps - 1) / (2 * kCullWarps)));
     prof_begin(g, "sweep_kernel", st, &tok);
     if (p->flags & DBT_FLAG_EXACT_WRITTEN) {
       // exact_pre sits between prep and the sweep: plain stream order
@@ -1601,6 +1648,111 @@ double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// The synchronous single-scan sequence as a CUDA graph: one cudaGraphLaunch
+// (plus two kernel-argument updates) instead of ~10 stream calls, and no
+// launch gaps between the kernels. Eligible: default-path launches (claim
+// mode, isotropic kernel, no first-return / exact / measurement flags), not
+// under profiling. The graph is re-captured when the launch shape changes
+// (bank, dtype, flags, parameters, scratch buffers, stream, shadow mode).
+// Returns DBT_OK after enqueueing the graph (counters D2H included).
+bool graph_eligible(const dbt_grid* g, const dbt_bank* b, const dbt_params* p) {
+  static const bool off = getenv("DBT_NO_GRAPH") != nullptr;
+  const uint32_t bad = DBT_FLAG_NO_DEDUP | DBT_FLAG_NO_SKIP | DBT_FLAG_FUSE_SHADOW | DBT_FLAG_GENERIC_SWEEP |
+                       DBT_FLAG_EXACT_WRITTEN | DBT_FLAG_MAP_FRAME;
+  return !off && !g->gdisabled && !g->profiling && b->iso && !p->first_return && !(p->flags & bad);
+}
+
+int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype, int64_t n_raw, const double* pose,
+                    const dbt_params* p, cudaStream_t st) {
+  const int64_t n = (n_raw + p->downsample - 1) / p->downsample;
+  if (g->sweep_ch != -b->K || n > g->cap_pts || 2 * n > g->cap_hash) {
+    // first launch with this bank / growth of the scratch buffers: the one-time
+    // setup (allocations, sweep shape, seed table) runs outside any capture
+    int rc = launch_integrate(g, b, d_src, dtype, &n_raw, 1, pose, p, nullptr, nullptr, st, nullptr);
+    return rc ? rc : fetch_counters(g, st);
+  }
+  uint64_t key[12] = {b->serial, (uint64_t)dtype, (uint64_t)p->flags,
+                      (uint64_t)p->h_max | ((uint64_t)p->t_occ << 8) | ((uint64_t)p->downsample << 16),
+                      (uint64_t)(uintptr_t)g->d_center, (uint64_t)g->cap_pts, (uint64_t)(uintptr_t)st,
+                      (uint64_t)(n <= (1 << 19)), (uint64_t)g->sweep_blocks, (uint64_t)(uintptr_t)g->d_raw,
+                      (uint64_t)g->cap_hash, (uint64_t)(uintptr_t)b};
+  GraphCtl gc;
+  const bool fresh = !g->gexec || std::memcmp(key, g->gkey, sizeof(key)) != 0;
+  if (fresh) {
+    if (g->gexec) cudaGraphExecDestroy(g->gexec);
+    if (g->ggraph) cudaGraphDestroy(g->ggraph);
+    g->gexec = nullptr;
+    g->ggraph = nullptr;
+    // the persistent sweep grid size is measured on first use: make sure it
+    // is known before the key is stored
+    gc.capture = true;
+    const int64_t c0 = dbt_launch_count();
+    int rc = launch_integrate(g, b, d_src, dtype, &n_raw, 1, pose, p, nullptr, nullptr, st, nullptr, &gc);
+    if (!rc) rc = fetch_counters(g, st);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+    add_launches(-(dbt_launch_count() - c0));  // nothing ran yet
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ei = ec == cudaSuccess ? cudaGraphInstantiate(&exec, graph, 0) : ec;
+    if (ei != cudaSuccess) {
+      // capture of this sequence is not supported here: direct launches
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      g->gdisabled = true;
+      rc = launch_integrate(g, b, d_src, dtype, &n_raw, 1, pose, p, nullptr, nullptr, st, nullptr);
+      if (!rc) rc = fetch_counters(g, st);
+      return rc;
+    }
+    size_t nn = 0;
+    DBT_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    DBT_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    g->gprep = g->gshadow = nullptr;
+    g->gkernels = 0;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      DBT_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      ++g->gkernels;
+      cudaKernelNodeParams kp;
+      DBT_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == (void*)prep_kernel) g->gprep = nd;
+      if (kp.func == (void*)shadow_kernel || kp.func == (void*)shadow_bin_kernel) g->gshadow = nd;
+    }
+    g->ggraph = graph;
+    g->gexec = exec;
+    std::memcpy(g->gkey, key, sizeof(key));
+    if (!g->gprep) return set_error(DBT_ERR_GENERIC, "graph capture lost the prep kernel");
+  } else {
+    gc.replay = true;
+    int rc = launch_integrate(g, b, d_src, dtype, &n_raw, 1, pose, p, nullptr, nullptr, st, nullptr, &gc);
+    if (rc) return rc;
+    cudaKernelNodeParams kp = {};
+    void* pargs[] = {&gc.pa};
+    kp.func = (void*)prep_kernel;
+    kp.gridDim = dim3(gc.prep_blocks);
+    kp.blockDim = dim3(kPrepThreads);
+    kp.kernelParams = pargs;
+    DBT_CUDA(cudaGraphExecKernelNodeSetParams(g->gexec, g->gprep, &kp));
+    if (gc.has_shadow != (g->gshadow != nullptr)) return set_error(DBT_ERR_GENERIC, "graph shape changed");
+    if (gc.has_shadow) {
+      void* sargs[] = {&gc.sa};
+      kp.func = gc.shadow_bin ? (void*)shadow_bin_kernel : (void*)shadow_kernel;
+      kp.gridDim = dim3(gc.shadow_blocks);
+      kp.blockDim = dim3(256);
+      kp.kernelParams = sargs;
+      DBT_CUDA(cudaGraphExecKernelNodeSetParams(g->gexec, g->gshadow, &kp));
+    }
+  }
+  DBT_CUDA(cudaGraphLaunch(g->gexec, st));
+  add_launches(g->gkernels);
+  return DBT_OK;
+}
+
 int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, const int64_t* counts,
                    int S, const double* poses, const dbt_params* p, dbt_stats* out) {
   double t0 = now_ms();
@@ -1638,9 +1790,12 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
     DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
     d_src = g->d_raw;
   }
-  rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st, nullptr);
-  if (rc) return rc;
-  rc = fetch_counters(g, st);
+  if (S == 1 && graph_eligible(g, b, p)) {
+    rc = integrate_graph(g, b, d_src, dtype, counts[0], poses, p, st);
+  } else {
+    rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st, nullptr);
+    if (!rc) rc = fetch_counters(g, st);
+  }
   if (rc) return rc;
   double dms = 0.0;
   rc = call_end(g, st, timed, &dms);

@@ -243,8 +243,8 @@ def trajectories() -> list:
         # config 2 in full: the 100-scan trajectory
         Trajectory("cfg2_traj100", 2, (0, 100), w2.dims, w2.voxel_size, w2.origin,
                    dict(size=21, shadow_radius=w2.shadow_radius)),
-        # config 3 prefix, also the config-5 batched case (batches of 8 / 32)
-        Trajectory("cfg3_traj32", 3, (0, 32), w3.dims, w3.voxel_size, w3.origin,
+        # config 3 prefix, also the config-5 batched case (batches of 8 / 32 / 128)
+        Trajectory("cfg3_traj128", 3, (0, 128), w3.dims, w3.voxel_size, w3.origin,
                    dict(size=21, shadow_radius=w3.shadow_radius), slow=True),
         # config-4 scene/sensor at 0.02 m on the 1000x1000x400 window (the
         # reference's host arrays for the full grid are 38 GB); scans 0-29

@@ -2,8 +2,8 @@
 
 The reference's grid hashes after EVERY scan of each trajectory of
 tests/cases.py (``trajectories()``: config 2 in full, 100 scans; config 3
-scans 0-31, also the config-5 batched case; the config-4 scene at 0.02 m on
-its 1000x1000x400 window, scans 0-29) are stored in
+scans 0-127, also the config-5 batched case; the config-4 scene at 0.02 m
+on its 1000x1000x400 window, scans 0-29) are stored in
 tests/golden/trajectories.json by tests/golden/make_trajectories.py, which
 imports the reference itself (integrator.py:207-287). Here the engine runs
 the same scans through its default path — stamp certificates carried across
@@ -11,7 +11,8 @@ launches, neighbour-dominance culling, lazy shadow-visit folds, the PDL sweep
 launch — and its downloaded grid must hash identically at every checkpoint:
 
 * scan by scan through ``integrate_frame`` (synchronous calls);
-* in batches of 8 and 32 scans per launch (``integrate_frames``, config 5);
+* in batches of 8, 32 and 128 scans per launch (``integrate_frames``,
+  config 5's batch sizes);
 * device-resident launches queued back to back without a host sync
   (``dbt_integrate_device``, exactly what bench.py times);
 * config 2 with ``exact_voxels_written``: every FrameStats field equals the
@@ -83,9 +84,10 @@ def assert_grid(g, t, i, how):
 
 def checkpoints(t):
     n = len(t.scan_ids())
-    # every scan on config 2 (21.7 M voxels); every 5th + the last on the
-    # 4e8-voxel grids (each check downloads and hashes 2.4 GB)
-    step = 1 if t.config <= 2 else 5
+    # every scan on config 2 (21.7 M voxels); every 5th (config-4 window) or
+    # 16th (config 3, 128 scans) + the last on the 4e8-voxel grids (each
+    # check downloads and hashes 2.4 GB)
+    step = 1 if t.config <= 2 else (5 if len(t.scan_ids()) <= 40 else 16)
     return sorted(set(range(step - 1, n, step)) | {n - 1})
 
 
@@ -104,7 +106,7 @@ def test_trajectory_scan_by_scan(name):
             assert_grid(g, t, i, "integrate_frame, scan by scan")
 
 
-@pytest.mark.parametrize("batch", [8, 32])
+@pytest.mark.parametrize("batch", [8, 32, 128])
 @pytest.mark.parametrize("name", list(TRAJ))
 def test_trajectory_batched(name, batch):
     t = TRAJ[name]
@@ -119,7 +121,7 @@ def test_trajectory_batched(name, batch):
         for j, st in enumerate(sts):
             assert [st.points_in, st.points_discarded] == ref[b0 + j]["stats"][:2]
         last = min(b0 + batch, n) - 1
-        if t.config <= 2 or last == n - 1 or (last + 1) % 16 == 0:
+        if t.config <= 2 or last == n - 1 or (last + 1) % 32 == 0:
             assert_grid(g, t, last, f"integrate_frames, {batch} scans per launch")
 
 
