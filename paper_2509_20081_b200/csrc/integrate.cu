@@ -1934,6 +1934,9 @@ int dbt_integrate_device(dbt_grid* g, const dbt_bank* b, const void* d_points, i
   if (!rc) rc = validate_params(p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;  // NULL = legacy default stream
+  // single scans on a capturable stream go through the launch-sequence graph
+  if (n_scans == 1 && st != nullptr && counts[0] > 0 && graph_eligible(g, b, p))
+    return integrate_graph(g, b, d_points, dtype, counts[0], poses, p, st);
   rc = launch_integrate(g, b, d_points, dtype, counts, n_scans, poses, p, nullptr, nullptr, st, nullptr);
   if (rc) return rc;
   return fetch_counters(g, st);
