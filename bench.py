@@ -181,6 +181,24 @@ def gen_scans(w, ids):
         return dict(zip(ids, ex.map(_scan_job, [(w.config, k) for k in ids])))
 
 
+def diag_reorder(pts, pose, w, how):
+    """Diagnostics: the scan's points permuted by their map-frame voxel
+    (Morton / lexicographic) or at random. The grid result does not depend
+    on the order; the sweep's memory locality does."""
+    if how == "random":
+        return pts[np.random.default_rng(0).permutation(len(pts))]
+    m = pts.astype(np.float64) @ pose[:3, :3].T + pose[:3, 3]
+    v = np.clip(np.floor((m - np.asarray(w.origin)) / w.voxel_size), 0, (1 << 20) - 1).astype(np.uint64)
+    if how == "xyz":
+        key = (v[:, 0] << np.uint64(42)) | (v[:, 1] << np.uint64(21)) | v[:, 2]
+    else:
+        key = np.zeros(len(v), np.uint64)
+        for b in range(21):
+            for a in range(3):
+                key |= ((v[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + (2 - a))
+    return np.ascontiguousarray(pts[np.argsort(key, kind="stable")])
+
+
 def cpu_grid_for(w):
     """Grid the CPU samples run on. Config 4's 6.4e9-voxel grid needs 38 GB
     of reference host arrays; per-scan CPU cost does not depend on grid size
@@ -319,6 +337,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="diagnostics only: skip the end-to-end passes")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
+    ap.add_argument("--diag-order", default=None, choices=["morton", "xyz", "random"],
+                    help="diagnostics only: reorder each scan's points (spatial locality of the sweep work list)")
     ap.add_argument("--interleave", type=int, default=None,
                     help="slab mode: x-block width of interleaved sharding (default 64, at most nx / 2N)")
     ap.add_argument("--multi", default="slab", choices=["replica", "slab"],
@@ -365,6 +385,8 @@ def main():
     replica = multi == "replica"
     holds_scans = rank == 0 or replica
     scans = gen_scans(w, pre + [k for b in win for k in b]) if holds_scans else {}
+    if args.diag_order:
+        scans = {k: diag_reorder(v, w.poses[k], w, args.diag_order) for k, v in scans.items()}
     bank = build_kernel_bank(size=K_EDGE, shadow_radius=w.shadow_radius)
     shadow_cells = float(np.mean([len(o) for o in bank.shadow_offsets]))
     params = IntegrationParams()
