@@ -224,6 +224,9 @@ struct dbt_grid {
   int last_scans = 0;
   std::vector<int64_t> last_points_in;
   std::vector<int64_t> last_points_in_host;
+  // pinned, mapped host staging of pageable scans (hostcopy.cu)
+  void* h_stage = nullptr;
+  int64_t cap_hstage = 0;
   // staging for upload/download/readout
   void* d_stage = nullptr;
   int64_t cap_stage = 0;
@@ -302,6 +305,10 @@ void add_launches(int64_t n);  // kernels run by a graph launch (or undo counts 
 void prof_begin(dbt_grid* g, const char* name, cudaStream_t s, int* token);
 void prof_end(dbt_grid* g, cudaStream_t s, int token);
 int prof_flush(dbt_grid* g);
+
+// pageable scans -> pinned mapped staging with a host thread pool
+// (hostcopy.cu): out[i] = device pointer of scan i; false = not staged
+bool stage_pageable(dbt_grid* g, const void* const* srcs, const int64_t* bytes, int n, const void** out);
 
 // scratch management (grid.cu)
 int ensure_stage(dbt_grid* g, int64_t bytes);

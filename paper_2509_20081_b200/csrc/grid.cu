@@ -377,6 +377,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->ev_b) cudaEventDestroy(g->ev_b);
   if (g->ev_done) cudaEventDestroy(g->ev_done);
   if (g->ev_meta) cudaEventDestroy(g->ev_meta);
+  if (g->h_stage) cudaFreeHost(g->h_stage);
   if (g->gexec) cudaGraphExecDestroy(g->gexec);
   if (g->ggraph) cudaGraphDestroy(g->ggraph);
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);

@@ -1783,6 +1783,13 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
       cudaGetLastError();  // pageable pointers report an error on some drivers
   }
   const bool timed = g->time_calls || g->profiling;
+  // pageable scans: multi-threaded host copy into pinned staging, read by
+  // prep over the host link like a pinned scan (the driver's pageable copy
+  // is single-threaded)
+  if (!d_src && !(p->flags & DBT_FLAG_STAGE_COPY)) {
+    const int64_t bytes = total * (int64_t)esz;
+    if (!stage_pageable(g, &points, &bytes, 1, &d_src)) d_src = nullptr;
+  }
   call_begin(g, st, timed);
   if (!d_src) {
     rc = stage_raw(g, total * (int64_t)esz);
@@ -1838,6 +1845,21 @@ int integrate_scans_host(dbt_grid* g, const dbt_bank* b, const void* const* poin
       dptr[s] = at.devicePointer;
     else
       cudaGetLastError();
+  }
+  if (!(p->flags & DBT_FLAG_STAGE_COPY)) {
+    // pageable scans: multi-threaded host copy into pinned staging
+    std::vector<const void*> src;
+    std::vector<int64_t> bytes;
+    std::vector<int> idx;
+    for (int s = 0; s < S; ++s)
+      if (!dptr[s] && counts[s]) {
+        src.push_back(points[s]);
+        bytes.push_back(counts[s] * (int64_t)esz);
+        idx.push_back(s);
+      }
+    std::vector<const void*> out(src.size());
+    if (!src.empty() && stage_pageable(g, src.data(), bytes.data(), (int)src.size(), out.data()))
+      for (size_t i = 0; i < idx.size(); ++i) dptr[idx[i]] = out[i];
   }
   for (int s = 0; s < S; ++s)
     if (!dptr[s]) staged += counts[s];

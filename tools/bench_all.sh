@@ -1,10 +1,22 @@
 #!/bin/bash
-# Per-config bench lines (BASELINE.json configs 1-5) into gpurun_out/bench_cfg*.log
-python bench.py --config 1 --steps 50 --warmup 5 > gpurun_out/bench_cfg1.log 2>&1
-python bench.py --config 2 > gpurun_out/bench_cfg2.log 2>&1
-python bench.py --config 3 --steps 40 --warmup 4 --max-scans 44 > gpurun_out/bench_cfg3.log 2>&1
-python bench.py --config 4 --steps 24 --warmup 3 --max-scans 27 > gpurun_out/bench_cfg4.log 2>&1
-for b in 8 32; do
-  python bench.py --config 5 --batch $b --steps 4 --warmup 1 --max-scans $((5*b)) --no-cpu-baseline > gpurun_out/bench_cfg5_b$b.log 2>&1
+# Per-config bench lines of the current build (GPU box, repo root):
+#   bash tools/bench_all.sh <tag>   -> gpurun_out/<tag>_bench_cfg*.log
+T=${1:-r2}
+for spec in "1 1" "2 1" "3 1" "4 1" "5 8" "5 32" "5 128"; do
+  set -- $spec
+  python bench.py --config $1 --batch $2 > gpurun_out/${T}_bench_cfg$1_b$2.log 2>&1
+  python bench.py --impl reference --config $1 --batch $2 > gpurun_out/${T}_bench_ref_cfg$1_b$2.log 2>&1
 done
-python bench.py --impl reference --config 2 --steps 20 --warmup 2 > gpurun_out/bench_ref_cfg2.log 2>&1
+python - "$T" <<'PY'
+import glob, json, sys
+T = sys.argv[1]
+for f in sorted(glob.glob(f"gpurun_out/{T}_bench_cfg*_b*.log")):
+    try:
+        d = json.loads(open(f).read().strip().splitlines()[-1])
+        r = json.loads(open(f.replace("_bench_cfg", "_bench_ref_cfg")).read().strip().splitlines()[-1])
+        print(f"{f:40s} value {d['value'] / 1e6:8.1f} M/s  step {d['ms_per_step'] * 1e3:7.1f} us  e2e {d['e2e']['value'] / 1e6:7.1f} "
+              f"({d['e2e']['ms_per_step'] * 1e3:.1f} us)  pageable {d['e2e_pageable']['value'] / 1e6:7.1f}  frac {d['roofline']['frac']:.3f}  "
+              f"sweep {d['kernels']['sweep_kernel']['avg_us']:.1f} us  ref {r['value'] / 1e6:.3f} M/s  clocks {d['clocks']['sm_mhz']}")
+    except Exception as e:
+        print(f, "failed", e)
+PY
