@@ -447,14 +447,21 @@ def main():
                 dist.broadcast(pts, 0)
         sg.integrate_device(bank, pts, counts, poses, params, stream=stream)
 
+    profiling = [False]
+
     def refill():
-        """reset + prefill (untimed, queued on the stream)."""
+        """reset + prefill (untimed, queued on the stream; its launches are
+        kept out of the per-kernel profile)."""
+        if profiling[0]:
+            L.dbt_profile_enable(g_local.handle, 0)
         L.dbt_grid_reset(g_local.handle)
         for item in pre_dev:
             launch(item)
         if replica:
             stream.synchronize()
             sg.mark()
+        if profiling[0]:
+            L.dbt_profile_enable(g_local.handle, 1)
 
     # applied returns of every window batch in its pass position (discards
     # do not depend on the grid state), so the timed pass needs no read-back
@@ -467,6 +474,7 @@ def main():
     def run_pass(timed):
         """warmup + steps; timed: no host sync or profiling inside the region
         (launches queue ahead), else per-step stats and per-kernel events."""
+        profiling[0] = not timed
         L.dbt_profile_enable(g_local.handle, 0 if timed else 1)
         refill()
         for s in range(args.warmup):

@@ -1,10 +1,11 @@
 // engine.cuh — internal definitions shared by the libdbtsdf CUDA sources.
 //
-// Device voxel record (8 bytes, one per voxel): the reference's serialized
-// record (grid.py:30-34) — .x = the 32-bit distance mask, .y = sign (byte 0)
-// | hits (byte 1) << 8 | pending shadow visits (bytes 2-3, 0 in every record
-// that leaves the device). The two halves are the single aligned words the
-// two update kinds touch:
+// Device voxel record (8 bytes, one per voxel, stored as two 32-bit arrays —
+// Cells below): the reference's serialized record (grid.py:30-34) — .x (m) =
+// the 32-bit distance mask, .y (y) = sign (byte 0) | hits (byte 1) << 8 |
+// pending shadow visits (bytes 2-3, 0 in every record that leaves the
+// device). The two words are the single aligned words the two update kinds
+// touch:
 //   * mask update (integrator.py:145-149): one native atomicAnd (RED.AND) of
 //     the kernel's run mask into .x — AND is commutative and idempotent, so
 //     no CAS and no retries;
@@ -130,6 +131,23 @@ struct XMap {
   }
 };
 
+// The voxel records, split into two arrays of 32-bit words with the same
+// indexing: m = the distance masks (the sweep's RED.AND target), y = sign |
+// hits << 8 | pending shadow visits << 16 (the shadow kernel's atomicAdd
+// target). A record is (m[i], y[i]); the split keeps each update kind's
+// traffic on its own array (4 bytes per touched voxel instead of the 8-byte
+// record sector share).
+struct Cells {
+  uint32_t* m = nullptr;
+  uint32_t* y = nullptr;
+  __host__ __device__ __forceinline__ uint2 get(int64_t i) const { return make_uint2(m[i], y[i]); }
+  __host__ __device__ __forceinline__ void put(int64_t i, uint2 v) const {
+    m[i] = v.x;
+    y[i] = v.y;
+  }
+  __host__ __device__ __forceinline__ Cells off(int64_t o) const { return Cells{m + o, y + o}; }
+};
+
 // Per-scan device counters (one entry per scan of a launch).
 struct ScanCounters {
   unsigned long long n_ok;       // non-discarded returns
@@ -181,13 +199,12 @@ struct dbt_grid {
   dbt::XMap xm;                             // owned planes (contiguous or interleaved)
   int64_t lx = 0;                           // owned plane count (storage x extent)
   double vs = 0, org[3] = {0, 0, 0};
-  uint2* cells = nullptr;                   // authoritative voxel records
+  dbt::Cells cells;                         // authoritative voxel records (masks | meta words)
   uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel of the GLOBAL grid
                                             // (index (x*ny + y)*nzp + z, x global): a part of a sharded
                                             // grid certifies every centre whose cube touches its planes
   int64_t n_cert = 0;                       // nx*ny*nzp certificate bits
-  uint32_t* diag_mask = nullptr;            // DBT_DIAG_RED_SPLIT builds only (A/B of a 4-byte mask array)
   uint32_t* d_exact_bits = nullptr;         // centre + touched + centre-row bitmaps (exact.cu), lazily
   uint32_t* d_exact_m0 = nullptr;           // pre-launch masks of touched cells (exact.cu)
   uint8_t* d_base_hits = nullptr;           // replica mode: hits at the last merge (replica.cu)

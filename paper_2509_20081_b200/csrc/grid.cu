@@ -31,62 +31,67 @@ namespace {
 
 constexpr int64_t kStageBytes = 256ll << 20;
 
-__global__ void fill_cells_kernel(uint2* __restrict__ cells, int64_t n) {
-  // n is even (allocation is padded); 128-bit stores of two fresh records
-  const uint4 v = make_uint4(kFullMask, kFreshMeta, kFullMask, kFreshMeta);
-  uint4* p = reinterpret_cast<uint4*>(cells);
-  int64_t n2 = n / 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = v;
+__global__ void fill_cells_kernel(Cells cells, int64_t n) {
+  // n is a multiple of 4 (allocation is padded); 128-bit stores of four
+  // fresh masks and four fresh meta words
+  const uint4 vm = make_uint4(kFullMask, kFullMask, kFullMask, kFullMask);
+  const uint4 vy = make_uint4(kFreshMeta, kFreshMeta, kFreshMeta, kFreshMeta);
+  uint4* pm = reinterpret_cast<uint4*>(cells.m);
+  uint4* py = reinterpret_cast<uint4*>(cells.y);
+  int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    pm[i] = vm;
+    py[i] = vy;
+  }
 }
 
 // Host C-order slice (xs, ny, nz) of mask/sign/hits -> device records. Any
 // mask and sign byte the reference can hold is stored as is.
-__global__ void encode_kernel(uint2* __restrict__ cells, const uint32_t* __restrict__ mask,
+__global__ void encode_kernel(Cells cells, const uint32_t* __restrict__ mask,
                               const uint8_t* __restrict__ sign, const uint8_t* __restrict__ hits,
                               int64_t n, int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    cells[row * nzp + z] = make_uint2(mask[i], make_meta(sign[i], hits[i]));
+    cells.put(row * nzp + z, make_uint2(mask[i], make_meta(sign[i], hits[i])));
   }
 }
 
 // dist[v] = bit length of the mask of cells[v] over the whole slab (after host writes)
-__global__ void rebuild_dist_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ dist, int64_t n) {
+__global__ void rebuild_dist_kernel(const uint32_t* __restrict__ cm, uint8_t* __restrict__ dist, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    dist[i] = (uint8_t)mask_bitlen(cells[i].x);
+    dist[i] = (uint8_t)mask_bitlen(cm[i]);
 }
 
 // pending shadow visits -> final sign/hits (no concurrent writers)
-__global__ void fold_kernel(uint2* __restrict__ cells, int64_t n, uint32_t h_max, uint32_t t_occ) {
+__global__ void fold_kernel(uint32_t* __restrict__ cy, int64_t n, uint32_t h_max, uint32_t t_occ) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t y = cells[i].y;
-    if (y >> kPendShift) cells[i].y = fold_meta(y, h_max, t_occ);
+    const uint32_t y = cy[i];
+    if (y >> kPendShift) cy[i] = fold_meta(y, h_max, t_occ);
   }
 }
 
 // distance cache of the z-range [z0, z1) only (chunked record loads)
-__global__ void rebuild_dist_range_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ dist, int64_t rows,
+__global__ void rebuild_dist_range_kernel(const uint32_t* __restrict__ cm, uint8_t* __restrict__ dist, int64_t rows,
                                           int64_t nzp, int64_t z0, int64_t z1) {
   const int64_t zc = z1 - z0, n = rows * zc;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / zc, off = row * nzp + z0 + (i - row * zc);
-    dist[off] = (uint8_t)mask_bitlen(cells[off].x);
+    dist[off] = (uint8_t)mask_bitlen(cm[off]);
   }
 }
 
-__global__ void decode_kernel(const uint2* __restrict__ cells, uint32_t* __restrict__ mask,
+__global__ void decode_kernel(const Cells cells, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits, int64_t n,
                               int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    const uint2 c = cells[row * nzp + z];
+    const uint2 c = cells.get(row * nzp + z);
     mask[i] = c.x;
     sign[i] = meta_sign(c.y);
     hits[i] = meta_hits(c.y);
@@ -96,13 +101,13 @@ __global__ void decode_kernel(const uint2* __restrict__ cells, uint32_t* __restr
 // Readout (grid.py:161-175). mode 0: popcount int32; 1: observed u8;
 // 2: signed distance f64 (+ observed u8). Decode = __popc of the mask
 // (grid.py:124-129, 166-167).
-__global__ void readout_kernel(const uint2* __restrict__ cells, int mode, int32_t* __restrict__ pop,
+__global__ void readout_kernel(const Cells cells, int mode, int32_t* __restrict__ pop,
                                uint8_t* __restrict__ obs, double* __restrict__ sdf, double vs,
                                int64_t n, int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    const uint2 c = cells[row * nzp + z];
+    const uint2 c = cells.get(row * nzp + z);
     const int len = __popc(c.x);
     if (mode == 0) {
       pop[i] = len;
@@ -119,13 +124,13 @@ __global__ void readout_kernel(const uint2* __restrict__ cells, int mode, int32_
   }
 }
 
-__global__ void count_kernel(const uint2* __restrict__ cells, int64_t n, int64_t nz, int64_t nzp,
+__global__ void count_kernel(const Cells cells, int64_t n, int64_t nz, int64_t nzp,
                              unsigned long long* __restrict__ out) {
   unsigned long long obs = 0, occ = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t row = i / nz, z = i - row * nz;
-    const uint2 c = cells[row * nzp + z];
+    const uint2 c = cells.get(row * nzp + z);
     obs += !(c.x == kFullMask && meta_hits(c.y) == 0);
     occ += meta_sign(c.y) == 0;
   }
@@ -144,7 +149,7 @@ __global__ void count_kernel(const uint2* __restrict__ cells, int64_t n, int64_t
 // the serialized record (reserved bytes 0); tile 32 (x) x 32 (z) per block at
 // fixed iy so both the cell reads (along z) and the record writes (along x)
 // are coalesced.
-__global__ void to_records_kernel(const uint2* __restrict__ cells, uint2* __restrict__ rec, int64_t nx,
+__global__ void to_records_kernel(const Cells cells, uint2* __restrict__ rec, int64_t nx,
                                   int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
   __shared__ uint2 tile[32][33];
   int64_t iy = blockIdx.y;
@@ -153,7 +158,7 @@ __global__ void to_records_kernel(const uint2* __restrict__ cells, uint2* __rest
   for (int k = ty; k < 32; k += 8) {
     int64_t ix = xb + k, iz = zb + tx;
     uint2 v = make_uint2(0, 0);
-    if (ix < nx && iz < zc) v = cells[(ix * ny + iy) * nzp + z0 + iz];
+    if (ix < nx && iz < zc) v = cells.get((ix * ny + iy) * nzp + z0 + iz);
     tile[k][tx] = v;
   }
   __syncthreads();
@@ -163,7 +168,7 @@ __global__ void to_records_kernel(const uint2* __restrict__ cells, uint2* __rest
   }
 }
 
-__global__ void from_records_kernel(uint2* __restrict__ cells, const uint2* __restrict__ rec, int64_t nx,
+__global__ void from_records_kernel(Cells cells, const uint2* __restrict__ rec, int64_t nx,
                                     int64_t ny, int64_t nzp, int64_t z0, int64_t zc) {
   __shared__ uint2 tile[32][33];
   int64_t iy = blockIdx.y;
@@ -181,16 +186,16 @@ __global__ void from_records_kernel(uint2* __restrict__ cells, const uint2* __re
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     int64_t ix = xb + k, iz = zb + tx;
-    if (ix < nx && iz < zc) cells[(ix * ny + iy) * nzp + z0 + iz] = tile[k][tx];
+    if (ix < nx && iz < zc) cells.put((ix * ny + iy) * nzp + z0 + iz, tile[k][tx]);
   }
 }
 
-__global__ void gather_kernel(const uint2* __restrict__ cells, const int64_t* __restrict__ xyz, int64_t n,
+__global__ void gather_kernel(const Cells cells, const int64_t* __restrict__ xyz, int64_t n,
                               XMap xm, int64_t ny, int64_t nzp, uint32_t* __restrict__ mask,
                               uint8_t* __restrict__ sign, uint8_t* __restrict__ hits) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 c = cells[(xm.local(xyz[3 * i]) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]];
+    const uint2 c = cells.get((xm.local(xyz[3 * i]) * ny + xyz[3 * i + 1]) * nzp + xyz[3 * i + 2]);
     mask[i] = c.x;
     sign[i] = meta_sign(c.y);
     hits[i] = meta_hits(c.y);
@@ -218,7 +223,7 @@ int dbt::fold_pending(dbt_grid* g, cudaStream_t st) {
     g->last_st = st;
   }
   if (!g->pend) return DBT_OK;
-  fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells, g->n_cells, (uint32_t)g->pend_h_max,
+  fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells.y, g->n_cells, (uint32_t)g->pend_h_max,
                                                       (uint32_t)g->pend_t_occ);
   DBT_CHECK_LAUNCH("fold_kernel");
   g->pend = false;
@@ -231,7 +236,7 @@ namespace {
 // every stamp certificate (host writes carry no stamp history)
 int finish_host_write(dbt_grid* g) {
   g->base_valid = false;  // replica base: host data replaced the records
-  rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells);
+  rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells.m, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
@@ -279,15 +284,14 @@ static int create_grid(const int64_t dims[3], double voxel_size, const double or
   }
   // +64 cells of slack: the sweep's aligned 4-cell chunks may read up to 3
   // cells past the last row of the slab (never written).
-  cudaError_t e = cudaMalloc(&g->cells, (size_t)(g->n_cells + 64) * sizeof(uint2));
+  // masks and meta words in one allocation: m = [0, n + 64), y = [n + 64, 2 (n + 64))
+  uint32_t* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, (size_t)(g->n_cells + 64) * 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) g->cells = Cells{base, base + (g->n_cells + 64)};
   if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
   if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cert + 63) / 32) * 4);
-#ifdef DBT_DIAG_RED_SPLIT
-  if (e == cudaSuccess) e = cudaMalloc(&g->diag_mask, (size_t)(g->n_cells + 64) * 4);
-  if (e == cudaSuccess) e = cudaMemset(g->diag_mask, 0xFF, (size_t)(g->n_cells + 64) * 4);
-#endif
   if (e != cudaSuccess) {
-    if (g->cells) cudaFree(g->cells);
+    if (g->cells.m) cudaFree(g->cells.m);
     delete g;
     return cuda_error(e, "cudaMalloc(voxel grid)");
   }
@@ -364,7 +368,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   dbt::prof_flush(g);
   for (auto e : g->event_pool) cudaEventDestroy(e);
-  void* dev[] = {g->cells,  g->dist,  g->stamped, g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
+  void* dev[] = {g->cells.m, g->dist,  g->stamped, g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_scan_off,
                  g->d_lcnt, g->d_stage, g->d_rowoff, g->d_exact_bits, g->d_exact_m0, g->d_base_hits, g->d_base_mask,
                  g->d_ray};
@@ -395,7 +399,7 @@ int dbt_grid_reset(dbt_grid* g) {
     DBT_CUDA(cudaDeviceSynchronize());
     g->last_st = g->stream;
   }
-  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 2), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
+  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
   g->pend = false;
   DBT_CHECK_LAUNCH("fill_cells_kernel");
   DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
@@ -438,7 +442,7 @@ int dbt_grid_upload(dbt_grid* g, const uint32_t* mask, const uint8_t* sign, cons
     DBT_CUDA(cudaMemcpyAsync(dm, mask + x * plane, 4 * n, cudaMemcpyHostToDevice, g->stream));
     DBT_CUDA(cudaMemcpyAsync(ds, sign + x * plane, n, cudaMemcpyHostToDevice, g->stream));
     DBT_CUDA(cudaMemcpyAsync(dh, hits + x * plane, n, cudaMemcpyHostToDevice, g->stream));
-    encode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, dm, ds, dh, n,
+    encode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells.off(x * g->ny * g->nzp), dm, ds, dh, n,
                                                          g->nz, g->nzp);
     DBT_CHECK_LAUNCH("encode_kernel");
   }
@@ -461,7 +465,7 @@ static int download_local(dbt_grid* g, int64_t l_begin, int64_t l_end, uint32_t*
     uint32_t* dm = (uint32_t*)st;
     uint8_t* ds = st + 4 * n;
     uint8_t* dh = ds + n;
-    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + (l_begin + x) * g->ny * g->nzp, dm, ds,
+    decode_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells.off((l_begin + x) * g->ny * g->nzp), dm, ds,
                                                          dh, n, g->nz, g->nzp);
     DBT_CHECK_LAUNCH("decode_kernel");
     DBT_CUDA(cudaMemcpyAsync(mask + x * plane, dm, 4 * n, cudaMemcpyDeviceToHost, g->stream));
@@ -507,7 +511,7 @@ static int readout(dbt_grid* g, int mode, int32_t* pop, uint8_t* obs, double* sd
     int32_t* dp = (int32_t*)st;
     double* dsdf = (double*)st;
     uint8_t* dob = mode == 2 ? st + 8 * n : st;
-    readout_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells + x * g->ny * g->nzp, mode, dp, dob,
+    readout_kernel<<<grid_blocks(n), 256, 0, g->stream>>>(g->cells.off(x * g->ny * g->nzp), mode, dp, dob,
                                                           dsdf, g->vs, n, g->nz, g->nzp);
     DBT_CHECK_LAUNCH("readout_kernel");
     if (mode == 0) {
@@ -631,7 +635,7 @@ int dbt_grid_from_records_range(dbt_grid* g, int64_t z_begin, int64_t z_end, con
   // distance cache of the written range; every stamp certificate dropped
   if (z_end > z_begin) {
     rebuild_dist_range_kernel<<<grid_blocks(plane * (z_end - z_begin)), 256, 0, g->stream>>>(
-        g->cells, g->dist, plane, g->nzp, z_begin, z_end);
+        g->cells.m, g->dist, plane, g->nzp, z_begin, z_end);
     DBT_CHECK_LAUNCH("rebuild_dist_range_kernel");
   }
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));

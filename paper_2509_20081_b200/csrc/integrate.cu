@@ -79,7 +79,7 @@ struct PrepArgs {
   uint64_t epoch;      // hash-key epoch tag (bits 52..63); stale slots count as empty
   // fused shadow update (no first-return, small shadow sets)
   int fuse_shadow;
-  uint2* cells;
+  Cells cells;
   const int8_t* sxyz;
   const int32_t* sstart;
   int64_t x0, x1, nzp;
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
           const char4 o = reinterpret_cast<const char4*>(a.sxyz)[b0 + k];
           const int64_t lgx = a.xm.local(cx + o.x);
           if (lgx >= 0)
-            shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+            shadow_add(&a.cells.y[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)], (uint32_t)a.h_max,
                        (uint32_t)a.t_occ);
         }
       }
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
 }
 
 struct ShadowArgs {
-  uint2* cells;
+  Cells cells;
   const uint64_t* center;
   const uint16_t* bin;
   const uint32_t* slot;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
     unpack_center(c, cx, cy, cz);
     const int64_t lgx = a.xm.local(cx + o.x);
     if (lgx < 0) continue;
-    shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+    shadow_add(&a.cells.y[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)], (uint32_t)a.h_max,
                (uint32_t)a.t_occ);
   }
 }
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
         unpack_center(c, cx, cy, cz);
         const int64_t lgx = a.xm.local(cx + o.x);
         if (lgx >= 0)
-          shadow_add(&a.cells[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)].y, (uint32_t)a.h_max,
+          shadow_add(&a.cells.y[(lgx * a.ny + (cy + o.y)) * a.nzp + (cz + o.z)], (uint32_t)a.h_max,
                      (uint32_t)a.t_occ);
       }
     }
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
 }
 
 struct SweepArgs {
-  uint2* cells;
+  Cells cells;
   uint8_t* dist;
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
             const uint32_t lt = b < 4 ? lt0 : lt1;
             if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
             const uint32_t d = (((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-            atomicAnd(&a.cells[off[k] + b].x, run_mask_of((int)d));  // RED.AND, fire and forget
+            atomicAnd(&a.cells.m[off[k] + b], run_mask_of((int)d));  // RED.AND, fire and forget
             ++changed;
           }
           // the chunk's cache word in one store (see sweep_cull_kernel)
@@ -648,8 +648,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 // does. Rows of a heavy centre (a fresh surface: nothing culled) thus spread
 // over the block instead of serialising one warp.
 struct CullArgs {
-  uint2* cells;
-  uint32_t* dmask;  // DBT_DIAG_RED_SPLIT
+  Cells cells;
   uint8_t* dist;
   const uint64_t* uniq;
   LaunchCounters* lc;
@@ -913,10 +912,8 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
           const uint32_t lt = b < 4 ? lt0 : lt1;
           if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
           const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-#if defined(DBT_DIAG_RED_SPLIT)
-          atomicAnd(&a.dmask[off + b], run_mask_of((int)d));
-#elif !defined(DBT_DIAG_NO_RED)
-          atomicAnd(&a.cells[off + b].x, run_mask_of((int)d));
+#if !defined(DBT_DIAG_NO_RED)
+          atomicAnd(&a.cells.m[off + b], run_mask_of((int)d));
 #endif
           ++changed;
         }
@@ -1479,7 +1476,6 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     }
     CullArgs wa;
     wa.cells = g->cells;
-    wa.dmask = g->diag_mask;
     wa.dist = g->dist;
     wa.uniq = g->d_uniq;
     wa.lc = g->d_lcnt;

@@ -62,16 +62,16 @@ struct MeshTab {
   int64_t eoff[12];       // storage offset of the edge's lower lattice point
 };
 
-// one warp per (x, y) row, 4 z per lane: 32-byte record loads, 4-byte flag stores
-__global__ void mesh_flags_kernel(const uint2* __restrict__ cells, uint8_t* __restrict__ flags, int64_t rows,
+// one warp per (x, y) row, 4 z per lane: 16-byte mask and meta loads, 4-byte flag stores
+__global__ void mesh_flags_kernel(const Cells cells, uint8_t* __restrict__ flags, int64_t rows,
                                   int64_t nz, int64_t nzp, uint64_t ins_free, uint64_t ins_occ) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
     for (int64_t z = 4 * lane; z < nzp; z += 128) {
-      const uint4* q = reinterpret_cast<const uint4*>(cells + r * nzp + z);
-      const uint4 c01 = q[0], c23 = q[1];
-      const uint32_t mx[4] = {c01.x, c01.z, c23.x, c23.z}, my[4] = {c01.y, c01.w, c23.y, c23.w};
+      const uint4 qm = *reinterpret_cast<const uint4*>(cells.m + r * nzp + z);
+      const uint4 qy = *reinterpret_cast<const uint4*>(cells.y + r * nzp + z);
+      const uint32_t mx[4] = {qm.x, qm.y, qm.z, qm.w}, my[4] = {qy.x, qy.y, qy.z, qy.w};
       uint32_t w = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -214,8 +214,8 @@ __device__ __forceinline__ int64_t edge_rank(const uint64_t* __restrict__ fw,
 }
 
 // field value of a voxel: sigma * (popcount * voxel_size) (grid.py:170-175)
-__device__ __forceinline__ double field_at(const uint2* __restrict__ cells, int64_t i, double vs) {
-  const uint2 c = cells[i];
+__device__ __forceinline__ double field_at(const Cells cells, int64_t i, double vs) {
+  const uint2 c = cells.get(i);
   const double d = __dmul_rn((double)__popc(c.x), vs);
   return __dmul_rn(meta_sign(c.y) == 0 ? -1.0 : 1.0, d);
 }
@@ -226,7 +226,7 @@ struct VertArgs {
 };
 
 // mesher.py:91-109, one thread per 8 lattice points
-__global__ void mesh_vert_kernel(const uint2* __restrict__ cells, const uint64_t* __restrict__ fw,
+__global__ void mesh_vert_kernel(const Cells cells, const uint64_t* __restrict__ fw,
                                  const unsigned long long* __restrict__ pre, VertArgs a,
                                  double* __restrict__ vert) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.n_words;

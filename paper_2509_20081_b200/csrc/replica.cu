@@ -26,29 +26,29 @@ using namespace dbt;
 
 namespace {
 
-__global__ void replica_mark_kernel(const uint2* __restrict__ cells, uint32_t* __restrict__ bmask,
+__global__ void replica_mark_kernel(const Cells cells, uint32_t* __restrict__ bmask,
                                     uint8_t* __restrict__ bhits, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 c = cells[i];
+    const uint2 c = cells.get(i);
     bmask[i] = c.x;
     bhits[i] = meta_hits(c.y);
   }
 }
 
 // compact C-order buffers over (nx, ny, nz) (no z padding)
-__global__ void replica_pack_kernel(const uint2* __restrict__ cells, const uint8_t* __restrict__ bhits,
+__global__ void replica_pack_kernel(const Cells cells, const uint8_t* __restrict__ bhits,
                                     uint8_t* __restrict__ mlen, uint8_t* __restrict__ sign,
                                     __half* __restrict__ delta, int64_t n, int64_t nz, int64_t nzp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / nz, v = row * nzp + (i - row * nz);
-    const uint2 c = cells[v];
+    const uint2 c = cells.get(v);
     mlen[i] = (uint8_t)mask_bitlen(c.x);
     sign[i] = meta_sign(c.y);
     delta[i] = __int2half_rn((int)meta_hits(c.y) - (int)bhits[v]);
   }
 }
 
-__global__ void replica_apply_kernel(uint2* __restrict__ cells, uint8_t* __restrict__ dist,
+__global__ void replica_apply_kernel(Cells cells, uint8_t* __restrict__ dist,
                                      uint32_t* __restrict__ bmask, uint8_t* __restrict__ bhits,
                                      const uint8_t* __restrict__ mlen, const uint8_t* __restrict__ sign,
                                      const __half* __restrict__ delta, int64_t n, int64_t nz, int64_t nzp, int h_max,
@@ -61,7 +61,7 @@ __global__ void replica_apply_kernel(uint2* __restrict__ cells, uint8_t* __restr
     const int d = (int)fminf(__half2float(delta[i]), 4096.f);
     const int h = h0 >= h_max ? h0 : min(h0 + d, h_max);
     const uint32_t s = (d > 0 && h >= t_occ) ? 0u : (uint32_t)sign[i];
-    cells[v] = make_uint2(m, make_meta(s, (uint32_t)h));
+    cells.put(v, make_uint2(m, make_meta(s, (uint32_t)h)));
     dist[v] = (uint8_t)mask_bitlen(m);
     bmask[v] = m;
     bhits[v] = (uint8_t)h;
