@@ -459,7 +459,9 @@ __global__ void __launch_bounds__(256) shadow_kernel(ShadowArgs a) {
 __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
   __shared__ uint64_t s_c[256];
   __shared__ uint16_t s_b[256];
-  const int per = 256 >> a.log2s;
+  // returns per tile: 256 >> log2s (one visit per thread), at least 64 (the
+  // binning phase keeps two warps busy; the visits then take several passes)
+  const int per = max(64, 256 >> a.log2s);
   const int smask = (1 << a.log2s) - 1;
   const int64_t tiles = (a.n + per - 1) / per;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -490,9 +492,10 @@ __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
       s_b[threadIdx.x] = bin;
     }
     __syncthreads();
-    const int j = threadIdx.x >> a.log2s, k = threadIdx.x & smask;
-    const uint64_t c = j < per ? s_c[j] : kEmptyKey;
-    if (c != kEmptyKey) {
+    for (int pair = threadIdx.x; pair < (per << a.log2s); pair += 256) {
+      const int j = pair >> a.log2s, k = pair & smask;
+      const uint64_t c = s_c[j];
+      if (c == kEmptyKey) continue;
       const int b = s_b[j];
       const int st = a.sstart[b];
       if (k < a.sstart[b + 1] - st) {
@@ -1313,11 +1316,14 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   int shadow_l2 = 0;
   while ((1 << shadow_l2) < b->max_shadow) ++shadow_l2;
   // bins in the shadow kernel (off the critical path) for a single-scan
-  // sized launch whose tile of 256 threads still bins >= 32 returns; big
-  // batched launches keep them in prep, where the latency-bound shadow tile
-  // loop would become the critical path (same-box A/B, config 5: 8 scans per
-  // launch +7 %, 32 scans +16 % with the bins in prep)
-  const bool shadow_bins = b->max_shadow > 0 && !fuse_shadow && shadow_l2 <= 3 && n <= (1 << 19);
+  // sized launch (tiles of >= 64 returns, |S| <= 32); big batched launches
+  // keep them in prep, where the latency-bound shadow tile loop would become
+  // the critical path (same-box A/B, config 5: 8 scans per launch +7 %, 32
+  // scans +16 % with the bins in prep)
+#ifndef DBT_SHADOW_BIN_MAX_L2
+#define DBT_SHADOW_BIN_MAX_L2 5
+#endif
+  const bool shadow_bins = b->max_shadow > 0 && !fuse_shadow && shadow_l2 <= DBT_SHADOW_BIN_MAX_L2 && n <= (1 << 19);
 
   PrepArgs pa;
   pa.pts = d_pts;
@@ -1426,7 +1432,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     int64_t total = n << l2;
     unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64);
     if (shadow_bins) {
-      const int64_t tiles = (n + (256 >> l2) - 1) >> (8 - l2);
+      const int per = std::max(64, 256 >> l2);
+      const int64_t tiles = (n + per - 1) / per;
       sa.ray = g->d_ray;
       sa.b_az = b->b_az;
       sa.b_el = b->b_el;
