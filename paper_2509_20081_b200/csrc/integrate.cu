@@ -910,6 +910,7 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
       const uint32_t lt1 = ((w[r][j].y | 0x80808080u) - d8[r][j].y) & 0x80808080u;
       if (lt0 | lt1) {
         const int64_t off = rb[r] + 8 * (cb[r] + j);
+#if defined(DBT_RED_SINGLE)
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
           const uint32_t lt = b < 4 ? lt0 : lt1;
@@ -920,6 +921,29 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
 #endif
           ++changed;
         }
+#else
+        // adjacent voxels (2p, 2p+1) of the chunk in one 64-bit RED.AND (the
+        // row start is a multiple of 8 voxels, so the pair is 8-byte
+        // aligned); a voxel of the pair that is not lowered ANDs all ones.
+        // Half the RED instructions and L2 sector operations of one RED per
+        // voxel on dense (fresh) rows.
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t lt = p < 2 ? lt0 : lt1, dw = p < 2 ? d8[r][j].x : d8[r][j].y;
+          const int s0 = 16 * (p & 1);  // byte 2p (mod 4) of the word
+          const bool l0 = (lt >> (s0 + 7)) & 1u, l1 = (lt >> (s0 + 15)) & 1u;
+          if (!(l0 | l1)) continue;
+          // run_mask(d) = all ones >> (32 - d), d = table byte - 1 (clamped
+          // funnel shift: d = 0 gives 0); shift 0 (all ones) when not lowered
+          const uint32_t lo = __funnelshift_rc(kFullMask, 0u, l0 ? 33u - ((dw >> s0) & 0xFFu) : 0u);
+          const uint32_t hi = __funnelshift_rc(kFullMask, 0u, l1 ? 33u - ((dw >> (s0 + 8)) & 0xFFu) : 0u);
+#if !defined(DBT_DIAG_NO_RED)
+          atomicAnd(reinterpret_cast<unsigned long long*>(a.cells.m + off + 2 * p),
+                    ((unsigned long long)hi << 32) | lo);
+#endif
+          changed += (unsigned)l0 + (unsigned)l1;
+        }
+#endif
         // the chunk's cache word in one store: lowered bytes take d (the
         // table byte - 1, never borrows), the others the value read above.
         // A concurrent lowering overwritten here only leaves its byte
