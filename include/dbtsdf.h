@@ -266,6 +266,27 @@ DBT_API int dbt_replica_mark(dbt_grid* g);
 DBT_API int dbt_replica_pack(dbt_grid* g, uint8_t* mask_len, uint8_t* sign, uint16_t* delta_f16, void* stream);
 DBT_API int dbt_replica_apply(dbt_grid* g, const uint8_t* mask_len_min, const uint8_t* sign_min,
                       const uint16_t* delta_sum_f16, int32_t h_max, int32_t t_occ, void* stream);
+/* Sparse merge: only the 16^3 bricks within a kernel radius of a return some
+ * rank applied since the last mark/merge travel (prep_kernel flags the brick
+ * of every applied centre).
+ *   bricks      : number of brick flags (nbx*nby*nbz, 16^3 bricks) and this
+ *                 rank's reach (largest kernel radius R integrated since the
+ *                 last merge)
+ *   dirty       : copy this rank's flags (u8 per brick) into `flags` (device)
+ *   (caller: all-reduce MAX of the flags and of the reach over replicas)
+ *   select      : dilate the reduced flags by ceil(reach/16) bricks and list
+ *                 the selected bricks in brick order (synchronous; *n_sel)
+ *   pack_bricks : mask_len_sign = [n_sel*4096 mask bit lengths | n_sel*4096
+ *                 signs] (u8), delta_f16 = n_sel*4096 hit deltas
+ *   (caller: all-reduce MIN mask_len_sign, SUM delta_f16)
+ *   apply_bricks: combine into the selected bricks, re-mark, clear the flags.
+ * Bricks nobody touched are equal on every replica already. */
+DBT_API int dbt_replica_bricks(dbt_grid* g, int64_t* n_bricks, int32_t* reach);
+DBT_API int dbt_replica_dirty(dbt_grid* g, uint8_t* flags, void* stream);
+DBT_API int dbt_replica_select(dbt_grid* g, const uint8_t* flags, int32_t reach, int64_t* n_sel, void* stream);
+DBT_API int dbt_replica_pack_bricks(dbt_grid* g, uint8_t* mask_len_sign, uint16_t* delta_f16, void* stream);
+DBT_API int dbt_replica_apply_bricks(dbt_grid* g, const uint8_t* mask_len_sign_min, const uint16_t* delta_sum_f16,
+                             int32_t h_max, int32_t t_occ, void* stream);
 
 /* pinned host buffers for callers without a CUDA runtime of their own */
 DBT_API int dbt_host_alloc(int64_t bytes, void** out);

@@ -119,6 +119,11 @@ SIGNATURES = {
     "dbt_replica_mark": (ctypes.c_int, [_vp]),
     "dbt_replica_pack": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "dbt_replica_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
+    "dbt_replica_bricks": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]),
+    "dbt_replica_dirty": (ctypes.c_int, [_vp, _vp, _vp]),
+    "dbt_replica_select": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _vp]),
+    "dbt_replica_pack_bricks": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dbt_replica_apply_bricks": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
     "dbt_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
     "dbt_host_free": (ctypes.c_int, [_vp]),
 }

@@ -60,6 +60,7 @@ constexpr int64_t kMaxDim = (1 << kCenterBits) - 1;
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kMaxK = 31;          // kernel edge supported by the sweep templates
 constexpr int kMaxScansPerLaunch = 4096;
+constexpr int kBrickShift = 4;     // replica dirty bricks: 16^3 voxels
 
 __host__ __device__ inline uint32_t make_meta(uint32_t sign, uint32_t hits) { return (sign & 0xFFu) | ((hits & 0xFFu) << 8); }
 __host__ __device__ inline uint8_t meta_sign(uint32_t m) { return (uint8_t)(m & 0xFFu); }
@@ -210,6 +211,14 @@ struct dbt_grid {
   uint8_t* d_base_hits = nullptr;           // replica mode: hits at the last merge (replica.cu)
   uint32_t* d_base_mask = nullptr;          // replica mode: masks at the last merge
   bool base_valid = false;                  // d_base_hits describes the current records' base
+  // replica mode: one flag per 16^3 brick holding the centre of a return
+  // applied since the last mark/merge (set by prep_kernel), so a merge moves
+  // only the bricks within a kernel radius of some rank's returns
+  uint8_t* d_dirty = nullptr;
+  int64_t dbx = 0, dby = 0, dbz = 0;        // brick grid (ceil(n / 16) per axis)
+  int dirty_reach = 0;                      // largest kernel radius R integrated since the last merge
+  int32_t* d_sel = nullptr;                 // selected bricks of the pending merge (dbt_replica_select)
+  int64_t n_sel = 0, cap_sel = 0;
   int64_t n_cells = 0;                      // lx*ny*nzp
   cudaStream_t stream = nullptr;
   bool own_stream = true;

@@ -30,6 +30,7 @@
 #include <chrono>
 
 #include <mutex>
+#include <thread>
 
 #include "engine.cuh"
 #include "svml_emu.cuh"
@@ -91,6 +92,9 @@ struct PrepArgs {
   uint32_t* stamped;
   int bins;     // direction bins here (else rays out, binned in shadow_bin_kernel)
   double* ray;  // n x 3 map-frame rays (bins == 0)
+  // replica mode: dirty flag of the 16^3 brick holding each applied centre
+  uint8_t* dirty;
+  int64_t dby, dbz;
 };
 
 constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
@@ -270,6 +274,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         a.ray[3 * i + 2] = rz;
       }
       packed = pack_center(cx, cy, cz);
+      if (a.dirty)  // replica merge bookkeeping (idempotent plain store)
+        a.dirty[((cx >> kBrickShift) * a.dby + (cy >> kBrickShift)) * a.dbz + (cz >> kBrickShift)] = 1;
       // a part of a sharded grid ignores returns whose cube misses its planes
       // (still counted; the first-return choice below stays global)
       if (a.claim && relevant) {
@@ -280,7 +286,16 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         // the centres whose cube touches its planes).
         const int64_t cidx = (cx * a.ny + cy) * a.nzp + cz;
         const uint32_t bit = 1u << (cidx & 31);
+#ifdef DBT_HINT_CLAIM_EL
+        uint32_t prev;
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
+                     : "=r"(prev) : "l"(a.stamped + (cidx >> 5)), "r"(bit), "l"(pol) : "memory");
+        claimed = (prev & bit) != 0;
+#else
         claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
+#endif
         append = !claimed;
       }
       // the hash table dedups centres for the sweep when certificates are not
@@ -663,7 +678,57 @@ struct CullArgs {
   XMap xm;
 };
 
+// L2 residency hints for the culling sweep: certificate words and
+// distance-cache chunks are re-read by neighbouring centres, so their loads
+// carry an evict_last policy (same-box A/B against no hints: config 4 +2.5 %,
+// config 3 +5 %, config 2 +2.5 %). Tried and not kept: evict_first on the
+// record RED.ANDs (config 4 -1.5 %), evict_last on prep's certificate claims
+// (neutral).
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_cert(const uint32_t* p) {
+#ifndef DBT_NO_HINT_CERT_EL
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_policy_last()));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+__device__ __forceinline__ uint2 ld_dist(const uint8_t* p) {
+#ifndef DBT_NO_HINT_DIST_EL
+  uint2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_policy_last()));
+  return v;
+#else
+  return *reinterpret_cast<const uint2*>(p);
+#endif
+}
+__device__ __forceinline__ void red_and64(uint32_t* p, unsigned long long v) {
+#ifdef DBT_HINT_RED_EF
+  asm volatile("red.global.and.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(l2_policy_first()) : "memory");
+#else
+  atomicAnd(reinterpret_cast<unsigned long long*>(p), v);
+#endif
+}
+
 constexpr int kFar = 1 << 20;
+// phase A row emission: balanced over the warp's lanes when
+// ceil(rows / 32) * NUM < max rows per column * DEN (A/B knobs)
+#ifndef DBT_ROWS_BAL_NUM
+#define DBT_ROWS_BAL_NUM 5
+#endif
+#ifndef DBT_ROWS_BAL_DEN
+#define DBT_ROWS_BAL_DEN 3
+#endif
 constexpr int kPlaneGatherBelow = 8;  // certified adjacent centres below which plane neighbours are read
 // centres per block batch (one warp each). Same-box A/B at 64 registers
 // (4 resident blocks of 8 warps): 8 vs 4 config 2 +8.5 %, config 3 +11 %,
@@ -679,13 +744,27 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
   return (uint64_t)(rbase >> 3) | ((uint64_t)c0 << 37) | ((uint64_t)c1 << 39) | ((uint64_t)drow << 41);
 }
 
+// Row-task writers of phase A. Put64: one 64-bit task per surviving row
+// (absolute row start, chunk range, d-table row); kEmptyKey for a row whose
+// dz interval is empty.
+struct Put64 {
+  uint64_t* queue;
+  __device__ __forceinline__ void operator()(int i, bool valid, int, int c0, int c1, int64_t rbase,
+                                             const uint16_t* rowd, int drow0) const {
+    queue[i] = valid ? pack_task(rbase, c0, c1, drow0 + __ldg(rowd)) : kEmptyKey;
+  }
+};
+struct NoInfo {
+  __device__ __forceinline__ void operator()(int, int64_t, int64_t, int) const {}
+};
+
 // Phase A of the culling sweep for one centre (one warp): neighbour
 // certificates -> per-lane dy interval and per-row dz interval -> the
 // surviving row tasks, reserved as one range of `total` slots through *q_n
 // (lane 0) and written with put(slot, task) (kEmptyKey for a row whose dz
 // interval is empty).
-template <typename Put>
-__device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put) {
+template <typename Put, typename Info>
+__device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put, Info info) {
   const int R = a.R, K = a.K;
   const int64_t sx = a.ny * a.nzp;
   const uint16_t* rowd = a.rowd;
@@ -698,8 +777,8 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     const int64_t gx = cx + na;  // certificates: global planes (boundary discard keeps it in the grid)
     {
       const int64_t idx = (gx * a.ny + (cy + nbb)) * a.nzp + (cz - 1);
-      const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-      const uint32_t w1 = ((idx & 31) > 29) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+      const uint32_t w0 = ld_cert(a.stamped + (idx >> 5));
+      const uint32_t w1 = ((idx & 31) > 29) ? ld_cert(a.stamped + (idx >> 5) + 1) : 0u;
       nb3 = (__funnelshift_r(w0, w1, (int)(idx & 31)) & 7u) << (3 * lane);
     }
   }
@@ -717,13 +796,13 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     const int64_t qx = along_x ? cx + sg * k : cx, qy = along_x ? cy : cy + sg * k;
     if (qy >= 0 && qy < a.ny && qx >= 0 && qx < a.nx) {
       const int64_t idx = (qx * a.ny + qy) * a.nzp + cz;
-      ax = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
+      ax = ((ld_cert(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << (lane - 9);
     }
   } else if (lane == 25 && cz >= 5 && cz + 5 < a.nzp) {  // padding bits are never set
     {
       const int64_t idx = (cx * a.ny + cy) * a.nzp + (cz - 5);
-      const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-      const uint32_t w1 = ((idx & 31) > 21) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+      const uint32_t w0 = ld_cert(a.stamped + (idx >> 5));
+      const uint32_t w1 = ((idx & 31) > 21) ? ld_cert(a.stamped + (idx >> 5) + 1) : 0u;
       const uint32_t b11 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x7FFu;  // bit i: cz - 5 + i
       const uint32_t up = (b11 >> 7) & 0xFu;                                // cz+2 .. cz+5
       const uint32_t dn = __brev(b11 & 0xFu) >> 28;                         // cz-2 .. cz-5
@@ -750,15 +829,15 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
       const int64_t qy = cy + pb, qx = cx + pa;
       if (qy >= 0 && qy < a.ny && qx >= 0 && qx < a.nx) {
         const int64_t idx = (qx * a.ny + qy) * a.nzp + cz;
-        plb = ((__ldcg(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
+        plb = ((ld_cert(a.stamped + (idx >> 5)) >> (idx & 31)) & 1u) << lane;
       }
     } else if (lane < 16 && cz >= 2 && cz + 2 < a.nzp) {
       const int pa = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
       const int64_t qx = cx + pa;
       if (qx >= 0 && qx < a.nx) {
         const int64_t idx = (qx * a.ny + cy) * a.nzp + (cz - 2);
-        const uint32_t w0 = __ldcg(a.stamped + (idx >> 5));
-        const uint32_t w1 = ((idx & 31) > 27) ? __ldcg(a.stamped + (idx >> 5) + 1) : 0u;
+        const uint32_t w0 = ld_cert(a.stamped + (idx >> 5));
+        const uint32_t w1 = ((idx & 31) > 27) ? ld_cert(a.stamped + (idx >> 5) + 1) : 0u;
         const uint32_t b5 = __funnelshift_r(w0, w1, (int)(idx & 31)) & 0x1Fu;  // bit i: cz - 2 + i
         const uint32_t cp1 = (b5 >> 3) & 1u, cm1 = (b5 >> 1) & 1u, cp2 = (b5 >> 4) & 1u, cm2 = b5 & 1u;
         uint32_t xz = 0;
@@ -852,35 +931,77 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
   qb = __shfl_sync(0xffffffffu, qb, 0);
   const int zhi0 = min(R, max(mp[1], -R + 1) - 1), zlo0 = max(-R, min(mm[1], R - 1) + 1);
   const int drow0 = sh * a.nd * a.CH;
-  const uint16_t* rowd_dx = rowd + (dx + R) * K + R;
-  for (int k = 0; k < cnt; ++k) {
-    const int rdy = ylo + k;
-    // dz interval: delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1),
-    // delta_z = -1 ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only
-    // when v is in their y-window)
-    int zhi = zhi0, zlo = zlo0;
+  info(lane, xbase, cbase, drow0);
+  // one row of column `col` (kernel x-offset col - R): its dz interval —
+  // delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1), delta_z = -1
+  // ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only when v is in
+  // their y-window) — and its task
+  auto emit = [&](int slot, int col, int rdy, int z_hi0, int z_lo0, int mp0, int mm0, int mp2, int mm2,
+                  int64_t xb) {
+    int zhi = z_hi0, zlo = z_lo0;
     if (rdy <= R - 1) {  // b = -1
-      zhi = min(zhi, max(mp[0] + rdy, -R + 1) - 1);
-      zlo = max(zlo, min(mm[0] - rdy, R - 1) + 1);
+      zhi = min(zhi, max(mp0 + rdy, -R + 1) - 1);
+      zlo = max(zlo, min(mm0 - rdy, R - 1) + 1);
     }
     if (rdy >= -R + 1) {  // b = +1
-      zhi = min(zhi, max(mp[2] - rdy, -R + 1) - 1);
-      zlo = max(zlo, min(mm[2] + rdy, R - 1) + 1);
+      zhi = min(zhi, max(mp2 - rdy, -R + 1) - 1);
+      zlo = max(zlo, min(mm2 + rdy, R - 1) + 1);
     }
-    uint64_t task = kEmptyKey;
-    if (zlo <= zhi) {
-      const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
-      task = pack_task(xbase + cbase + rdy * a.nzp, c0, c1, drow0 + __ldg(rowd_dx + rdy));
+    const bool valid = zlo <= zhi;
+    const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
+    put(qb + slot, valid, rdy, c0, c1, xb + cbase + rdy * a.nzp, rowd + col * K + R + rdy, drow0);
+  };
+  const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+  if (((total + 31) >> 5) * DBT_ROWS_BAL_NUM < cmax * DBT_ROWS_BAL_DEN) {
+    // few rows spread unevenly over the columns (a culled centre): the
+    // warp's lanes take consecutive rows of the whole list, each finding its
+    // column by a binary search over the inclusive prefix sums, instead of
+    // every lane walking its own column (the loop would run max(cnt) times
+    // with most lanes idle)
+    const int incl = pre + cnt;
+    for (int base = 0; base < total; base += 32) {
+      const int j = base + lane;
+      int col = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, col + step - 1);
+        if (v <= j) col += step;
+      }
+      col &= 31;
+      const int o_ylo = __shfl_sync(0xffffffffu, ylo, col), o_pre = __shfl_sync(0xffffffffu, pre, col);
+      const int o_zhi0 = __shfl_sync(0xffffffffu, zhi0, col), o_zlo0 = __shfl_sync(0xffffffffu, zlo0, col);
+      const int o_mp0 = __shfl_sync(0xffffffffu, mp[0], col), o_mm0 = __shfl_sync(0xffffffffu, mm[0], col);
+      const int o_mp2 = __shfl_sync(0xffffffffu, mp[2], col), o_mm2 = __shfl_sync(0xffffffffu, mm[2], col);
+      const int64_t o_xb = __shfl_sync(0xffffffffu, xbase, col);
+      if (j < total) emit(j, col, o_ylo + (j - o_pre), o_zhi0, o_zlo0, o_mp0, o_mm0, o_mp2, o_mm2, o_xb);
     }
-    put(qb + pre + k, task);
+  } else {
+    // each lane writes its own column's rows at its prefix offset
+    for (int k = 0; k < cnt; ++k) emit(pre + k, lane, ylo + k, zhi0, zlo0, mp[0], mm[0], mp[2], mm[2], xbase);
   }
 }
 
-// Phase B of the culling sweep: one thread, two row tasks (kEmptyKey = none)
+// A decoded row task: row start (cells), first / last chunk (c1 = -1: no
+// row), d-table row offset.
+struct RowTask {
+  int64_t rb;
+  int c0, c1, drow;
+};
+
+__device__ __forceinline__ RowTask decode_task64(uint64_t task) {
+  RowTask r;
+  r.rb = (int64_t)(task & ((1ull << 37) - 1)) << 3;
+  r.c0 = (int)((task >> 37) & 3);
+  r.c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
+  r.drow = (int)(task >> 41);
+  return r;
+}
+
+// Phase B of the culling sweep: one thread, two row tasks (c1 = -1: none)
 // with their chunk loads in flight together; a cached byte above the row's
 // run length marks a voxel this centre lowers: RED.AND into the record, and
 // the chunk's cache word written back once.
-__device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t tasks[2], unsigned long long& changed,
+__device__ __forceinline__ void sweep_rows2(const CullArgs& a, const RowTask rows[2], unsigned long long& changed,
                                             unsigned long long& rows_done) {
   const uint2* dtab = a.dtab;
   uint2 w[2][4], d8[2][4];
@@ -888,18 +1009,17 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
   int cb[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const uint64_t task = tasks[r];
-    rows_done += task != kEmptyKey;
-    rb[r] = (int64_t)(task & ((1ull << 37) - 1)) << 3;
-    const int c0 = (int)((task >> 37) & 3), c1 = task != kEmptyKey ? (int)((task >> 39) & 3) : -1;
+    rows_done += rows[r].c1 >= 0;
+    rb[r] = rows[r].rb;
+    const int c0 = rows[r].c0, c1 = rows[r].c1;
     cb[r] = c0;
-    const uint2* drow = dtab + (int)(task >> 41);
+    const uint2* drow = dtab + rows[r].drow;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool act = c0 + j <= c1;
       d8[r][j] = act ? __ldg(drow + c0 + j) : make_uint2(0x40404040u, 0x40404040u);
       // inactive chunks read one shared dummy sector
-      w[r][j] = *reinterpret_cast<const uint2*>(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
+      w[r][j] = ld_dist(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
     }
   }
 #pragma unroll
@@ -938,8 +1058,7 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const uint64_t ta
           const uint32_t lo = __funnelshift_rc(kFullMask, 0u, l0 ? 33u - ((dw >> s0) & 0xFFu) : 0u);
           const uint32_t hi = __funnelshift_rc(kFullMask, 0u, l1 ? 33u - ((dw >> (s0 + 8)) & 0xFFu) : 0u);
 #if !defined(DBT_DIAG_NO_RED)
-          atomicAnd(reinterpret_cast<unsigned long long*>(a.cells.m + off + 2 * p),
-                    ((unsigned long long)hi << 32) | lo);
+          red_and64(a.cells.m + off + 2 * p, ((unsigned long long)hi << 32) | lo);
 #endif
           changed += (unsigned)l0 + (unsigned)l1;
         }
@@ -986,7 +1105,7 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
     const int64_t item = batch0 + warp;
     if (batch0 >= n_items) break;
     if (item < n_items) {
-      cull_centre(a, a.uniq[item], lane, &q_n, [&](int i, uint64_t t) { queue[i] = t; });
+      cull_centre(a, a.uniq[item], lane, &q_n, Put64{queue}, NoInfo{});
     }
     __syncthreads();
     // next batch index: its atomic overlaps phase B
@@ -995,9 +1114,9 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
     // two rows' chunk loads in flight per thread =====
     const int nq = q_n;
     for (int i = threadIdx.x; i < nq; i += 2 * blockDim.x) {
-      const uint64_t tasks[2] = {i < nq ? queue[i] : kEmptyKey,
-                                 i + (int)blockDim.x < nq ? queue[i + blockDim.x] : kEmptyKey};
-      sweep_rows2(a, tasks, changed, rows_done);
+      const RowTask rows[2] = {decode_task64(i < nq ? queue[i] : kEmptyKey),
+                               decode_task64(i + (int)blockDim.x < nq ? queue[i + blockDim.x] : kEmptyKey)};
+      sweep_rows2(a, rows, changed, rows_done);
     }
     __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
@@ -1038,12 +1157,12 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_wa
     for (int k = 0; k < G && cur + k < n_items; ++k) {
       if (lane == 0) q_n[warp] = 0;
       __syncwarp();
-      cull_centre(a, a.uniq[cur + k], lane, &q_n[warp], [&](int i, uint64_t t) { queue[i] = t; });
+      cull_centre(a, a.uniq[cur + k], lane, &q_n[warp], Put64{queue}, NoInfo{});
       __syncwarp();
       const int nq = q_n[warp];
       for (int i = lane; i < nq; i += 64) {
-        const uint64_t tasks[2] = {queue[i], i + 32 < nq ? queue[i + 32] : kEmptyKey};
-        sweep_rows2(a, tasks, changed, rows_done);
+        const RowTask rows[2] = {decode_task64(queue[i]), decode_task64(i + 32 < nq ? queue[i + 32] : kEmptyKey)};
+        sweep_rows2(a, rows, changed, rows_done);
       }
       __syncwarp();
     }
@@ -1063,7 +1182,7 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_wa
   if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
 }
 
-#ifdef DBT_SWEEP_WARP
+#if defined(DBT_SWEEP_WARP)
 #define DBT_ISO_SWEEP sweep_warp_kernel
 #else
 #define DBT_ISO_SWEEP sweep_cull_kernel
@@ -1409,6 +1528,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.seeds = device_seeds(g->device, &rc);
   pa.bins = shadow_bins ? 0 : 1;
   pa.ray = g->d_ray;
+  pa.dirty = g->d_dirty;
+  pa.dby = g->dby;
+  pa.dbz = g->dbz;
+  if (g->d_dirty) g->dirty_reach = std::max(g->dirty_reach, b->R);
   if (rc) return rc;
   int tok;
   const unsigned prep_blocks = (unsigned)((n + kPrepThreads - 1) / kPrepThreads);
@@ -1644,9 +1767,17 @@ int stage_raw(dbt_grid* g, int64_t bytes) { return grow(&g->d_raw, &g->cap_raw_b
 // Synchronous entry points poll the completion event instead of sleeping in
 // cudaStreamSynchronize: the call is about to return anyway, and polling
 // answers within ~1 us of completion (a blocking wake-up can take ~10 us).
+// Completion of a synchronous call: poll the event (answers within ~1 us;
+// a blocking wake-up costs ~10 us, a quarter of a config-2 step) for up to
+// 1 ms, then poll every 50 us with the thread asleep in between, so long
+// batched calls do not keep a host core spinning. (A blocking-sync event
+// instead made every config-2 call ~14 us slower, even when polled.)
 cudaError_t wait_event(cudaEvent_t ev) {
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e;
   while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(1000))
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
   return e;
 }

@@ -102,6 +102,15 @@ def reduce_stats(stats: list, dist, group=None, device=None) -> list:
     return out
 
 
+def _replica_stream(st):
+    """Stream argument of the dbt_replica_* calls: NULL there means the
+    grid's own stream, so torch's legacy default stream (handle 0) is passed
+    as cudaStreamLegacy (0x1). Otherwise the pack/apply kernels would run on
+    the grid's non-blocking stream, unordered with the collectives torch
+    enqueues on the default stream."""
+    return ctypes.c_void_p(st.cuda_stream or 1)
+
+
 def _launch_device(grid: VoxelGrid, bank: KernelBank, points, dtype, counts, poses, prm, stream):
     """dbt_integrate_device on ``grid`` (asynchronous on ``stream``). A host
     mirror the caller may have written is uploaded first; afterwards it is
@@ -163,10 +172,11 @@ class ReplicatedGrid:
     """Data-parallel replicas: every rank holds the whole grid (device
     resident) and integrates its OWN scans — no collective per scan. ``merge``
     makes all replicas equal to the grid that every rank's scans produce
-    together (exact: see csrc/replica.cu), with three all-reduces over the
-    packed grid (MIN of the mask bit lengths, MIN of the signs, float16 SUM
-    of the hit deltas: 4 B per voxel). Until then each replica holds a valid partial
-    map; reads that need the global map merge first.
+    together (exact: see csrc/replica.cu): the ranks OR their dirty-brick
+    flags, and the 16^3 bricks within a kernel radius of any rank's returns
+    are reduced (MIN of the mask bit lengths and signs, float16 SUM of the
+    hit deltas: 4 B per voxel of those bricks only). Until then each replica
+    holds a valid partial map; reads that need the global map merge first.
 
     The scans between two merges must share (h_max, t_occ), as the hit-count
     combine depends on them."""
@@ -226,9 +236,10 @@ class ReplicatedGrid:
         _native.check(_native.lib().dbt_stats_read(self.local.handle, out, self._last_scans))
         return [FrameStats.from_native(out[i]) for i in range(self._last_scans)]
 
-    def _agreed_params(self, dev):
-        """(h_max, t_occ) every rank that integrated since the last merge used
-        (collective). Ranks without scans take them from the others, so all
+    def _agreed_params(self, dev, reach: int = 0):
+        """(h_max, t_occ) every rank that integrated since the last merge used,
+        and the largest kernel radius any rank integrated with (collective).
+        Ranks without scans take the parameters from the others, so all
         replicas fold the hit deltas identically; disagreement raises on
         every rank."""
         import torch
@@ -236,40 +247,84 @@ class ReplicatedGrid:
         have = self._params is not None
         h, t = self._params if have else (0, 0)
         v = torch.tensor([h if have else 1 << 20, t if have else 1 << 20, -h if have else 1 << 20,
-                          -t if have else 1 << 20], dtype=torch.int64, device=dev)
+                          -t if have else 1 << 20, -int(reach)], dtype=torch.int64, device=dev)
         self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN, group=self.group)
-        lo_h, lo_t, hi_h, hi_t = (int(x) for x in v.tolist())
+        lo_h, lo_t, hi_h, hi_t, nreach = (int(x) for x in v.tolist())
         if lo_h == 1 << 20:  # no rank integrated: no deltas to fold
-            return 255, 2
+            return 255, 2, -nreach
         if (lo_h, lo_t) != (-hi_h, -hi_t):
             raise ConfigurationError("replica scans between two merges must share h_max and t_occ across ranks")
-        return lo_h, lo_t
+        return lo_h, lo_t, -nreach
 
-    def merge(self, stream=None):
+    def merge(self, stream=None, sparse: bool = True):
         """All ranks: combine the replicas (collective). Returns when the
         merged records are enqueued on ``stream`` (current torch stream by
-        default)."""
+        default).
+
+        sparse (default): only the 16^3 bricks within a kernel radius of a
+        return some rank applied since the last merge travel — the ranks OR
+        their dirty-brick flags (1 B per brick), then reduce 4 B per voxel of
+        the selected bricks. sparse=False reduces the whole grid."""
+        import torch
+
+        dev = torch.device("cuda", self.local.device)
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        L = _native.lib()
+        self.local.push_host()
+        if not sparse:
+            self._merge_dense(dev, st)
+        else:
+            nb, reach = ctypes.c_int64(), ctypes.c_int32()
+            _native.check(L.dbt_replica_bricks(self.local.handle, ctypes.byref(nb), ctypes.byref(reach)))
+            flags = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+            _native.check(L.dbt_replica_dirty(self.local.handle, ctypes.c_void_p(flags.data_ptr()),
+                                              _replica_stream(st)))
+            with torch.cuda.stream(st):
+                self.dist.all_reduce(flags, op=self.dist.ReduceOp.MAX, group=self.group)
+            h_max, t_occ, reach_all = self._agreed_params(dev, reach.value)
+            n_sel = ctypes.c_int64()
+            _native.check(L.dbt_replica_select(self.local.handle, ctypes.c_void_p(flags.data_ptr()), int(reach_all),
+                                               ctypes.byref(n_sel), _replica_stream(st)))
+            cells = int(n_sel.value) * 4096
+            self.last_merge_voxels = cells
+            if cells:
+                ms = torch.empty(2 * cells, dtype=torch.uint8, device=dev)
+                dl = torch.empty(cells, dtype=torch.float16, device=dev)
+                _native.check(L.dbt_replica_pack_bricks(self.local.handle, ctypes.c_void_p(ms.data_ptr()),
+                                                        ctypes.c_void_p(dl.data_ptr()), _replica_stream(st)))
+                with torch.cuda.stream(st):
+                    self.dist.all_reduce(ms, op=self.dist.ReduceOp.MIN, group=self.group)
+                    self.dist.all_reduce(dl, op=self.dist.ReduceOp.SUM, group=self.group)
+                _native.check(L.dbt_replica_apply_bricks(self.local.handle, ctypes.c_void_p(ms.data_ptr()),
+                                                         ctypes.c_void_p(dl.data_ptr()), int(h_max), int(t_occ),
+                                                         _replica_stream(st)))
+                # the reduction buffers must outlive the enqueued apply
+                ms.record_stream(st)
+                dl.record_stream(st)
+            else:
+                _native.check(L.dbt_replica_apply_bricks(self.local.handle, None, None, int(h_max), int(t_occ),
+                                                         _replica_stream(st)))
+        self.local.pull_host()
+        self._params = None
+
+    def _merge_dense(self, dev, st):
         import torch
 
         n = self.dims[0] * self.dims[1] * self.dims[2]
-        dev = torch.device("cuda", self.local.device)
         if self._bufs is None:
             self._bufs = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
                           torch.empty(n, dtype=torch.float16, device=dev))
         mk, sg, dl = self._bufs
-        st = torch.cuda.current_stream(dev) if stream is None else stream
         L = _native.lib()
-        self.local.push_host()
         _native.check(L.dbt_replica_pack(self.local.handle, ctypes.c_void_p(mk.data_ptr()),
                                          ctypes.c_void_p(sg.data_ptr()), ctypes.c_void_p(dl.data_ptr()),
-                                         ctypes.c_void_p(st.cuda_stream)))
+                                         _replica_stream(st)))
         with torch.cuda.stream(st):
             self.dist.all_reduce(mk, op=self.dist.ReduceOp.MIN, group=self.group)
             self.dist.all_reduce(sg, op=self.dist.ReduceOp.MIN, group=self.group)
             self.dist.all_reduce(dl, op=self.dist.ReduceOp.SUM, group=self.group)
-        h_max, t_occ = self._agreed_params(dev)
+        h_max, t_occ, _ = self._agreed_params(dev)
+        self.last_merge_voxels = n
         _native.check(L.dbt_replica_apply(self.local.handle, ctypes.c_void_p(mk.data_ptr()),
                                           ctypes.c_void_p(sg.data_ptr()), ctypes.c_void_p(dl.data_ptr()),
-                                          int(h_max), int(t_occ), ctypes.c_void_p(st.cuda_stream)))
-        self.local.pull_host()
-        self._params = None
+                                          int(h_max), int(t_occ), _replica_stream(st)))

@@ -809,7 +809,50 @@ class TestReplicaMerge:
             g.synchronize()
         torch.cuda.synchronize()
 
-    def run(self, c, n_rep, intervals=1):
+    @staticmethod
+    def merge_apply_sparse(grids, params):
+        """The sparse protocol (dbt_replica_dirty/select/pack_bricks/
+        apply_bricks) with torch reductions standing in for NCCL."""
+        import ctypes
+
+        import torch
+
+        L = _native.lib()
+        nb, reach = ctypes.c_int64(), ctypes.c_int32()
+        flags, reaches = [], []
+        for g in grids:
+            _native.check(L.dbt_replica_bricks(g.handle, ctypes.byref(nb), ctypes.byref(reach)))
+            f = torch.empty(int(nb.value), dtype=torch.uint8, device="cuda")
+            _native.check(L.dbt_replica_dirty(g.handle, ctypes.c_void_p(f.data_ptr()), None))
+            g.synchronize()
+            flags.append(f)
+            reaches.append(reach.value)
+        fl = torch.stack(flags).amax(0).contiguous()
+        torch.cuda.synchronize()
+        packs, nsel = [], []
+        for g in grids:
+            n = ctypes.c_int64()
+            _native.check(L.dbt_replica_select(g.handle, ctypes.c_void_p(fl.data_ptr()), max(reaches),
+                                               ctypes.byref(n), None))
+            nsel.append(n.value)
+            ms = torch.empty(2 * 4096 * n.value, dtype=torch.uint8, device="cuda")
+            dl = torch.empty(4096 * n.value, dtype=torch.float16, device="cuda")
+            _native.check(L.dbt_replica_pack_bricks(g.handle, ctypes.c_void_p(ms.data_ptr()),
+                                                    ctypes.c_void_p(dl.data_ptr()), None))
+            g.synchronize()
+            packs.append((ms, dl))
+        assert len(set(nsel)) == 1
+        ms = torch.stack([p[0] for p in packs]).amin(0).contiguous()
+        dl = torch.stack([p[1] for p in packs]).sum(0).contiguous()
+        torch.cuda.synchronize()
+        for g in grids:
+            _native.check(L.dbt_replica_apply_bricks(g.handle, ctypes.c_void_p(ms.data_ptr()),
+                                                     ctypes.c_void_p(dl.data_ptr()), params.h_max, params.t_occ, None))
+            g.synchronize()
+        torch.cuda.synchronize()
+        return nsel[0]
+
+    def run(self, c, n_rep, intervals=1, sparse=False):
         bank = build_kernel_bank(**c.bank)
         grids = []
         for _ in range(n_rep):
@@ -825,7 +868,10 @@ class TestReplicaMerge:
         for chunk in chunks:
             for j, k in enumerate(chunk):
                 integrate_frame(grids[j % n_rep], bank, frames[k], params)
-            self.apply(grids, self.merge(grids), params)
+            if sparse:
+                self.merge_apply_sparse(grids, params)
+            else:
+                self.apply(grids, self.merge(grids), params)
         return grids
 
     @pytest.mark.parametrize("name,n_rep,intervals", [
@@ -840,6 +886,32 @@ class TestReplicaMerge:
             assert cases.sha(m) == ref["mask"], "mask differs from the reference"
             assert cases.sha(s) == ref["sign"], "sign differs from the reference"
             assert cases.sha(h) == ref["hits"], "hits differ from the reference"
+
+    @pytest.mark.parametrize("name,n_rep,intervals", [
+        ("cfg2_scans0-2", 2, 1), ("cfg2_scans0-2", 3, 2), ("yaw_frames_f32", 3, 2),
+        ("nonfresh_hemisphere_h7_t3", 2, 1), ("nonfresh_cone_h200_t2", 3, 1), ("nonfresh_hemisphere_h255_t1", 2, 2),
+        ("arbitrary_state", 2, 1), ("edge_returns", 2, 1)])
+    def test_sparse_merge_matches_reference(self, name, n_rep, intervals, golden):
+        c = next(c for c in SMALL + CONFIG if c.name == name)
+        ref = golden["cases"][name]
+        for g in self.run(c, n_rep, intervals, sparse=True):
+            m, s, h = g.download_range(0, c.dims[0])
+            assert cases.sha(m) == ref["mask"], "mask differs from the reference"
+            assert cases.sha(s) == ref["sign"], "sign differs from the reference"
+            assert cases.sha(h) == ref["hits"], "hits differ from the reference"
+
+    def test_sparse_merge_moves_only_touched_bricks(self):
+        """One return in a corner of a 256^3 grid: the merge selects the
+        3^3 bricks around its brick (R = 10 -> one brick of dilation), not
+        the 4096 bricks of the grid; a merge with no work selects none."""
+        bank = build_kernel_bank()
+        g = new_grid((256, 256, 256), 0.1)
+        _native.check(_native.lib().dbt_replica_mark(g.handle))
+        assert self.merge_apply_sparse([g], IntegrationParams()) == 0
+        pts = np.array([[2.45, 2.45, 2.45]])  # voxel (24, 24, 24): brick (1, 1, 1)
+        integrate_frame(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+        assert self.merge_apply_sparse([g], IntegrationParams()) == 27
+        assert self.merge_apply_sparse([g], IntegrationParams()) == 0
 
     def test_merge_without_work_is_identity(self, golden):
         c = next(c for c in SMALL if c.name == "arbitrary_state")

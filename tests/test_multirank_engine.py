@@ -83,7 +83,7 @@ def _sharded_worker(rank, world, port, case_name, interleave, out_path):
     dist.destroy_process_group()
 
 
-def _replica_worker(rank, world, port, case_name, out_path):
+def _replica_worker(rank, world, port, case_name, out_path, sparse=True):
     torch, dist = _init(rank, world, port)
     import cases as C
     from paper_2509_20081_b200 import IntegrationParams, ScanFrame, build_kernel_bank
@@ -101,7 +101,7 @@ def _replica_worker(rank, world, port, case_name, out_path):
     for k, (pts, pose) in enumerate(c.frames):
         if k % world == rank:
             rg.integrate_frame(bank, ScanFrame(points=pts, pose=pose), params)
-    rg.merge()
+    rg.merge(sparse=sparse)
     torch.cuda.synchronize()
     m, s, h = rg.local.mask, rg.local.sign, rg.local.hits
     shas = [None] * world
@@ -128,11 +128,13 @@ def test_sharded_engine_ranks_match_reference(case_name, interleave, world, gold
         assert got[:2] == want[:2]
 
 
-@pytest.mark.parametrize("case_name,world", [("cfg2_scans0-2", 2), ("nonfresh_hemisphere_h7_t3", 2),
-                                             ("yaw_frames_f32", 3), ("nonfresh_cone_h200_t2", 4)])
-def test_replicated_engine_merge_matches_reference(case_name, world, golden, tmp_path):
+@pytest.mark.parametrize("case_name,world,sparse", [("cfg2_scans0-2", 2, True), ("nonfresh_hemisphere_h7_t3", 2, True),
+                                                    ("yaw_frames_f32", 3, True), ("nonfresh_cone_h200_t2", 4, True),
+                                                    ("arbitrary_state", 2, True), ("cfg2_scans0-2", 2, False),
+                                                    ("nonfresh_cone_h200_t2", 3, False)])
+def test_replicated_engine_merge_matches_reference(case_name, world, sparse, golden, tmp_path):
     out = tmp_path / "r.npz"
-    _spawn(_replica_worker, world, case_name, str(out))
+    _spawn(_replica_worker, world, case_name, str(out), sparse)
     r = np.load(out)
     ref = golden["cases"][case_name]
     assert (str(r["mask"]), str(r["sign"]), str(r["hits"])) == (ref["mask"], ref["sign"], ref["hits"])
