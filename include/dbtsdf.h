@@ -180,6 +180,36 @@ DBT_API int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* poin
 DBT_API int dbt_integrate_scans(dbt_grid* g, const dbt_bank* b, const void* const* points, int dtype,
                         const int64_t* counts, int32_t n_scans, const double* poses,
                         const dbt_params* p, dbt_stats* out);
+/* Motion-compensated scan (compensation "yaw" / "se3", integrator.py:91-123,
+ * 223-230), deskewed on the device: per point the pose at its time is
+ * interpolated and the point moved to the end-of-sweep sensor frame exactly
+ * as the reference's scipy/numpy code does (bit for bit, including the C
+ * library's sin/cos: csrc/libm_emu.cuh), then integrated like
+ * dbt_integrate_frame with `pose` = the scan's (end) pose. `d` holds the
+ * point-independent quantities, computed by the caller with scipy as the
+ * reference does (paper_2509_20081_b200/integrator.py deskew_params).
+ * timestamps: host float64, one per raw point (downsampled with the points),
+ * or NULL for linspace(0, 1) over the downsampled scan. Fails with
+ * DBT_ERR_CONFIG when the restatement cannot be matched to this process's C
+ * library (dbt_deskew_available). */
+typedef struct dbt_deskew {
+  int32_t mode;           /* DBT_DESKEW_YAW or DBT_DESKEW_SE3 */
+  int32_t reserved;
+  double q[4];            /* yaw: tilt quaternion _rot_z(-y1) * R1; se3: start rotation (x, y, z, w) */
+  double rv[3];           /* se3: the Slerp interval's rotation vector */
+  double y0, dy;          /* yaw: start heading and wrapped heading change */
+  double t0[3], t1[3];    /* prev_pose / pose translations */
+  double r1[9];           /* pose rotation, row-major */
+} dbt_deskew;
+#define DBT_DESKEW_YAW 1
+#define DBT_DESKEW_SE3 2
+DBT_API int dbt_deskew_available(int32_t* ok);
+DBT_API int dbt_integrate_frame_deskew(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
+                               const double* timestamps, const double pose[16], const dbt_deskew* d,
+                               const dbt_params* p, dbt_stats* out);
+/* the deskewed float64 points alone (host in, host out; parity tests) */
+DBT_API int dbt_deskew_points(int device, const void* points, int dtype, int64_t n, const double* timestamps,
+                      int32_t downsample, const dbt_deskew* d, double* out);
 /* Map-frame points with per-point sensor positions (integrate_point,
  * integrator.py:163-189); outcome[i] = 1 applied, 0 discarded (nullable). */
 DBT_API int dbt_integrate_points_map(dbt_grid* g, const dbt_bank* b, const double* p_map,

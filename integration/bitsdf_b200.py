@@ -77,6 +77,10 @@ def lib(path: str | None = None):
                                                    ctypes.POINTER(Params), ctypes.POINTER(Stats)]),
             "dbt_integrate_points_map": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.POINTER(Params),
                                                         ctypes.POINTER(Stats), vp]),
+            "dbt_deskew_available": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
+            "dbt_integrate_frame_deskew": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.c_int64, vp, dp,
+                                                          ctypes.POINTER(Deskew), ctypes.POINTER(Params),
+                                                          ctypes.POINTER(Stats)]),
             "dbt_mesh_extract": (ctypes.c_int, [vp, ctypes.c_double, ctypes.POINTER(McTables), ctypes.POINTER(vp),
                                                 i64p, i64p]),
             "dbt_mesh_download": (ctypes.c_int, [vp, vp, vp]),
@@ -98,6 +102,12 @@ class Stats(ctypes.Structure):  # dbt_stats, 80 bytes
     _fields_ = [(n, ctypes.c_int64) for n in ("points_in", "points_discarded", "voxels_written", "points_applied",
                                               "unique_centers", "centers_skipped", "bin_fallbacks")] + \
                [("elapsed_ms", ctypes.c_double), ("device_ms", ctypes.c_double), ("rows_swept", ctypes.c_int64)]
+
+
+class Deskew(ctypes.Structure):  # dbt_deskew, 240 bytes
+    _fields_ = [("mode", ctypes.c_int32), ("reserved", ctypes.c_int32), ("q", ctypes.c_double * 4),
+                ("rv", ctypes.c_double * 3), ("y0", ctypes.c_double), ("dy", ctypes.c_double),
+                ("t0", ctypes.c_double * 3), ("t1", ctypes.c_double * 3), ("r1", ctypes.c_double * 9)]
 
 
 class McTables(ctypes.Structure):  # dbt_mc_tables
@@ -216,6 +226,43 @@ def _params(params, flags=0, downsample=None):
                   int(bool(params.first_return_per_voxel)), flags, 0)
 
 
+_DESKEW_OK = None
+
+
+def _deskew(scan, mode):
+    """The point-independent part of motion_compensate (integrator.py:
+    91-123), computed with scipy as the reference does; the per-point part
+    (pose at each point's time, the move to the end-of-sweep frame, the C
+    library's sin/cos restated) runs in the engine's preprocessing."""
+    from scipy.spatial.transform import Rotation, Slerp
+
+    global _DESKEW_OK
+    if _DESKEW_OK is None:
+        ok = ctypes.c_int32()
+        _check(lib().dbt_deskew_available(ctypes.byref(ok)))
+        _DESKEW_OK = bool(ok.value)
+    if not _DESKEW_OK or scan.prev_pose is None:
+        return None
+    T0, T1 = np.asarray(scan.prev_pose, np.float64), np.asarray(scan.pose, np.float64)
+    d = Deskew()
+    if mode == "se3":
+        s = Slerp([0.0, 1.0], Rotation.from_matrix(np.stack([T0[:3, :3], T1[:3, :3]])))
+        d.mode = 2
+        d.q[:] = [float(v) for v in s.rotations[0].as_quat(canonical=False)]
+        d.rv[:] = [float(v) for v in s.rotvecs[0]]
+    else:
+        y0 = Rotation.from_matrix(T0[:3, :3]).as_euler("zyx")[0]
+        y1 = Rotation.from_matrix(T1[:3, :3]).as_euler("zyx")[0]
+        tilt = Rotation.from_euler("z", -y1) * Rotation.from_matrix(T1[:3, :3])
+        d.mode = 1
+        d.q[:] = [float(v) for v in np.asarray(tilt.as_quat(canonical=False)).reshape(4)]
+        d.y0, d.dy = float(y0), float((y1 - y0 + np.pi) % (2 * np.pi) - np.pi)
+    d.t0[:] = [float(v) for v in T0[:3, 3]]
+    d.t1[:] = [float(v) for v in T1[:3, 3]]
+    d.r1[:] = [float(v) for v in T1[:3, :3].reshape(9)]
+    return d
+
+
 # ----------------------------------------------------------- entry points
 def integrate_frame(grid, bank, scan, params, threads: int = 1):
     """integrator.integrate_frame on the GPU: same FrameStats fields
@@ -225,6 +272,23 @@ def integrate_frame(grid, bank, scan, params, threads: int = 1):
     if scan.points.shape[0] == 0:
         return FrameStats()
     downsample = params.downsample
+    dk = _deskew(scan, params.compensation) if params.compensation != "none" else None
+    if dk is not None:
+        # deskewed on the device (bit-identical to motion_compensate)
+        pts = np.ascontiguousarray(scan.points, np.float64)
+        ts = None if scan.timestamps is None else np.ascontiguousarray(scan.timestamps, np.float64)
+        pose = np.ascontiguousarray(scan.pose, np.float64)
+        g = _upload(grid)
+        prm = _params(params)
+        st = Stats()
+        _check(lib().dbt_integrate_frame_deskew(
+            g, device_bank(bank), _ptr(pts), DBT_F64, pts.shape[0], None if ts is None else _ptr(ts),
+            pose.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(dk), ctypes.byref(prm),
+            ctypes.byref(st)))
+        _download(grid)
+        grid.h_max, grid.t_occ = params.h_max, params.t_occ
+        return FrameStats(int(st.points_in), int(st.points_discarded), int(st.voxels_written),
+                          (time.perf_counter() - t0) * 1e3)
     if params.compensation != "none":
         if motion_compensate is None:
             raise RuntimeError("compensation needs the reference's motion_compensate")

@@ -59,6 +59,23 @@ class Stats(ctypes.Structure):
     ]
 
 
+class Deskew(ctypes.Structure):
+    """dbt_deskew: per-scan constants of the device motion compensation."""
+    _fields_ = [
+        ("mode", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("q", ctypes.c_double * 4),
+        ("rv", ctypes.c_double * 3),
+        ("y0", ctypes.c_double),
+        ("dy", ctypes.c_double),
+        ("t0", ctypes.c_double * 3),
+        ("t1", ctypes.c_double * 3),
+        ("r1", ctypes.c_double * 9),
+    ]
+
+
+DESKEW_YAW, DESKEW_SE3 = 1, 2
+
 # name -> (restype, argtypes); mirrors include/dbtsdf.h one to one
 SIGNATURES = {
     "dbt_last_error": (ctypes.c_char_p, []),
@@ -119,6 +136,11 @@ SIGNATURES = {
     "dbt_replica_mark": (ctypes.c_int, [_vp]),
     "dbt_replica_pack": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "dbt_replica_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
+    "dbt_deskew_available": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
+    "dbt_integrate_frame_deskew": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, _vp,
+                                                  _vp]),
+    "dbt_deskew_points": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int64, _vp, ctypes.c_int32, _vp,
+                                         _vp]),
     "dbt_replica_bricks": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]),
     "dbt_replica_dirty": (ctypes.c_int, [_vp, _vp, _vp]),
     "dbt_replica_select": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _vp]),

@@ -240,6 +240,8 @@ struct dbt_grid {
   int64_t cap_sensor = 0;
   int8_t* d_outcome = nullptr;
   int64_t cap_outcome = 0;
+  double* d_ts = nullptr;       // device deskew: per-point times
+  int64_t cap_ts = 0;
   // per-scan metadata
   int64_t* d_scan_off = nullptr;    // kMaxScansPerLaunch + 1 (downsampled)
   dbt::ScanCounters* d_scnt = nullptr;

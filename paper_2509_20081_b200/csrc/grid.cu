@@ -371,7 +371,7 @@ int dbt_grid_destroy(dbt_grid* g) {
   void* dev[] = {g->cells.m, g->dist,  g->stamped, g->d_raw,  g->d_center, g->d_bin,     g->d_slot,    g->d_uniq,
                  g->d_hkey, g->d_hmin, g->d_sensor, g->d_outcome, g->d_scan_off,
                  g->d_lcnt, g->d_stage, g->d_rowoff, g->d_exact_bits, g->d_exact_m0, g->d_base_hits, g->d_base_mask,
-                 g->d_ray, g->d_dirty, g->d_sel};
+                 g->d_ray, g->d_dirty, g->d_sel, g->d_ts};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {g->h_lcnt, g->h_meta};

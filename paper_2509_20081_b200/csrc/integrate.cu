@@ -33,7 +33,11 @@
 #include <thread>
 
 #include "engine.cuh"
+#include <math_constants.h>
+
 #include "svml_emu.cuh"
+#include "deskew.cuh"
+#include "libm_table.h"
 
 using namespace dbt;
 
@@ -95,6 +99,13 @@ struct PrepArgs {
   // replica mode: dirty flag of the 16^3 brick holding each applied centre
   uint8_t* dirty;
   int64_t dby, dbz;
+  // device deskew (compensation yaw/se3, single-scan launches): the point is
+  // moved to the end-of-sweep frame first (deskew.cuh); dk_ts = per-point
+  // times by raw index, or null for linspace over the n downsampled points
+  int deskew;
+  dbt_deskew dk;
+  const double* dk_ts;
+  const double* sincos;  // the C library's sin/cos table (libm_emu.cuh)
 };
 
 constexpr uint64_t kKeyMask = (1ull << 52) - 1;  // cflat (< 2^40) | scan << 40
@@ -182,6 +193,7 @@ constexpr int kPrepThreads = 256;
 // (downsampled index, per-scan offsets), and m = p @ R.T + t with the sensor
 // position t (map mode: given per point). Shared by prep and the shadow
 // kernel's bin phase, so both see the same doubles.
+template <bool DESKEW>
 __device__ __forceinline__ void map_point(const PrepArgs& a, int64_t i, int& s, double& m0, double& m1, double& m2,
                                           double& t0, double& t1, double& t2) {
   int64_t src;
@@ -204,6 +216,16 @@ __device__ __forceinline__ void map_point(const PrepArgs& a, int64_t i, int& s, 
     p0 = q[0];
     p1 = q[1];
     p2 = q[2];
+  }
+  if (DESKEW) {
+    // integrator.py:223-230: motion_compensate, then pts @ R.T + t below
+    const double t = deskew::clip01(a.dk_ts ? a.dk_ts[src] : deskew::linspace01(i, a.n));
+    double o[3];
+    int rare = 0;
+    deskew::apply(a.dk, t, p0, p1, p2, o, a.sincos, &rare);
+    p0 = rare ? CUDART_NAN : o[0];  // (never for finite poses) discarded like a NaN return
+    p1 = o[1];
+    p2 = o[2];
   }
   if (a.map_mode) {
     m0 = p0;
@@ -230,6 +252,9 @@ __device__ __forceinline__ double ray_norm(double rx, double ry, double rz) {
   return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
 }
 
+// DESKEW: the motion-compensated variant (a separate instantiation keeps the
+// default path's register budget)
+template <bool DESKEW>
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   // the sweep (programmatic dependent launch) may be scheduled once every
   // prep block has started; it waits for this grid's completion before
@@ -247,7 +272,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
   uint64_t packed = kEmptyKey;
   if (live) {
     double m0, m1, m2, t0, t1, t2;
-    map_point(a, i, s, m0, m1, m2, t0, t1, t2);
+    map_point<DESKEW>(a, i, s, m0, m1, m2, t0, t1, t2);
     double rx = __dsub_rn(m0, t0), ry = __dsub_rn(m1, t1), rz = __dsub_rn(m2, t2);
     double nrm = ray_norm(rx, ry, rz);
     ok = a.skip_norm ? 1 : (nrm >= a.vs);
@@ -1245,6 +1270,74 @@ const uint16_t* device_seeds(int device, int* rc) {
   return tabs[device];
 }
 
+// The C library's sin/cos table for the deskew restatement (libm_emu.cuh):
+// located in this process's libm, checked against its sin/cos on 200 000
+// arguments, uploaded once per device. nullptr (and *rc) when the library
+// cannot be matched (another libm build or dispatch variant).
+const double* device_sincostab(int device, int* rc) {
+  static std::mutex mu;
+  static double* tabs[64] = {nullptr};
+  static int host_state = 0;  // 0 unknown, 1 matched, -1 not matched
+  static const double* host_tab = nullptr;
+  *rc = DBT_OK;
+  if (device < 0 || device >= 64) {
+    *rc = set_error(DBT_ERR_CONFIG, "device ordinal out of range");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (host_state == 0) {
+    host_tab = libm_emu::find_sincostab();
+    host_state = (host_tab && libm_emu::check_sincostab(host_tab) == 0) ? 1 : -1;
+  }
+  if (host_state < 0) {
+    *rc = set_error(DBT_ERR_CONFIG, "device deskew unavailable: the C library's sin/cos do not match the restatement");
+    return nullptr;
+  }
+  if (!tabs[device]) {
+    double* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, libm_emu::kTabEntries * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p, host_tab, libm_emu::kTabEntries * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      *rc = cuda_error(e, "sin/cos table");
+      return nullptr;
+    }
+    tabs[device] = p;
+  }
+  return tabs[device];
+}
+
+// deskewed float64 points of a (downsampled) scan (dbt_deskew_points)
+__global__ void deskew_points_kernel(const void* pts, int dtype, int64_t n, int ds, const double* ts, dbt_deskew dk,
+                                     const double* tab, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = i * ds;
+    double p0, p1, p2;
+    if (dtype == DBT_F32) {
+      const float* q = (const float*)pts + 3 * src;
+      p0 = q[0];
+      p1 = q[1];
+      p2 = q[2];
+    } else {
+      const double* q = (const double*)pts + 3 * src;
+      p0 = q[0];
+      p1 = q[1];
+      p2 = q[2];
+    }
+    const double t = deskew::clip01(ts ? ts[src] : deskew::linspace01(i, n));
+    int rare = 0;
+    deskew::apply(dk, t, p0, p1, p2, out + 3 * i, tab, &rare);
+    if (rare) out[3 * i] = CUDART_NAN;
+  }
+}
+
+int check_deskew(const dbt_deskew* d) {
+  if (!d) return set_error(DBT_ERR_CONFIG, "null deskew parameters");
+  if (d->mode != DBT_DESKEW_YAW && d->mode != DBT_DESKEW_SE3)
+    return set_error(DBT_ERR_CONFIG, "deskew mode must be DBT_DESKEW_YAW or DBT_DESKEW_SE3");
+  return DBT_OK;
+}
+
 int grow(void** p, int64_t* cap, int64_t need, size_t elem) {
   if (need <= *cap) return DBT_OK;
   int64_t c = std::max<int64_t>(need, *cap + *cap / 2);
@@ -1341,10 +1434,17 @@ struct GraphCtl {
   bool has_shadow = false;
 };
 
+struct DeskewArgs {
+  dbt_deskew dk;
+  const double* d_ts;    // device times by raw index, or null (linspace)
+  const double* sincos;  // device copy of the C library's sin/cos table
+};
+
 int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtype,
                      const int64_t* counts, int S, const double* poses, const dbt_params* p,
                      const double* d_map_sensor, int8_t* d_outcome, cudaStream_t st,
-                     const void* const* scan_ptrs, GraphCtl* gc = nullptr) {
+                     const void* const* scan_ptrs, GraphCtl* gc = nullptr, const DeskewArgs* dka = nullptr) {
+  if (dka && (S != 1 || d_map_sensor)) return set_error(DBT_ERR_CONFIG, "device deskew needs one scan per launch");
   if (S < 1 || S > kMaxScansPerLaunch) return set_error(DBT_ERR_CONFIG, "scan count per launch out of range");
   if (b->device != g->device) return set_error(DBT_ERR_CONFIG, "bank and grid live on different devices");
   if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
@@ -1531,6 +1631,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   pa.dirty = g->d_dirty;
   pa.dby = g->dby;
   pa.dbz = g->dbz;
+  pa.deskew = dka ? 1 : 0;
+  if (dka) pa.dk = dka->dk;
+  pa.dk_ts = dka ? dka->d_ts : nullptr;
+  pa.sincos = dka ? dka->sincos : nullptr;
   if (g->d_dirty) g->dirty_reach = std::max(g->dirty_reach, b->R);
   if (rc) return rc;
   int tok;
@@ -1542,7 +1646,10 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
   if (issue) {
     prof_begin(g, "prep_kernel", st, &tok);
-    prep_kernel<<<prep_blocks, kPrepThreads, 0, st>>>(pa);
+    if (pa.deskew)
+      prep_kernel<true><<<prep_blocks, kPrepThreads, 0, st>>>(pa);
+    else
+      prep_kernel<false><<<prep_blocks, kPrepThreads, 0, st>>>(pa);
     prof_end(g, st, tok);
     DBT_CHECK_LAUNCH("prep_kernel");
   }
@@ -1878,7 +1985,7 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
       ++g->gkernels;
       cudaKernelNodeParams kp;
       DBT_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == (void*)prep_kernel) g->gprep = nd;
+      if (kp.func == (void*)prep_kernel<false>) g->gprep = nd;
       if (kp.func == (void*)shadow_kernel || kp.func == (void*)shadow_bin_kernel) g->gshadow = nd;
     }
     g->ggraph = graph;
@@ -1891,7 +1998,7 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
     if (rc) return rc;
     cudaKernelNodeParams kp = {};
     void* pargs[] = {&gc.pa};
-    kp.func = (void*)prep_kernel;
+    kp.func = (void*)prep_kernel<false>;
     kp.gridDim = dim3(gc.prep_blocks);
     kp.blockDim = dim3(kPrepThreads);
     kp.kernelParams = pargs;
@@ -1912,10 +2019,12 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
 }
 
 int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, const int64_t* counts,
-                   int S, const double* poses, const dbt_params* p, dbt_stats* out) {
+                   int S, const double* poses, const dbt_params* p, dbt_stats* out, const dbt_deskew* dk = nullptr,
+                   const double* timestamps = nullptr) {
   double t0 = now_ms();
   int rc = check(g, b);
   if (!rc) rc = validate_params(p);
+  if (!rc && dk) rc = check_deskew(dk);
   if (rc) return rc;
   int64_t total = 0;
   for (int s = 0; s < S; ++s) total += counts[s];
@@ -1955,7 +2064,22 @@ int integrate_host(dbt_grid* g, const dbt_bank* b, const void* points, int dtype
     DBT_CUDA(cudaMemcpyAsync(g->d_raw, points, total * esz, cudaMemcpyHostToDevice, st));
     d_src = g->d_raw;
   }
-  if (S == 1 && graph_eligible(g, b, p)) {
+  if (dk) {
+    // device deskew: the C library's sin/cos table, the per-point times
+    DeskewArgs dka;
+    dka.dk = *dk;
+    dka.d_ts = nullptr;
+    dka.sincos = device_sincostab(g->device, &rc);
+    if (rc) return rc;
+    if (timestamps) {
+      rc = grow((void**)&g->d_ts, &g->cap_ts, counts[0], sizeof(double));
+      if (rc) return rc;
+      DBT_CUDA(cudaMemcpyAsync(g->d_ts, timestamps, counts[0] * sizeof(double), cudaMemcpyHostToDevice, st));
+      dka.d_ts = g->d_ts;
+    }
+    rc = launch_integrate(g, b, d_src, dtype, counts, 1, poses, p, nullptr, nullptr, st, nullptr, nullptr, &dka);
+    if (!rc) rc = fetch_counters(g, st);
+  } else if (S == 1 && graph_eligible(g, b, p)) {
     rc = integrate_graph(g, b, d_src, dtype, counts[0], poses, p, st);
   } else {
     rc = launch_integrate(g, b, d_src, dtype, counts, S, poses, p, nullptr, nullptr, st, nullptr);
@@ -2064,6 +2188,60 @@ int dbt_integrate_scans(dbt_grid* g, const dbt_bank* b, const void* const* point
 int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
                         const double pose[16], const dbt_params* p, dbt_stats* out) {
   return integrate_host(g, b, points, dtype, &n, 1, pose, p, out);
+}
+
+int dbt_deskew_available(int32_t* ok) {
+  if (!ok) return set_error(DBT_ERR_CONFIG, "null output");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    *ok = 0;
+    return DBT_OK;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  int rc = DBT_OK;
+  *ok = device_sincostab(cur, &rc) != nullptr ? 1 : 0;
+  return DBT_OK;
+}
+
+int dbt_integrate_frame_deskew(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
+                               const double* timestamps, const double pose[16], const dbt_deskew* d,
+                               const dbt_params* p, dbt_stats* out) {
+  return integrate_host(g, b, points, dtype, &n, 1, pose, p, out, d, timestamps);
+}
+
+int dbt_deskew_points(int device, const void* points, int dtype, int64_t n, const double* timestamps,
+                      int32_t downsample, const dbt_deskew* d, double* out) {
+  int rc = check_deskew(d);
+  if (rc) return rc;
+  if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
+  if (downsample < 1 || n < 0) return set_error(DBT_ERR_CONFIG, "bad point count or downsample factor");
+  if (n == 0) return DBT_OK;
+  DBT_CUDA(cudaSetDevice(device));
+  const double* tab = device_sincostab(device, &rc);
+  if (rc) return rc;
+  const int64_t m = (n + downsample - 1) / downsample;
+  const size_t esz = dtype == DBT_F32 ? 12 : 24;
+  void* dp = nullptr;
+  double *dts = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMalloc(&dp, n * esz);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&dout, m * 24);
+  if (e == cudaSuccess && timestamps) e = cudaMalloc((void**)&dts, n * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(dp, points, n * esz, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && timestamps) e = cudaMemcpy(dts, timestamps, n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    deskew_points_kernel<<<(unsigned)std::min<int64_t>((m + 255) / 256, 148 * 8), 256>>>(dp, dtype, m, downsample,
+                                                                                       dts, *d, tab, dout);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) count_launch();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, m * 24, cudaMemcpyDeviceToHost);
+  cudaFree(dp);
+  cudaFree(dout);
+  if (dts) cudaFree(dts);
+  if (e != cudaSuccess) return cuda_error(e, "dbt_deskew_points");
+  return DBT_OK;
 }
 
 int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,

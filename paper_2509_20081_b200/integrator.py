@@ -147,6 +147,39 @@ def _scan_times(scan: ScanFrame) -> np.ndarray:
     return np.linspace(0.0, 1.0, n) if n > 1 else np.zeros(n)
 
 
+def deskew_params(scan: ScanFrame, mode: str) -> "_native.Deskew":
+    """The point-independent part of motion_compensate (integrator.py:91-123)
+    for the device deskew (dbt_integrate_frame_deskew): computed here with
+    scipy exactly as the reference computes it; the per-point part (pose at
+    the point's time, the move to the end-of-sweep frame) runs on the device
+    (csrc/deskew.cuh)."""
+    if mode not in ("yaw", "se3"):
+        raise ConfigurationError(f"no device deskew for compensation {mode!r}")
+    if scan.prev_pose is None:
+        raise ConfigurationError("motion compensation requires prev_pose")
+    T0, T1 = scan.prev_pose, scan.pose
+    d = _native.Deskew()
+    if mode == "se3":
+        rots = Rotation.from_matrix(np.stack([T0[:3, :3], T1[:3, :3]]))
+        s = Slerp([0.0, 1.0], rots)
+        rv = s.rotvecs[0] if hasattr(s, "rotvecs") else (rots[:-1].inv() * rots[1:]).as_rotvec()[0]
+        d.mode = _native.DESKEW_SE3
+        d.q[:] = [float(v) for v in s.rotations[0].as_quat(canonical=False)]
+        d.rv[:] = [float(v) for v in rv]
+    else:
+        y0 = Rotation.from_matrix(T0[:3, :3]).as_euler("zyx")[0]
+        y1 = Rotation.from_matrix(T1[:3, :3]).as_euler("zyx")[0]
+        dy = (y1 - y0 + np.pi) % (2 * np.pi) - np.pi
+        tilt = _rot_z(-y1) * Rotation.from_matrix(T1[:3, :3])
+        d.mode = _native.DESKEW_YAW
+        d.q[:] = [float(v) for v in np.asarray(tilt.as_quat(canonical=False)).reshape(4)]
+        d.y0, d.dy = float(y0), float(dy)
+    d.t0[:] = [float(v) for v in T0[:3, 3]]
+    d.t1[:] = [float(v) for v in T1[:3, 3]]
+    d.r1[:] = [float(v) for v in np.asarray(T1[:3, :3], np.float64).reshape(9)]
+    return d
+
+
 def motion_compensate(scan: ScanFrame, mode: str) -> ScanFrame:
     """Deskew to the end-of-sweep sensor frame (integrator.py:91-123). Host
     side (scipy Slerp/Rotation, as the reference); "none" is the identity."""
@@ -226,8 +259,26 @@ def integrate_frame(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: 
     if scan.n_points == 0:
         return FrameStats()
     downsample = params.downsample
+    if params.compensation != "none" and device_deskew_available():
+        # deskew on the device (csrc/deskew.cuh): the point-independent part
+        # here with scipy, the per-point part in the preprocessing kernel
+        dk = deskew_params(scan, params.compensation)
+        grid.h_max = params.h_max
+        grid.t_occ = params.t_occ
+        pts, dtype = scan.device_payload()
+        pose, pose_p = _pose_arg(scan.pose)
+        ts = scan.timestamps
+        prm = params.native(downsample=downsample)
+        st = _native.Stats()
+        grid.push_host()
+        _native.check(_native.lib().dbt_integrate_frame_deskew(
+            grid.handle, bank.device_handle(grid.device), _native.ptr(pts), dtype, pts.shape[0],
+            None if ts is None else _native.ptr(ts), pose_p, ctypes.byref(dk), ctypes.byref(prm), ctypes.byref(st)))
+        grid.pull_host()
+        return FrameStats.from_native(st, (time.perf_counter() - t0) * 1e3)
     if params.compensation != "none":
-        # deskew on the host exactly as the reference, then ship float64
+        # the C library could not be matched (device_deskew_available): deskew
+        # on the host exactly as the reference, then ship float64
         if downsample > 1:
             keep = slice(None, None, downsample)
             scan = ScanFrame(points=scan.points[keep], pose=scan.pose,
@@ -248,6 +299,24 @@ def integrate_frame(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: 
     return FrameStats.from_native(st, (time.perf_counter() - t0) * 1e3)
 
 
+_DESKEW_OK = None
+
+
+def device_deskew_available() -> bool:
+    """The device deskew reproduces the C library's sin/cos bit for bit
+    (csrc/libm_emu.cuh); the engine checks that against this process's libm
+    once. False (host deskew through scipy) on another libm build."""
+    global _DESKEW_OK
+    if _DESKEW_OK is None:
+        if os.environ.get("DBT_HOST_DESKEW") == "1":
+            _DESKEW_OK = False
+        else:
+            ok = ctypes.c_int32()
+            _native.check(_native.lib().dbt_deskew_available(ctypes.byref(ok)))
+            _DESKEW_OK = bool(ok.value)
+    return _DESKEW_OK
+
+
 def integrate_frames(grid: VoxelGrid, bank: KernelBank, scans, params: IntegrationParams) -> list:
     """Several scans in one launch sequence (batched config-5 path). Per-frame
     downsampling, discards and first-return are preserved; the final grid is
@@ -256,6 +325,10 @@ def integrate_frames(grid: VoxelGrid, bank: KernelBank, scans, params: Integrati
     scans = list(scans)
     if params.exact_voxels_written:
         # the serial count is per scan: one launch each
+        return [integrate_frame(grid, bank, s, params) for s in scans]
+    if params.compensation != "none" and device_deskew_available():
+        # device deskew: one launch per scan (the per-scan pose interpolation
+        # constants travel as kernel parameters)
         return [integrate_frame(grid, bank, s, params) for s in scans]
     if params.compensation != "none":
         prepped = []

@@ -167,6 +167,82 @@ def config_cases(include_slow=True) -> list:
     return cases
 
 
+@dataclass
+class DeskewCase:
+    """Motion-compensated frames (compensation "se3" / "yaw",
+    integrator.py:91-123): frames are (points, pose, prev_pose, timestamps
+    or None)."""
+    name: str
+    dims: tuple
+    voxel_size: float
+    origin: tuple
+    bank: dict
+    params: dict
+    frames: list
+
+    def input_hash(self) -> str:
+        h = hashlib.sha256()
+        for p, pose, prev, ts in self.frames:
+            for a in (p, pose, prev) + (() if ts is None else (ts,)):
+                h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()[:32]
+
+
+def _euler_pose(yaw, pitch, roll, t):
+    cy, sy, cp, sp, cr, sr = (math.cos(yaw), math.sin(yaw), math.cos(pitch), math.sin(pitch), math.cos(roll),
+                              math.sin(roll))
+    Rz = np.array([[cy, -sy, 0], [sy, cy, 0], [0, 0, 1]])
+    Ry = np.array([[cp, 0, sp], [0, 1, 0], [-sp, 0, cp]])
+    Rx = np.array([[1, 0, 0], [0, cr, -sr], [0, sr, cr]])
+    T = np.eye(4)
+    T[:3, :3] = Rz @ Ry @ Rx
+    T[:3, 3] = t
+    return T
+
+
+def deskew_cases() -> list:
+    """Seeded sweeps with motion during the sweep: heading wraps across +-pi,
+    tilted poses, tiny rotations (Slerp's small-angle branch), explicit
+    timestamps (some outside [0, 1]: clipped) and point-order timestamps,
+    float32 and float64 points, downsampling."""
+    out = []
+    dims, vs, org = (64, 64, 64), 0.1, (0.0, 0.0, 0.0)
+    c = (3.2, 3.2, 3.2)
+    b = dict(size=21, shadow_radius=2)
+
+    def sweep(rng, n, f32):
+        p = rng.uniform(-1.4, 1.4, size=(n, 3))
+        return p.astype(np.float32) if f32 else p
+
+    for mode in ("se3", "yaw"):
+        rng = np.random.default_rng(71 if mode == "se3" else 72)
+        frames = []
+        for k in range(3):
+            y0 = rng.uniform(-math.pi, math.pi)
+            y1 = y0 + rng.uniform(-0.6, 0.6) + (2 * math.pi if k == 1 else 0.0)  # k = 1 wraps
+            T0 = _euler_pose(y0, rng.normal() * 0.05, rng.normal() * 0.05, np.add(c, rng.normal(size=3) * 0.1))
+            T1 = _euler_pose(y1, rng.normal() * 0.05, rng.normal() * 0.05, np.add(c, rng.normal(size=3) * 0.1))
+            frames.append((sweep(rng, 1500, k == 2), T1, T0, None))
+        out.append(DeskewCase(f"deskew_{mode}_linspace", dims, vs, org, b, {"compensation": mode}, frames))
+        frames = []
+        for k in range(3):
+            y0 = rng.uniform(-math.pi, math.pi)
+            T0 = _euler_pose(y0, 0.02, -0.03, np.add(c, rng.normal(size=3) * 0.1))
+            dyaw = 1e-5 if k == 0 else rng.uniform(-0.4, 0.4)  # k = 0: small-angle Slerp
+            T1 = _euler_pose(y0 + dyaw, 0.02 + (0 if k == 0 else 0.03), -0.03, np.add(c, rng.normal(size=3) * 0.1))
+            n = 1800
+            ts = np.sort(rng.uniform(-0.05, 1.05, n))
+            frames.append((sweep(rng, n, k != 1), T1, T0, ts))
+        out.append(DeskewCase(f"deskew_{mode}_ts_ds2", dims, vs, org, b, {"compensation": mode, "downsample": 2},
+                              frames))
+    # config 2's trajectory with the previous scan's pose as the sweep start
+    w = workloads.get(2)
+    frames = [(w.scan(k), w.poses[k], w.poses[k - 1], None) for k in (1, 2, 3)]
+    out.append(DeskewCase("deskew_cfg2_scans1-3_se3", w.dims, w.voxel_size, w.origin,
+                          dict(size=21, shadow_radius=w.shadow_radius), {"compensation": "se3"}, frames))
+    return out
+
+
 def bank_specs() -> list:
     return [
         dict(size=21, shadow_radius=1),

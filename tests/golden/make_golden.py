@@ -127,6 +127,46 @@ def main():
         out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))
         print("wrote", out_path)
         return
+    if "--only-deskew" in sys.argv:
+        # motion-compensated frames through the reference's integrate_frame
+        # (and the hash of its motion_compensate output per frame). The
+        # reference's yaw mode calls Rotation.from_euler("z", angles) with a
+        # 1-D angle array, which scipy >= 1.15 rejects (it wants (n, 1) for a
+        # single axis); for that call only, the angles are reshaped to (n, 1)
+        # — the same rotations older scipy versions built.
+        from scipy.spatial.transform import Rotation
+        from bitsdf.integrator import motion_compensate
+        orig = Rotation.from_euler
+
+        def from_euler_1d(seq, angles, degrees=False):
+            a = np.asarray(angles)
+            if len(seq) == 1 and a.ndim == 1:
+                a = a[:, None]
+            return orig(seq, a, degrees=degrees)
+
+        Rotation.from_euler = staticmethod(from_euler_1d)
+        gold.setdefault("deskew", {})
+        for c in cases.deskew_cases():
+            bank = build_kernel_bank(**c.bank)
+            g = new_grid(c.dims, c.voxel_size, c.origin, memory_cap=1 << 40)
+            params = IntegrationParams(**c.params)
+            stats, moved = [], []
+            t0 = time.perf_counter()
+            for pts, pose, prev, ts in c.frames:
+                st = integrate_frame(g, bank, ScanFrame(points=pts, pose=pose, timestamps=ts, prev_pose=prev), params,
+                                     threads=8)
+                stats.append([st.points_in, st.points_discarded, st.voxels_written])
+                k = slice(None, None, params.downsample)
+                sc = ScanFrame(points=np.asarray(pts, np.float64)[k], pose=pose,
+                               timestamps=None if ts is None else ts[k], prev_pose=prev)
+                moved.append(cases.sha(motion_compensate(sc, params.compensation).points))
+            gold["deskew"][c.name] = {"input": c.input_hash(), "mask": cases.sha(g.mask), "sign": cases.sha(g.sign),
+                                      "hits": cases.sha(g.hits), "stats": stats, "points": moved,
+                                      "ref_seconds": round(time.perf_counter() - t0, 2)}
+            print(c.name, gold["deskew"][c.name], flush=True)
+        out_path.write_text(json.dumps(gold, indent=1, sort_keys=True))
+        print("wrote", out_path)
+        return
     if "--only-snapshots" in sys.argv:
         # add the snapshot hashes of the small cases; every other stored value
         # must come out unchanged

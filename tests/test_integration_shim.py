@@ -45,7 +45,8 @@ def layout(tmp_path_factory):
 
 @pytest.mark.parametrize("pair", [("dbt_params", shim.Params), ("dbt_stats", shim.Stats),
                                   ("dbt_mc_tables", shim.McTables), ("dbt_params", _native.Params),
-                                  ("dbt_stats", _native.Stats)], ids=lambda p: f"{p[1].__module__}.{p[0]}")
+                                  ("dbt_stats", _native.Stats), ("dbt_deskew", shim.Deskew),
+                                  ("dbt_deskew", _native.Deskew)], ids=lambda p: f"{p[1].__module__}.{p[0]}")
 def test_ctypes_structs_match_header(layout, pair):
     cname, cls = pair
     assert ctypes.sizeof(cls) == layout[cname]
@@ -176,3 +177,23 @@ def test_shim_extract_mesh_matches_reference(golden):
         v, f = shim.extract_mesh(g, float(iso), tables)
         assert cases.sha(np.ascontiguousarray(v, np.float64)) == ref["vertices"]
         assert cases.sha(np.ascontiguousarray(f, np.int64)) == ref["triangles"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["deskew_se3_linspace", "deskew_yaw_ts_ds2"])
+def test_shim_deskew_matches_reference(name, golden):
+    """compensation "se3" / "yaw" through the shim: deskewed on the device."""
+    shim.lib(str(_native.LIB_PATH))
+    c = next(x for x in cases.deskew_cases() if x.name == name)
+    g = _standin(SimpleNamespace(dims=c.dims, voxel_size=c.voxel_size, origin=c.origin, init=None))
+    bank = build_kernel_bank(**c.bank)
+    prm = _params(c.params)
+    prm.compensation = c.params["compensation"]
+    ref = golden["deskew"][name]
+    for (pts, pose, prev, ts), want in zip(c.frames, ref["stats"]):
+        scan = SimpleNamespace(points=np.asarray(pts, np.float64).reshape(-1, 3), pose=pose, timestamps=ts,
+                               prev_pose=prev)
+        st = shim.integrate_frame(g, bank, scan, prm)
+        assert [st.points_in, st.points_discarded] == want[:2]
+    assert shim._DESKEW_OK
+    assert (cases.sha(g.mask), cases.sha(g.sign), cases.sha(g.hits)) == (ref["mask"], ref["sign"], ref["hits"])
