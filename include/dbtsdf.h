@@ -169,6 +169,17 @@ DBT_API int dbt_bank_destroy(dbt_bank* b);
  * D2H; returns when the grid is updated. pose: 4x4 row-major float64. */
 DBT_API int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,
                         int64_t n, const double pose[16], const dbt_params* p, dbt_stats* out);
+/* Asynchronous dbt_integrate_frame: copies the scan to the device on a copy
+ * stream and enqueues the launch sequence, then returns a ticket at once;
+ * consecutive calls pipeline (the next scan's copy and the host work overlap
+ * the previous scan's kernels). The points must stay valid until
+ * dbt_frame_wait of that ticket returns. Stats of a ticket stay readable
+ * until 4 more calls have been issued. Default launch path only (no
+ * first-return, exact voxels_written or measurement flags: DBT_ERR_CONFIG).
+ * Any other call on the grid is ordered after the queued ones. */
+DBT_API int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
+                              const double pose[16], const dbt_params* p, int64_t* ticket);
+DBT_API int dbt_frame_wait(dbt_grid* g, int64_t ticket, dbt_stats* out);
 /* S scans in one launch sequence (config 5): points concatenated, counts[S],
  * poses[S*16]; out[S] per-scan stats (voxels_written reported on out[0]). */
 DBT_API int dbt_integrate_batch(dbt_grid* g, const dbt_bank* b, const void* points, int dtype,

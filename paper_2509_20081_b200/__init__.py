@@ -34,6 +34,8 @@ from .integrator import (
     ScanFrame,
     integrate_frame,
     integrate_frames,
+    integrate_frame_async,
+    PendingFrame,
     integrate_point,
     integrate_points,
 )
@@ -61,6 +63,8 @@ __all__ = [
     "FrameStats",
     "integrate_frame",
     "integrate_frames",
+    "integrate_frame_async",
+    "PendingFrame",
     "integrate_point",
     "integrate_points",
     "TriangleMesh",

@@ -136,6 +136,8 @@ SIGNATURES = {
     "dbt_replica_mark": (ctypes.c_int, [_vp]),
     "dbt_replica_pack": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "dbt_replica_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
+    "dbt_integrate_frame_async": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp, _c_i64p]),
+    "dbt_frame_wait": (ctypes.c_int, [_vp, ctypes.c_int64, _vp]),
     "dbt_deskew_available": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
     "dbt_integrate_frame_deskew": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, _vp,
                                                   _vp]),

@@ -167,6 +167,21 @@ struct LaunchCounters {
   unsigned long long pad[2];
 };
 
+// One in-flight asynchronous single-scan call (dbt_integrate_frame_async):
+// the device copy of its points, its counters' pinned destination, its
+// completion event.
+struct AsyncSlot {
+  int64_t ticket = -1;
+  cudaEvent_t copied = nullptr, done = nullptr;
+  void* d_buf = nullptr;
+  int64_t cap = 0;
+  LaunchCounters* h = nullptr;  // LaunchCounters + one ScanCounters, pinned
+  int64_t points_in = 0;
+  dbt_params p{};
+  double t0 = 0;
+};
+constexpr int kAsyncSlots = 4;
+
 struct ProfEvent {
   cudaEvent_t a, b;
   int kernel;  // index into prof_names
@@ -299,6 +314,14 @@ struct dbt_grid {
   int sweep_ch = 0;                            // cached sweep launch shape
   int64_t sweep_blocks = 0;
   double last_device_ms = 0;
+  // asynchronous single-scan calls (integrate.cu): copies on cstream
+  dbt::AsyncSlot aslot[dbt::kAsyncSlots];
+  // one executable graph per async slot (instantiated from ggraph): updating
+  // the arguments of an executable graph that is still running waits for it,
+  // so pipelined calls must not share one
+  cudaGraphExec_t aexec[dbt::kAsyncSlots] = {};
+  int64_t a_next = 0;
+  cudaStream_t cstream = nullptr;
 };
 
 namespace dbt {

@@ -387,6 +387,15 @@ int dbt_grid_destroy(dbt_grid* g) {
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);
   if (g->ev_join) cudaEventDestroy(g->ev_join);
   if (g->aux) cudaStreamDestroy(g->aux);
+  for (auto& sl : g->aslot) {
+    if (sl.copied) cudaEventDestroy(sl.copied);
+    if (sl.done) cudaEventDestroy(sl.done);
+    if (sl.d_buf) cudaFree(sl.d_buf);
+    if (sl.h) cudaFreeHost(sl.h);
+  }
+  if (g->cstream) cudaStreamDestroy(g->cstream);
+  for (auto& e : g->aexec)
+    if (e) cudaGraphExecDestroy(e);
   if (g->stream && g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
   return DBT_OK;

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -1928,7 +1929,7 @@ bool graph_eligible(const dbt_grid* g, const dbt_bank* b, const dbt_params* p) {
 }
 
 int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype, int64_t n_raw, const double* pose,
-                    const dbt_params* p, cudaStream_t st) {
+                    const dbt_params* p, cudaStream_t st, int exec_slot = -1) {
   const int64_t n = (n_raw + p->downsample - 1) / p->downsample;
   if (g->sweep_ch != -b->K || n > g->cap_pts || 2 * n > g->cap_hash) {
     // first launch with this bank / growth of the scratch buffers: the one-time
@@ -1948,6 +1949,10 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
     if (g->ggraph) cudaGraphDestroy(g->ggraph);
     g->gexec = nullptr;
     g->ggraph = nullptr;
+    for (auto& e : g->aexec) {
+      if (e) cudaGraphExecDestroy(e);  // stale shape (a running launch completes first)
+      e = nullptr;
+    }
     // the persistent sweep grid size is measured on first use: make sure it
     // is known before the key is stored
     gc.capture = true;
@@ -1996,13 +2001,18 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
     gc.replay = true;
     int rc = launch_integrate(g, b, d_src, dtype, &n_raw, 1, pose, p, nullptr, nullptr, st, nullptr, &gc);
     if (rc) return rc;
+    cudaGraphExec_t ex = g->gexec;
+    if (exec_slot >= 0) {
+      if (!g->aexec[exec_slot]) DBT_CUDA(cudaGraphInstantiate(&g->aexec[exec_slot], g->ggraph, 0));
+      ex = g->aexec[exec_slot];
+    }
     cudaKernelNodeParams kp = {};
     void* pargs[] = {&gc.pa};
     kp.func = (void*)prep_kernel<false>;
     kp.gridDim = dim3(gc.prep_blocks);
     kp.blockDim = dim3(kPrepThreads);
     kp.kernelParams = pargs;
-    DBT_CUDA(cudaGraphExecKernelNodeSetParams(g->gexec, g->gprep, &kp));
+    DBT_CUDA(cudaGraphExecKernelNodeSetParams(ex, g->gprep, &kp));
     if (gc.has_shadow != (g->gshadow != nullptr)) return set_error(DBT_ERR_GENERIC, "graph shape changed");
     if (gc.has_shadow) {
       void* sargs[] = {&gc.sa};
@@ -2010,8 +2020,11 @@ int integrate_graph(dbt_grid* g, const dbt_bank* b, const void* d_src, int dtype
       kp.gridDim = dim3(gc.shadow_blocks);
       kp.blockDim = dim3(256);
       kp.kernelParams = sargs;
-      DBT_CUDA(cudaGraphExecKernelNodeSetParams(g->gexec, g->gshadow, &kp));
+      DBT_CUDA(cudaGraphExecKernelNodeSetParams(ex, g->gshadow, &kp));
     }
+    DBT_CUDA(cudaGraphLaunch(ex, st));
+    add_launches(g->gkernels);
+    return DBT_OK;
   }
   DBT_CUDA(cudaGraphLaunch(g->gexec, st));
   add_launches(g->gkernels);
@@ -2188,6 +2201,104 @@ int dbt_integrate_scans(dbt_grid* g, const dbt_bank* b, const void* const* point
 int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
                         const double pose[16], const dbt_params* p, dbt_stats* out) {
   return integrate_host(g, b, points, dtype, &n, 1, pose, p, out);
+}
+
+// Asynchronous single-scan call: the scan is copied into a device buffer
+// of its slot on a copy stream (overlapping the previous calls' kernels),
+// the launch sequence (graph) follows on the grid stream, and the counters
+// land in the slot's pinned block; dbt_frame_wait collects them. Up to
+// kAsyncSlots calls are in flight; a fifth call waits for the oldest slot's
+// completion (its stats stay readable until the slot is reused).
+int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
+                              const double pose[16], const dbt_params* p, int64_t* ticket) {
+  const double t0 = now_ms();
+  int rc = check(g, b);
+  if (!rc) rc = validate_params(p);
+  if (rc) return rc;
+  if (!ticket) return set_error(DBT_ERR_CONFIG, "null ticket");
+  if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
+  if (n < 0) return set_error(DBT_ERR_CONFIG, "negative point count");
+  if (!graph_eligible(g, b, p))
+    return set_error(DBT_ERR_CONFIG, "asynchronous calls take the default launch path (no first-return, exact "
+                                     "count or measurement flags)");
+  cudaStream_t st = g->stream;
+  if (g->last_st != st) {
+    DBT_CUDA(cudaDeviceSynchronize());
+    g->last_st = st;
+  }
+  if (!g->cstream) DBT_CUDA(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
+  const int64_t tk = g->a_next++;
+  AsyncSlot& sl = g->aslot[tk % kAsyncSlots];
+  if (!sl.done) {
+    DBT_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    DBT_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+    DBT_CUDA(cudaHostAlloc((void**)&sl.h, sizeof(LaunchCounters) + sizeof(ScanCounters), cudaHostAllocDefault));
+  }
+  static const bool dbg = getenv("DBT_DEBUG_ASYNC") != nullptr;
+  double tA = now_ms();
+  if (sl.ticket >= 0) DBT_CUDA(wait_event(sl.done));  // the slot's previous call (buffer and counters free)
+  double tB = now_ms();
+  const size_t esz = dtype == DBT_F32 ? 12 : 24;
+  if (n * (int64_t)esz > sl.cap) {
+    // with headroom (scan sizes vary by their dropouts) and geometric
+    // growth: cudaFree / cudaMalloc synchronise the device
+    if (sl.d_buf) DBT_CUDA(cudaFree(sl.d_buf));
+    sl.d_buf = nullptr;
+    sl.cap = std::max<int64_t>(n * (int64_t)esz * 5 / 4, sl.cap + sl.cap / 2);
+    DBT_CUDA(cudaMalloc(&sl.d_buf, sl.cap));
+  }
+  sl.ticket = tk;
+  sl.p = *p;
+  sl.points_in = (n + p->downsample - 1) / p->downsample;
+  sl.t0 = t0;
+  if (n == 0) {
+    std::memset(sl.h, 0, sizeof(LaunchCounters) + sizeof(ScanCounters));
+    DBT_CUDA(cudaEventRecord(sl.done, st));
+    *ticket = tk;
+    return DBT_OK;
+  }
+  DBT_CUDA(cudaMemcpyAsync(sl.d_buf, points, n * esz, cudaMemcpyHostToDevice, g->cstream));
+  DBT_CUDA(cudaEventRecord(sl.copied, g->cstream));
+  DBT_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
+  double tC = now_ms();
+  rc = integrate_graph(g, b, sl.d_buf, dtype, n, pose, p, st, (int)(tk % kAsyncSlots));
+  if (rc) return rc;
+  double tD = now_ms();
+  DBT_CUDA(cudaMemcpyAsync(sl.h, g->d_lcnt, sizeof(LaunchCounters) + sizeof(ScanCounters), cudaMemcpyDeviceToHost,
+                           st));
+  DBT_CUDA(cudaEventRecord(sl.done, st));
+  if (dbg) {
+    cudaPointerAttributes at;
+    int ty = cudaPointerGetAttributes(&at, points) == cudaSuccess ? (int)at.type : -1;
+    cudaGetLastError();
+    fprintf(stderr, "async %lld: pre %.1f wait %.1f copy %.1f graph %.1f tail %.1f us (host mem type %d, %p, %lld B)\n",
+            (long long)tk, (tA - t0) * 1e3, (tB - tA) * 1e3, (tC - tB) * 1e3, (tD - tC) * 1e3, (now_ms() - tD) * 1e3,
+            ty, points, (long long)(n * esz));
+  }
+  *ticket = tk;
+  return DBT_OK;
+}
+
+int dbt_frame_wait(dbt_grid* g, int64_t ticket, dbt_stats* out) {
+  if (!g) return set_error(DBT_ERR_CONFIG, "null grid handle");
+  if (!out) return set_error(DBT_ERR_CONFIG, "null stats");
+  if (ticket < 0 || ticket >= g->a_next) return set_error(DBT_ERR_CONFIG, "unknown ticket");
+  AsyncSlot& sl = g->aslot[ticket % kAsyncSlots];
+  if (sl.ticket != ticket) return set_error(DBT_ERR_CONFIG, "ticket expired (more than 4 calls issued since)");
+  DBT_CUDA(wait_event(sl.done));
+  const LaunchCounters& lc = *sl.h;
+  const ScanCounters& sc = *reinterpret_cast<const ScanCounters*>(sl.h + 1);
+  std::memset(out, 0, sizeof(*out));
+  out->points_in = sl.points_in;
+  out->points_discarded = sl.points_in - (int64_t)sc.n_ok;
+  out->points_applied = (int64_t)sc.n_ok;
+  out->bin_fallbacks = (int64_t)sc.n_fallback;
+  out->voxels_written = (int64_t)lc.changed;
+  out->unique_centers = (int64_t)lc.n_unique;
+  out->centers_skipped = (int64_t)lc.skipped;
+  out->rows_swept = (int64_t)lc.rows;
+  out->elapsed_ms = now_ms() - sl.t0;
+  return DBT_OK;
 }
 
 int dbt_deskew_available(int32_t* ok) {

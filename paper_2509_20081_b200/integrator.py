@@ -252,9 +252,11 @@ def integrate_points(grid: VoxelGrid, bank: KernelBank, p_map, sensor_pos, param
 def integrate_frame(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: IntegrationParams,
                     threads: int = 1) -> FrameStats:
     """Fuse one scan (integrator.py:207-287): the points cross the host link
-    once (pinned scans are read zero-copy by the preprocessing kernel,
-    pageable ones staged by one H2D copy), then the device launch sequence
-    and one D2H copy of the counters."""
+    once (pinned scans are read zero-copy by the preprocessing kernel;
+    pageable ones are first copied by a host thread pool into pinned, mapped
+    staging and then read the same way), then the device launch sequence and
+    one D2H copy of the counters. compensation "yaw"/"se3" deskews on the
+    device (deskew_params + csrc/deskew.cuh)."""
     t0 = time.perf_counter()
     if scan.n_points == 0:
         return FrameStats()
@@ -297,6 +299,52 @@ def integrate_frame(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: 
                                                     dtype, pts.shape[0], pose_p, ctypes.byref(prm), ctypes.byref(st)))
     grid.pull_host()
     return FrameStats.from_native(st, (time.perf_counter() - t0) * 1e3)
+
+
+class PendingFrame:
+    """A queued integrate_frame_async call: ``result()`` waits for it and
+    returns its FrameStats (idempotent). Keeps the scan's points alive until
+    then (the device copy reads them asynchronously)."""
+
+    def __init__(self, grid: VoxelGrid, ticket: int | None, keep=None, stats: FrameStats | None = None):
+        self._grid, self._ticket, self._keep, self._stats = grid, ticket, keep, stats
+
+    def done(self) -> bool:
+        return self._stats is not None
+
+    def result(self) -> FrameStats:
+        if self._stats is None:
+            st = _native.Stats()
+            _native.check(_native.lib().dbt_frame_wait(self._grid.handle, self._ticket, ctypes.byref(st)))
+            self._stats = FrameStats.from_native(st, st.elapsed_ms)
+            self._keep = None
+        return self._stats
+
+
+def integrate_frame_async(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, params: IntegrationParams) -> PendingFrame:
+    """integrate_frame without waiting (dbt_integrate_frame_async): the scan
+    is copied to the device on a copy stream and its launch sequence queued;
+    consecutive calls pipeline, so the next scan's host work and host->device
+    copy overlap this scan's kernels. Collect FrameStats with ``.result()``
+    (at most 4 calls may be outstanding: the fifth call waits for the
+    oldest). The grid's host mirror is dropped; reading grid.mask/sign/hits
+    orders after every queued call. Calls the default path cannot take
+    (compensation, first-return, exact voxels_written) run synchronously."""
+    if (params.compensation != "none" or params.first_return_per_voxel or params.exact_voxels_written
+            or scan.n_points == 0):
+        return PendingFrame(grid, None, stats=integrate_frame(grid, bank, scan, params))
+    grid.h_max = params.h_max
+    grid.t_occ = params.t_occ
+    grid.push_host()
+    grid._host = None
+    pts, dtype = scan.device_payload()
+    pose, pose_p = _pose_arg(scan.pose)
+    prm = params.native()
+    ticket = ctypes.c_int64()
+    _native.check(_native.lib().dbt_integrate_frame_async(grid.handle, bank.device_handle(grid.device),
+                                                          _native.ptr(pts), dtype, pts.shape[0], pose_p,
+                                                          ctypes.byref(prm), ctypes.byref(ticket)))
+    return PendingFrame(grid, ticket.value, keep=(pts, pose))
 
 
 _DESKEW_OK = None

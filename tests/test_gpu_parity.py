@@ -958,3 +958,62 @@ def test_bin_fallback_counted_per_scan(shadow_radius):
     oracle.integrate_frame(og, ob, pts_b, eye)
     m, s, h = g.download_range(0, dims[0])
     assert np.array_equal(m, og.mask) and np.array_equal(s, og.sign) and np.array_equal(h, og.hits)
+
+
+class TestAsyncFrames:
+    """integrate_frame_async (dbt_integrate_frame_async / dbt_frame_wait):
+    pipelined calls give the same grid and FrameStats as synchronous ones."""
+
+    @pytest.mark.parametrize("name", ["cfg2_scans0-2", "yaw_frames_f32", "nonfresh_cone_h200_t2"])
+    def test_async_matches_reference(self, name, golden):
+        from paper_2509_20081_b200 import integrate_frame_async
+
+        c = next(c for c in SMALL + CONFIG if c.name == name)
+        ref = golden["cases"][name]
+        bank = build_kernel_bank(**c.bank)
+        g = new_grid(c.dims, c.voxel_size, c.origin)
+        if c.init is not None:
+            g.mask[...], g.sign[...], g.hits[...] = c.init
+        params = IntegrationParams(**c.params)
+        futs = [integrate_frame_async(g, bank, ScanFrame(points=p, pose=pose), params) for p, pose in c.frames]
+        sts = [f.result() for f in futs]
+        assert [[s.points_in, s.points_discarded] for s in sts] == [r[:2] for r in ref["stats"]]
+        m, s, h = g.download_range(0, c.dims[0])
+        assert (cases.sha(m), cases.sha(s), cases.sha(h)) == (ref["mask"], ref["sign"], ref["hits"])
+
+    def test_trajectory_pipelined_equals_sync(self):
+        """40 config-2 scans, at most 2 outstanding, against synchronous
+        calls: identical grids and per-scan counts."""
+        import workloads
+        from paper_2509_20081_b200 import integrate_frame_async
+
+        w = workloads.get(2)
+        bank = build_kernel_bank(shadow_radius=w.shadow_radius)
+        scans = [w.scan(k) for k in range(40)]
+        a, b = new_grid(w.dims, w.voxel_size, w.origin), new_grid(w.dims, w.voxel_size, w.origin)
+        sync = [integrate_frame(a, bank, ScanFrame(points=s, pose=w.poses[k]), IntegrationParams())
+                for k, s in enumerate(scans)]
+        pend, got = [], []
+        for k, s in enumerate(scans):
+            pend.append(integrate_frame_async(b, bank, ScanFrame(points=s, pose=w.poses[k]), IntegrationParams()))
+            if len(pend) > 2:
+                got.append(pend.pop(0).result())
+        got += [f.result() for f in pend]
+        assert [(x.points_in, x.points_discarded) for x in got] == [(x.points_in, x.points_discarded) for x in sync]
+        for x0, x1 in ((0, 211), (211, w.dims[0])):
+            ma, sa, ha = a.download_range(x0, x1)
+            mb, sb, hb = b.download_range(x0, x1)
+            assert np.array_equal(ma, mb) and np.array_equal(sa, sb) and np.array_equal(ha, hb)
+
+    def test_expired_ticket_and_result_idempotent(self):
+        from paper_2509_20081_b200 import integrate_frame_async
+
+        bank = build_kernel_bank()
+        g = new_grid((48, 48, 48), 0.1)
+        pts = np.random.default_rng(0).uniform(1.2, 3.6, size=(300, 3))
+        futs = [integrate_frame_async(g, bank, ScanFrame(points=pts, pose=np.eye(4)), IntegrationParams())
+                for _ in range(6)]
+        with pytest.raises(ConfigurationError):
+            futs[0].result()  # 5 calls issued since: its slot was reused
+        r = futs[5].result()
+        assert r.points_in == 300 and futs[5].result() is r
