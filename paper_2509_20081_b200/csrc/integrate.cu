@@ -789,13 +789,12 @@ struct NoInfo {
 // surviving row tasks, reserved as one range of `total` slots through *q_n
 // (lane 0) and written with put(slot, task) (kEmptyKey for a row whose dz
 // interval is empty).
-template <typename Put, typename Info>
-__device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put, Info info) {
-  const int R = a.R, K = a.K;
-  const int64_t sx = a.ny * a.nzp;
-  const uint16_t* rowd = a.rowd;
-  int64_t cx, cy, cz;
-  unpack_center(centre, cx, cy, cz);
+// The certificates phase A cuts with (one warp, every lane gets the same
+// bits): the 26 adjacent centres (nb, bit (a+1)*9 + (b+1)*3 + (c+1), bit 13
+// cleared), the axis neighbours at distance 2-5 (axm) and, for sparse
+// neighbourhoods, the norm-2 plane neighbours (plm).
+__device__ __forceinline__ void gather_certs(const CullArgs& a, int64_t cx, int64_t cy, int64_t cz, int lane,
+                                             uint32_t& nb, uint32_t& axm, uint32_t& plm) {
   // neighbour certificates: 27 bits, bit (a+1)*9 + (b+1)*3 + (c+1)
   uint32_t nb3 = 0;
   if (lane < 9) {
@@ -835,12 +834,12 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
       ax = (up << 16) | (dn << 20);
     }
   }
-  const uint32_t nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
-  const uint32_t axm = __reduce_or_sync(0xffffffffu, ax);
+  nb = __reduce_or_sync(0xffffffffu, nb3) & ~(1u << 13);  // not c itself
+  axm = __reduce_or_sync(0xffffffffu, ax);
   // sparse neighbourhood (few of the 26 adjacent centres certified): also
   // gather the norm-2 plane neighbours below (a second round of loads,
   // skipped for dense surfaces where they add little)
-  uint32_t plm = 0;
+  plm = 0;
   if (__popc(nb) < kPlaneGatherBelow) {
     // plane neighbours of norm 2 with one zero coordinate besides the
     // axes: (a, b, 0) (lanes 0-11, bit cz) and (a, 0, c) (lanes 12-15: rows
@@ -876,6 +875,17 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     }
     plm = __reduce_or_sync(0xffffffffu, plb);
   }
+}
+
+template <typename Put, typename Info>
+__device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put, Info info) {
+  const int R = a.R, K = a.K;
+  const int64_t sx = a.ny * a.nzp;
+  const uint16_t* rowd = a.rowd;
+  int64_t cx, cy, cz;
+  unpack_center(centre, cx, cy, cz);
+  uint32_t nb, axm, plm;
+  gather_certs(a, cx, cy, cz, lane, nb, axm, plm);
 #define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
   // per lane: kernel x-offset dx, its dy interval and z-cut terms
   const int dx = lane - R;
