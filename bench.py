@@ -299,7 +299,7 @@ def config_desc(w, batch, interleave=0, multi="single"):
     scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
     par = {"single": "single GPU",
            "replica": "data-parallel whole-grid replicas: each rank integrates a contiguous segment of the window, "
-                      "one exact merge (MIN/MIN/SUM all-reduces) at the end of every pass, timed",
+                      "one exact merge at the end of every pass (MIN/MIN/SUM all-reduces over the 16^3 bricks any rank touched), timed",
            "slab": f"x-interleaved slabs ({interleave}-plane blocks dealt round-robin over the ranks): every rank "
                    "stamps only the part of each return's cube inside its planes; points broadcast from rank 0 "
                    "over NCCL every step"}[multi]
@@ -429,8 +429,10 @@ def main():
     win_dev = [to_dev(b) for b in win]
     nw = len(win)
     # replicas: every pass over the window is split into W contiguous segments
+    # (slab parts all integrate every batch: one segment, the whole window)
     W = world if replica else 1
-    seg = (rank * nw // W, (rank + 1) * nw // W)
+    r_seg = rank if replica else 0
+    seg = (r_seg * nw // W, (r_seg + 1) * nw // W)
     P = -(-nw // W)  # steps per pass (longest segment)
 
     def batch_of(s):

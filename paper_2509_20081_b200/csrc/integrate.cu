@@ -312,16 +312,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(PrepArgs a) {
         // the centres whose cube touches its planes).
         const int64_t cidx = (cx * a.ny + cy) * a.nzp + cz;
         const uint32_t bit = 1u << (cidx & 31);
-#ifdef DBT_HINT_CLAIM_EL
-        uint32_t prev;
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
-                     : "=r"(prev) : "l"(a.stamped + (cidx >> 5)), "r"(bit), "l"(pol) : "memory");
-        claimed = (prev & bit) != 0;
-#else
         claimed = (atomicOr(a.stamped + (cidx >> 5), bit) & bit) != 0;
-#endif
         append = !claimed;
       }
       // the hash table dedups centres for the sweep when certificates are not
