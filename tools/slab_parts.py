@@ -68,7 +68,10 @@ def run_part(g, timed_from=10):
 single = None
 for N in Ns:
     worst, worst_k, parts = 0.0, None, []
+    only = os.environ.get("SLAB_ONLY")  # "N:r": run only part r of N (profiling)
     for r in range(N):
+        if only and (int(only.split(":")[0]) != N or int(only.split(":")[1]) != r):
+            continue
         width = min(WIDTH, w.dims[0] // (2 * N))
         g = VoxelGrid(w.dims, w.voxel_size, w.origin, interleave=(width, N, r)) if N > 1 else \
             VoxelGrid(w.dims, w.voxel_size, w.origin)
@@ -83,6 +86,6 @@ for N in Ns:
     prep = worst_k.get("prep_kernel", 0.0)
     crit = 1.3 * (single / N + prep) if single else float("nan")
     print(f"config {cfg} N={N}: slowest part {worst:.1f} us/scan (prep {prep:.1f}, sweep "
-          f"{worst_k.get('sweep_kernel', 0):.1f}, shadow {worst_k.get('shadow_kernel', 0):.1f}); single {single:.1f}; "
+          f"{worst_k.get('sweep_kernel', 0):.1f}, shadow {worst_k.get('shadow_kernel', 0):.1f}); single {single or float('nan'):.1f}; "
           f"criterion 1.3*(single/N + prep) = {crit:.1f} -> {'met' if worst <= crit else 'NOT met'}; width {WIDTH}, "
           f"parts {parts}", flush=True)
