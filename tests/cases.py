@@ -240,6 +240,15 @@ def deskew_cases() -> list:
     frames = [(w.scan(k), w.poses[k], w.poses[k - 1], None) for k in (1, 2, 3)]
     out.append(DeskewCase("deskew_cfg2_scans1-3_se3", w.dims, w.voxel_size, w.origin,
                           dict(size=21, shadow_radius=w.shadow_radius), {"compensation": "se3"}, frames))
+    # config 3's street trajectory (262 k returns per scan), yaw mode with
+    # per-return times in firing order (azimuth-major sweep)
+    w = workloads.get(3)
+    frames = []
+    for k in (1, 2):
+        pts = w.scan(k)
+        frames.append((pts, w.poses[k], w.poses[k - 1], np.linspace(0.0, 1.0, len(pts))[::-1].copy()))
+    out.append(DeskewCase("deskew_cfg3_scans1-2_yaw", w.dims, w.voxel_size, w.origin,
+                          dict(size=21, shadow_radius=w.shadow_radius), {"compensation": "yaw"}, frames))
     return out
 
 
