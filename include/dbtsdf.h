@@ -174,9 +174,10 @@ DBT_API int dbt_integrate_frame(dbt_grid* g, const dbt_bank* b, const void* poin
  * consecutive calls pipeline (the next scan's copy and the host work overlap
  * the previous scan's kernels). The points must stay valid until
  * dbt_frame_wait of that ticket returns. Stats of a ticket stay readable
- * until 4 more calls have been issued. Default launch path only (no
- * first-return, exact voxels_written or measurement flags: DBT_ERR_CONFIG).
- * Any other call on the grid is ordered after the queued ones. */
+ * until 4 more calls have been issued. Any parameters of dbt_integrate_frame
+ * (the default path replays a CUDA graph per in-flight slot; first-return,
+ * exact voxels_written and measurement flags launch directly). Any other
+ * call on the grid is ordered after the queued ones. */
 DBT_API int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points, int dtype, int64_t n,
                               const double pose[16], const dbt_params* p, int64_t* ticket);
 DBT_API int dbt_frame_wait(dbt_grid* g, int64_t ticket, dbt_stats* out);

@@ -2219,9 +2219,6 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
   if (!ticket) return set_error(DBT_ERR_CONFIG, "null ticket");
   if (dtype != DBT_F32 && dtype != DBT_F64) return set_error(DBT_ERR_CONFIG, "points dtype must be f32 or f64");
   if (n < 0) return set_error(DBT_ERR_CONFIG, "negative point count");
-  if (!graph_eligible(g, b, p))
-    return set_error(DBT_ERR_CONFIG, "asynchronous calls take the default launch path (no first-return, exact "
-                                     "count or measurement flags)");
   cudaStream_t st = g->stream;
   if (g->last_st != st) {
     DBT_CUDA(cudaDeviceSynchronize());
@@ -2262,7 +2259,13 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
   DBT_CUDA(cudaEventRecord(sl.copied, g->cstream));
   DBT_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
   double tC = now_ms();
-  rc = integrate_graph(g, b, sl.d_buf, dtype, n, pose, p, st, (int)(tk % kAsyncSlots));
+  // the default path replays the slot's own executable graph; other launch
+  // shapes (first-return, exact count, measurement flags, profiling) are
+  // issued directly
+  if (graph_eligible(g, b, p))
+    rc = integrate_graph(g, b, sl.d_buf, dtype, n, pose, p, st, (int)(tk % kAsyncSlots));
+  else
+    rc = launch_integrate(g, b, sl.d_buf, dtype, &n, 1, pose, p, nullptr, nullptr, st, nullptr);
   if (rc) return rc;
   double tD = now_ms();
   DBT_CUDA(cudaMemcpyAsync(sl.h, g->d_lcnt, sizeof(LaunchCounters) + sizeof(ScanCounters), cudaMemcpyDeviceToHost,
@@ -2292,9 +2295,9 @@ int dbt_frame_wait(dbt_grid* g, int64_t ticket, dbt_stats* out) {
   std::memset(out, 0, sizeof(*out));
   out->points_in = sl.points_in;
   out->points_discarded = sl.points_in - (int64_t)sc.n_ok;
-  out->points_applied = (int64_t)sc.n_ok;
+  out->points_applied = sl.p.first_return ? (int64_t)sc.n_applied : (int64_t)sc.n_ok;
   out->bin_fallbacks = (int64_t)sc.n_fallback;
-  out->voxels_written = (int64_t)lc.changed;
+  out->voxels_written = (int64_t)((sl.p.flags & DBT_FLAG_EXACT_WRITTEN) ? lc.exact_written : lc.changed);
   out->unique_centers = (int64_t)lc.n_unique;
   out->centers_skipped = (int64_t)lc.skipped;
   out->rows_swept = (int64_t)lc.rows;

@@ -328,10 +328,9 @@ def integrate_frame_async(grid: VoxelGrid, bank: KernelBank, scan: ScanFrame, pa
     copy overlap this scan's kernels. Collect FrameStats with ``.result()``
     (at most 4 calls may be outstanding: the fifth call waits for the
     oldest). The grid's host mirror is dropped; reading grid.mask/sign/hits
-    orders after every queued call. Calls the default path cannot take
-    (compensation, first-return, exact voxels_written) run synchronously."""
-    if (params.compensation != "none" or params.first_return_per_voxel or params.exact_voxels_written
-            or scan.n_points == 0):
+    orders after every queued call. Motion-compensated scans run
+    synchronously (integrate_frame)."""
+    if params.compensation != "none" or scan.n_points == 0:
         return PendingFrame(grid, None, stats=integrate_frame(grid, bank, scan, params))
     grid.h_max = params.h_max
     grid.t_occ = params.t_occ

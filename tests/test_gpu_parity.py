@@ -964,7 +964,8 @@ class TestAsyncFrames:
     """integrate_frame_async (dbt_integrate_frame_async / dbt_frame_wait):
     pipelined calls give the same grid and FrameStats as synchronous ones."""
 
-    @pytest.mark.parametrize("name", ["cfg2_scans0-2", "yaw_frames_f32", "nonfresh_cone_h200_t2"])
+    @pytest.mark.parametrize("name", ["cfg2_scans0-2", "yaw_frames_f32", "nonfresh_cone_h200_t2",
+                                      "frame500_first_return", "frame500_downsample3"])
     def test_async_matches_reference(self, name, golden):
         from paper_2509_20081_b200 import integrate_frame_async
 
@@ -1004,6 +1005,18 @@ class TestAsyncFrames:
             ma, sa, ha = a.download_range(x0, x1)
             mb, sb, hb = b.download_range(x0, x1)
             assert np.array_equal(ma, mb) and np.array_equal(sa, sb) and np.array_equal(ha, hb)
+
+    def test_async_exact_voxels_written(self, golden):
+        from paper_2509_20081_b200 import integrate_frame_async
+
+        c = next(c for c in SMALL + CONFIG if c.name == "cfg2_scans0-2")
+        ref = golden["cases"][c.name]
+        bank = build_kernel_bank(**c.bank)
+        g = new_grid(c.dims, c.voxel_size, c.origin)
+        params = IntegrationParams(exact_voxels_written=True, **c.params)
+        futs = [integrate_frame_async(g, bank, ScanFrame(points=p, pose=pose), params) for p, pose in c.frames]
+        assert [[f.result().points_in, f.result().points_discarded, f.result().voxels_written] for f in futs] == \
+            ref["stats"]
 
     def test_expired_ticket_and_result_idempotent(self):
         from paper_2509_20081_b200 import integrate_frame_async
