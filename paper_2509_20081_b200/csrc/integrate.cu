@@ -2232,10 +2232,7 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
     DBT_CUDA(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
     DBT_CUDA(cudaHostAlloc((void**)&sl.h, sizeof(LaunchCounters) + sizeof(ScanCounters), cudaHostAllocDefault));
   }
-  static const bool dbg = getenv("DBT_DEBUG_ASYNC") != nullptr;
-  double tA = now_ms();
   if (sl.ticket >= 0) DBT_CUDA(wait_event(sl.done));  // the slot's previous call (buffer and counters free)
-  double tB = now_ms();
   const size_t esz = dtype == DBT_F32 ? 12 : 24;
   if (n * (int64_t)esz > sl.cap) {
     // with headroom (scan sizes vary by their dropouts) and geometric
@@ -2258,7 +2255,6 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
   DBT_CUDA(cudaMemcpyAsync(sl.d_buf, points, n * esz, cudaMemcpyHostToDevice, g->cstream));
   DBT_CUDA(cudaEventRecord(sl.copied, g->cstream));
   DBT_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-  double tC = now_ms();
   // the default path replays the slot's own executable graph; other launch
   // shapes (first-return, exact count, measurement flags, profiling) are
   // issued directly
@@ -2267,18 +2263,9 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
   else
     rc = launch_integrate(g, b, sl.d_buf, dtype, &n, 1, pose, p, nullptr, nullptr, st, nullptr);
   if (rc) return rc;
-  double tD = now_ms();
   DBT_CUDA(cudaMemcpyAsync(sl.h, g->d_lcnt, sizeof(LaunchCounters) + sizeof(ScanCounters), cudaMemcpyDeviceToHost,
                            st));
   DBT_CUDA(cudaEventRecord(sl.done, st));
-  if (dbg) {
-    cudaPointerAttributes at;
-    int ty = cudaPointerGetAttributes(&at, points) == cudaSuccess ? (int)at.type : -1;
-    cudaGetLastError();
-    fprintf(stderr, "async %lld: pre %.1f wait %.1f copy %.1f graph %.1f tail %.1f us (host mem type %d, %p, %lld B)\n",
-            (long long)tk, (tA - t0) * 1e3, (tB - tA) * 1e3, (tC - tB) * 1e3, (tD - tC) * 1e3, (now_ms() - tD) * 1e3,
-            ty, points, (long long)(n * esz));
-  }
   *ticket = tk;
   return DBT_OK;
 }

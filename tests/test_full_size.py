@@ -35,6 +35,15 @@ def _scan4(k):
     return workloads.get(4).scan(k)
 
 
+def _scan3(k):
+    return workloads.get(3).scan(k)
+
+
+# scans of the config-4 trajectory checked (bench.py's 30 by default;
+# DBT_FULL_SCANS=200 runs the whole BASELINE trajectory, ~6 min)
+N4 = int(os.environ.get("DBT_FULL_SCANS", "30"))
+
+
 def test_config4_full_grid_matches_oracle_by_slabs():
     import torch
 
@@ -52,13 +61,13 @@ def test_config4_full_grid_matches_oracle_by_slabs():
     from concurrent.futures import ProcessPoolExecutor
 
     with ProcessPoolExecutor(max_workers=min(30, os.cpu_count() or 1)) as ex:
-        pts_all = list(ex.map(_scan4, range(30)))
+        pts_all = list(ex.map(_scan4, range(N4)))
     scans = [(p, w.poses[k]) for k, p in enumerate(pts_all)]
     applied = 0
     for pts, pose in scans:
         st = integrate_frame(g, bank, ScanFrame(points=pts, pose=pose), IntegrationParams())
         applied += st.points_in - st.points_discarded
-    assert applied > 3_000_000
+    assert applied > 100_000 * N4
     ob = oracle.OracleBank.from_bank(bank)
     threads = oracle.os_threads()
     for s in range(n_slabs):
@@ -71,3 +80,28 @@ def test_config4_full_grid_matches_oracle_by_slabs():
         assert np.array_equal(sg, og.sign), f"sign differs in slab [{x0}, {x1})"
         assert np.array_equal(h, og.hits), f"hits differ in slab [{x0}, {x1})"
         del og, m, sg, h
+
+
+@pytest.mark.skipif(os.environ.get("DBT_LONG") != "1", reason="long run (DBT_LONG=1): config 3's whole trajectory")
+def test_config3_whole_trajectory_matches_oracle():
+    """All 500 scans of config 3 (BASELINE configs[2]) into the 2000 x 2000 x
+    100 grid, one synchronous integrate_frame each, against the oracle over
+    the same 500 scans (the reference itself is pinned over scans 0-127,
+    tests/test_trajectories.py)."""
+    w = workloads.get(3)
+    n = int(os.environ.get("DBT_CFG3_SCANS", str(len(w.poses))))
+    from concurrent.futures import ProcessPoolExecutor
+
+    with ProcessPoolExecutor(max_workers=min(30, os.cpu_count() or 1)) as ex:
+        pts_all = list(ex.map(_scan3, range(n)))
+    bank = build_kernel_bank(shadow_radius=w.shadow_radius)
+    g = new_grid(w.dims, w.voxel_size, w.origin, memory_cap=1 << 42)
+    og = oracle.OracleGrid(w.dims, w.voxel_size, w.origin)
+    ob = oracle.OracleBank.from_bank(bank)
+    threads = oracle.os_threads()
+    for k, pts in enumerate(pts_all):
+        st = integrate_frame(g, bank, ScanFrame(points=pts, pose=w.poses[k]), IntegrationParams())
+        ost = oracle.integrate_frame(og, ob, pts, w.poses[k], threads=threads)
+        assert (st.points_in, st.points_discarded) == (ost.points_in, ost.points_discarded), k
+    m, sg, h = g.download_range(0, w.dims[0])
+    assert np.array_equal(m, og.mask) and np.array_equal(sg, og.sign) and np.array_equal(h, og.hits)
