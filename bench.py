@@ -15,7 +15,10 @@ batch the grid is reset and refilled (untimed, between the step events), so
 every pass over the window times the same grid states. Warm-up steps run the
 same window, then the grid is reset and refilled before the timed region.
 Config 1 has one scan: every step integrates it into a fresh grid. L2 is
-flushed (256 MB write) before every step; the config-4 grid is 58 GB anyway.
+flushed before every step (the config-4 grid is 58 GB anyway): a 256 MB
+write, then a 256 MB read of a second buffer, so the flush's own dirty lines
+are written back before the step events rather than by the step's kernels
+(`--flush write` keeps the write-only flush).
 
   value : applied returns / device seconds, scans resident in HBM, CUDA
           events on the launch stream around each step (launch sequence incl.
@@ -285,7 +288,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": config_desc(w, B),
+        "config": config_desc(w, B, l2=L2_CLEAN),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{args.steps} timed window steps of config {args.config} (at most "
                                    f"{CPU_SCANS_PER_STEP} scans of each step's batch; {note}), oracle C port of the "
@@ -295,7 +298,31 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(w, batch, interleave=0, multi="single"):
+L2_CLEAN = ("flushed before every step: 256 MB write, then a 256 MB read of another buffer (write-back of the "
+            "flush's dirty lines outside the step)")
+
+
+class L2Flush:
+    """Evict L2 before a timed step: write a 256 MB buffer (> the 126 MB L2);
+    mode "clean" then reads a second 256 MB buffer, so the dirty lines the
+    write left are written back here, not by the next step's kernels."""
+
+    def __init__(self, dev, mode):
+        import torch
+        self.mode = mode
+        self.w = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+        self.r = torch.zeros(64 << 20, dtype=torch.float32, device=dev) if mode == "clean" else None
+
+    def __call__(self):
+        self.w.zero_()
+        if self.r is not None:
+            self.r.max()
+
+    def desc(self):
+        return L2_CLEAN if self.mode == "clean" else "flushed before every step (256 MB write)"
+
+
+def config_desc(w, batch, interleave=0, multi="single", l2="flushed before every step (256 MB write)"):
     scene = "synthetic room" if w.config <= 2 else "synthetic street (ground, 40 buildings, 200 poles)"
     par = {"single": "single GPU",
            "replica": "data-parallel whole-grid replicas: each rank integrates a contiguous segment of the window, "
@@ -308,7 +335,7 @@ def config_desc(w, batch, interleave=0, multi="single"):
                         + (" (literal room grid padded by 11)" if w.config <= 2 else ""),
             "kernel": f"{K_EDGE}^3", "bins": "40x40", "shadow_radius": w.shadow_radius, "t_occ": 2, "h_max": 255,
             "scans_per_step": batch, "window": window_desc(w, batch),
-            "l2": "flushed before every step (256 MB write)", "parallelism": par}
+            "l2": l2, "parallelism": par}
 
 
 def relaunch(n: int) -> int:
@@ -344,6 +371,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="diagnostics only: skip the end-to-end passes")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
+    ap.add_argument("--flush", default="clean", choices=["clean", "write"],
+                    help="L2 flush before a step: write a 256 MB buffer, then (clean) read another 256 MB buffer so "
+                         "the flush's dirty lines are written back before the step instead of inside it")
     ap.add_argument("--diag-order", default=None, choices=["morton", "xyz", "random"],
                     help="diagnostics only: reorder each scan's points (spatial locality of the sweep work list)")
     ap.add_argument("--interleave", type=int, default=None,
@@ -440,7 +470,7 @@ def main():
         i = s % P
         return seg[0] + i if seg[0] + i < seg[1] else None
 
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > L2
+    flush = L2Flush(dev, args.flush)
     stream = torch.cuda.Stream(device=local)  # every timed op (flush, broadcast, engine) on this stream
     torch.cuda.set_stream(stream)
 
@@ -519,7 +549,7 @@ def main():
                     timed_merge()
                 refill()  # untimed: between the step events
             if not args.no_flush:
-                flush.zero_()
+                flush()
             j = batch_of(i)
             ev[i][0].record(stream)
             if j is not None:
@@ -583,11 +613,11 @@ def main():
     applied_per_launch = local_applied / steps_with_work
     tr = kernel_traffic(args.config, B) if world == 1 else None
     dram = (tr or {}).get("kernels", {}).get(dom, {}).get("dram_bytes")
-    # bytes the sweep touches (live device counters): one 32-byte sector of
-    # the 1-byte distance cache per kernel row it read after culling (a row's
-    # 1-4 chunks span 1-2 sectors) + the 8-byte record sector share and the
-    # cache byte of every lowered voxel
-    touched = ((rows * 32 if rows else swept * K_EDGE ** 3) + written * 5) / steps_with_work
+    # bytes the sweep touches (live device counters): two 32-byte sectors of
+    # the 16-bit length cache per kernel row it read after culling (a row's
+    # 1-4 16-byte chunks span 1-2 sectors); the MIN reductions of lowered
+    # chunks hit the same sectors
+    touched = (rows * 64 if rows else swept * K_EDGE ** 3 * 2) / steps_with_work
     alg = b_alg(shadow_cells) * applied_per_launch / (1 if replica else max(world, 1))
     if dram is not None:
         achieved, basis = dram / (kd["avg_us"] * 1e-6) / 1e9, (
@@ -602,7 +632,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if replica else ("strong" if world > 1 else "weak"), "vs_baseline": None,
         "dtype": "u32/f64", "data": "synthetic (seeded ray-cast scenes with the BASELINE configs' shapes)",
-        "config": config_desc(w, B, ilv, multi),
+        "config": config_desc(w, B, ilv, multi, l2="not flushed (diagnostic)" if args.no_flush else flush.desc()),
         "gpu_launches": int(launches),
         "kernels": kernels,
         "profiled_step_ms": prof_ms / args.steps,
@@ -626,7 +656,7 @@ def main():
                         "def": "SURVEY.md 8(d) 4*21^3 + 4*|S| B per applied return (the reference's per-return "
                                "traffic) x applied returns / sweep time; above the HBM peak by design: the engine "
                                "sweeps each centre once, skips centres whose stamp is applied (certificates), culls "
-                               "voxels a closer certified centre covers and reads a 1-byte cache"},
+                               "voxels a closer certified centre covers and lowers a 16-bit length cache instead of the 4-byte masks"},
     }
 
     # ---------------- e2e through the public API ----------------------------
@@ -713,7 +743,7 @@ def run_e2e(args, w, B, pre, win, scans, sg, bank, params, dist, rank, world, re
                 refill(src)
             j = batch_of(i)
             if not args.no_flush:
-                flush.zero_()
+                flush()
             torch.cuda.synchronize()
             if j is None:
                 continue

@@ -6,9 +6,8 @@
 // pending shadow visits (bytes 2-3, 0 in every record that leaves the
 // device). The two words are the single aligned words the two update kinds
 // touch:
-//   * mask update (integrator.py:145-149): one native atomicAnd (RED.AND) of
-//     the kernel's run mask into .x — AND is commutative and idempotent, so
-//     no CAS and no retries;
+//   * mask update (integrator.py:145-149): a MIN on the voxel's length cache
+//     word (below); the mask word itself is folded lazily;
 //   * shadow update (integrator.py:151-159): one atomicAdd of 1 << 16 on .y
 //     counts the visit. n visits of the step h += (h < h_max), sign = 0 when
 //     h >= T, compose to h' = h >= h_max ? h : min(h + n, h_max) and sign = 0
@@ -18,15 +17,18 @@
 // Any mask and sign byte the reference can hold is represented (no run-mask
 // assumption).
 //
-// Distance cache: one byte per voxel, dist[v] >= bitlen(mask[v]) at all times
-// (equal after upload/reset), where bitlen = 32 - clz (the popcount for the
-// low-bit run masks integration produces). ANDing run_mask(d) changes a mask
-// exactly when d < bitlen(mask), so the sweep reads the cache (8 voxels per
-// 64-bit load) to find the voxels a return lowers, applies RED.AND to their
-// records and stores d into the cache. Cache stores race only with other
-// lowering stores, so a cache byte can end up stale-high (a later redundant
-// AND) but never below the record: no update is ever lost.
-//
+// Length cache: one 16-bit word per voxel, the run length the voxel's mask
+// is lowered to: the effective mask of voxel v is m[v] & run_mask(len[v]).
+// The sweep never touches the mask words: a return lowers voxel v exactly
+// when its kernel run length d < len[v] (for the run masks integration
+// produces, len = bit length of the effective mask), and the lowering is one
+// hardware MIN on the cache — REDG.MIN.F16x8 over 8 voxels, the lengths kept
+// as raw 16-bit integers 0..64, which are (subnormal) f16 values ordered like
+// the integers under .noftz. MIN is commutative and idempotent, so the cache
+// is exact: AND-ing run masks composes as m & run(d1) & run(d2) =
+// m & run(min(d1, d2)). The masks are folded lazily (m &= run_mask(len),
+// fold_pending) before any read of the records, like the pending shadow
+// visits below; uploads and resets set len = bit length of the mask.
 // Stamp certificates: one bit per voxel, set when the full K^3 stamp centred
 // at that voxel (on a sharded grid: the part of it on this part's planes) is
 // in the grid or claimed by a return of the running launch;
@@ -216,7 +218,8 @@ struct dbt_grid {
   int64_t lx = 0;                           // owned plane count (storage x extent)
   double vs = 0, org[3] = {0, 0, 0};
   dbt::Cells cells;                         // authoritative voxel records (masks | meta words)
-  uint8_t* dist = nullptr;                  // distance cache, dist[v] >= len(cells[v])
+  uint16_t* dist = nullptr;                 // length cache: effective mask = cells.m[v] & run_mask(dist[v])
+  bool lazy_m = false;                      // masks not yet folded with the length cache (fold_pending)
   uint32_t* stamped = nullptr;              // stamp certificates, one bit per voxel of the GLOBAL grid
                                             // (index (x*ny + y)*nzp + z, x global): a part of a sharded
                                             // grid certifies every centre whose cube touches its planes

@@ -27,7 +27,8 @@ using namespace dbt;
 namespace {
 
 struct ExactArgs {
-  const uint32_t* cm;     // masks (Cells::m)
+  const uint32_t* cm;     // masks (Cells::m), lazily lowered:
+  const uint16_t* lc;     // effective mask = cm[v] & run_mask(lc[v]) (engine.cuh length cache)
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
   unsigned long long* out;
@@ -84,7 +85,7 @@ __global__ void exact_snap_kernel(ExactArgs a) {
        w += (int64_t)gridDim.x * blockDim.x) {
     for (uint32_t bits = a.tbits[w]; bits; bits &= bits - 1) {
       const int64_t v = w * 32 + (__ffs(bits) - 1);
-      a.m0[v] = a.cm[v];
+      a.m0[v] = a.cm[v] & run_mask(a.lc[v]);
     }
   }
 }
@@ -128,7 +129,7 @@ __global__ void exact_count_kernel(ExactArgs a) {
       const uint32_t bits = __shfl_sync(0xffffffffu, word, src);
       if (!((bits >> lane) & 1u)) continue;
       const int64_t v = (w0 + src) * 32 + lane;
-      const uint32_t fin = a.cm[v];
+      const uint32_t fin = a.cm[v] & run_mask(a.lc[v]);
       uint32_t m = a.m0[v];
       if (m == fin) continue;  // not changed by this launch
       const int64_t row = v / a.nzp, z = v - row * a.nzp;
@@ -177,6 +178,7 @@ __global__ void exact_count_kernel(ExactArgs a) {
 ExactArgs exact_args(dbt_grid* g, const dbt_bank* b, int64_t n_words) {
   ExactArgs a;
   a.cm = g->cells.m;
+  a.lc = g->dist;
   a.uniq = g->d_uniq;
   a.lc_in = g->d_lcnt;
   a.out = &g->d_lcnt->exact_written;

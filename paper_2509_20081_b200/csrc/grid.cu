@@ -31,18 +31,21 @@ namespace {
 
 constexpr int64_t kStageBytes = 256ll << 20;
 
-__global__ void fill_cells_kernel(Cells cells, int64_t n) {
-  // n is a multiple of 4 (allocation is padded); 128-bit stores of four
-  // fresh masks and four fresh meta words
+__global__ void fill_cells_kernel(Cells cells, uint16_t* __restrict__ dist, int64_t n) {
+  // n is a multiple of 8 (allocation is padded); 128-bit stores of four
+  // fresh masks and four fresh meta words, and of eight fresh cache lengths
   const uint4 vm = make_uint4(kFullMask, kFullMask, kFullMask, kFullMask);
   const uint4 vy = make_uint4(kFreshMeta, kFreshMeta, kFreshMeta, kFreshMeta);
+  const uint4 vd = make_uint4(0x00200020u, 0x00200020u, 0x00200020u, 0x00200020u);
   uint4* pm = reinterpret_cast<uint4*>(cells.m);
   uint4* py = reinterpret_cast<uint4*>(cells.y);
+  uint4* pd = reinterpret_cast<uint4*>(dist);
   int64_t n4 = n / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     pm[i] = vm;
     py[i] = vy;
+    if (!(i & 1)) pd[i >> 1] = vd;
   }
 }
 
@@ -59,29 +62,37 @@ __global__ void encode_kernel(Cells cells, const uint32_t* __restrict__ mask,
 }
 
 // dist[v] = bit length of the mask of cells[v] over the whole slab (after host writes)
-__global__ void rebuild_dist_kernel(const uint32_t* __restrict__ cm, uint8_t* __restrict__ dist, int64_t n) {
+__global__ void rebuild_dist_kernel(const uint32_t* __restrict__ cm, uint16_t* __restrict__ dist, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    dist[i] = (uint8_t)mask_bitlen(cm[i]);
+    dist[i] = (uint16_t)mask_bitlen(cm[i]);
 }
 
-// pending shadow visits -> final sign/hits (no concurrent writers)
-__global__ void fold_kernel(uint32_t* __restrict__ cy, int64_t n, uint32_t h_max, uint32_t t_occ) {
+// pending shadow visits -> final sign/hits (pend), lazily lowered masks ->
+// final masks (lazy: m &= run_mask(len)); no concurrent writers
+__global__ void fold_kernel(Cells cells, const uint16_t* __restrict__ dist, int64_t n, int pend, int lazy,
+                            uint32_t h_max, uint32_t t_occ) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t y = cy[i];
-    if (y >> kPendShift) cy[i] = fold_meta(y, h_max, t_occ);
+    if (pend) {
+      const uint32_t y = cells.y[i];
+      if (y >> kPendShift) cells.y[i] = fold_meta(y, h_max, t_occ);
+    }
+    if (lazy) {
+      const uint32_t m = cells.m[i], f = m & run_mask_of(dist[i]);
+      if (f != m) cells.m[i] = f;
+    }
   }
 }
 
 // distance cache of the z-range [z0, z1) only (chunked record loads)
-__global__ void rebuild_dist_range_kernel(const uint32_t* __restrict__ cm, uint8_t* __restrict__ dist, int64_t rows,
+__global__ void rebuild_dist_range_kernel(const uint32_t* __restrict__ cm, uint16_t* __restrict__ dist, int64_t rows,
                                           int64_t nzp, int64_t z0, int64_t z1) {
   const int64_t zc = z1 - z0, n = rows * zc;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / zc, off = row * nzp + z0 + (i - row * zc);
-    dist[off] = (uint8_t)mask_bitlen(cm[off]);
+    dist[off] = (uint16_t)mask_bitlen(cm[off]);
   }
 }
 
@@ -222,11 +233,13 @@ int dbt::fold_pending(dbt_grid* g, cudaStream_t st) {
     DBT_CUDA(cudaDeviceSynchronize());
     g->last_st = st;
   }
-  if (!g->pend) return DBT_OK;
-  fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells.y, g->n_cells, (uint32_t)g->pend_h_max,
+  if (!g->pend && !g->lazy_m) return DBT_OK;
+  fold_kernel<<<grid_blocks(g->n_cells), 256, 0, st>>>(g->cells, g->dist, g->n_cells, g->pend ? 1 : 0,
+                                                      g->lazy_m ? 1 : 0, (uint32_t)g->pend_h_max,
                                                       (uint32_t)g->pend_t_occ);
   DBT_CHECK_LAUNCH("fold_kernel");
   g->pend = false;
+  g->lazy_m = false;
   return DBT_OK;
 }
 
@@ -236,6 +249,7 @@ namespace {
 // every stamp certificate (host writes carry no stamp history)
 int finish_host_write(dbt_grid* g) {
   g->base_valid = false;  // replica base: host data replaced the records
+  g->lazy_m = false;      // every mask replaced; the cache is rebuilt from them
   rebuild_dist_kernel<<<grid_blocks(g->n_cells), 256, 0, g->stream>>>(g->cells.m, g->dist, g->n_cells);
   DBT_CHECK_LAUNCH("rebuild_dist_kernel");
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
@@ -288,7 +302,7 @@ static int create_grid(const int64_t dims[3], double voxel_size, const double or
   uint32_t* base = nullptr;
   cudaError_t e = cudaMalloc(&base, (size_t)(g->n_cells + 64) * 2 * sizeof(uint32_t));
   if (e == cudaSuccess) g->cells = Cells{base, base + (g->n_cells + 64)};
-  if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64));
+  if (e == cudaSuccess) e = cudaMalloc(&g->dist, (size_t)(g->n_cells + 64) * sizeof(uint16_t));
   if (e == cudaSuccess) e = cudaMalloc(&g->stamped, (size_t)((g->n_cert + 63) / 32) * 4);
   if (e != cudaSuccess) {
     if (g->cells.m) cudaFree(g->cells.m);
@@ -408,10 +422,10 @@ int dbt_grid_reset(dbt_grid* g) {
     DBT_CUDA(cudaDeviceSynchronize());
     g->last_st = g->stream;
   }
-  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->n_cells + 64);
+  fill_cells_kernel<<<grid_blocks((g->n_cells + 64) / 4), 256, 0, g->stream>>>(g->cells, g->dist, g->n_cells + 64);
   g->pend = false;
+  g->lazy_m = false;
   DBT_CHECK_LAUNCH("fill_cells_kernel");
-  DBT_CUDA(cudaMemsetAsync(g->dist, 32, (size_t)(g->n_cells + 64), g->stream));
   DBT_CUDA(cudaMemsetAsync(g->stamped, 0, (size_t)((g->n_cert + 63) / 32) * 4, g->stream));
   DBT_CUDA(cudaStreamSynchronize(g->stream));
   g->cert_dk = 0;
@@ -426,7 +440,7 @@ int dbt_grid_info(const dbt_grid* g, int64_t dims[3], int64_t slab[2], int64_t* 
   dims[2] = g->nz;
   slab[0] = g->x0;
   slab[1] = g->x1;
-  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint2) + 1) + (g->n_cert + 63) / 32 * 4;
+  *device_bytes = (g->n_cells + 64) * (int64_t)(sizeof(uint2) + sizeof(uint16_t)) + (g->n_cert + 63) / 32 * 4;
   return DBT_OK;
 }
 

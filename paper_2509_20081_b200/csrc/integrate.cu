@@ -544,9 +544,32 @@ __global__ void __launch_bounds__(256) shadow_bin_kernel(ShadowArgs a) {
   }
 }
 
+// Length-cache lowering of one 8-voxel chunk of a kernel row (engine.cuh):
+// w = the 8 cached lengths (16-bit lanes), d8 = the row's 8 run lengths + 1
+// (bytes, 64 outside the kernel). Per 16-bit lane (L | 0x8000) - (d + 1)
+// never borrows across lanes (L <= 32, d + 1 <= 64) and its bit 15 is set
+// exactly when d < L: the return lowers that voxel. A chunk with a lowered
+// voxel takes ONE REDG.MIN.F16x8 of its 8 run lengths (a lane that does not
+// lower holds d >= L, a no-op under MIN); returns the lowered voxels.
+__device__ __forceinline__ void red_min_len8(uint16_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.min.noftz.v4.f16x2 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
+}
+__device__ __forceinline__ unsigned lower_chunk(uint16_t* p, uint4 w, uint2 d8) {
+  constexpr uint32_t H = 0x80008000u, O = 0x00010001u;
+  // the table bytes as 16-bit lanes: d + 1
+  const uint32_t t0 = __byte_perm(d8.x, 0u, 0x7170), t1 = __byte_perm(d8.x, 0u, 0x7372);
+  const uint32_t t2 = __byte_perm(d8.y, 0u, 0x7170), t3 = __byte_perm(d8.y, 0u, 0x7372);
+  const uint32_t l0 = ((w.x | H) - t0) & H, l1 = ((w.y | H) - t1) & H;
+  const uint32_t l2 = ((w.z | H) - t2) & H, l3 = ((w.w | H) - t3) & H;
+  const uint32_t lt = l0 | (l1 >> 1) | (l2 >> 2) | (l3 >> 3);
+  if (!lt) return 0u;
+  red_min_len8(p, t0 - O, t1 - O, t2 - O, t3 - O);
+  return (unsigned)__popc(lt);
+}
+
 struct SweepArgs {
   Cells cells;
-  uint8_t* dist;
+  uint16_t* dist;
   const uint64_t* uniq;
   const LaunchCounters* lc_in;
   unsigned long long* changed_out;
@@ -611,7 +634,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
     const int jhi = (int)((dxhi + a.R + 1) * a.K * nch);
     const uint2* dt = dtab + sh * a.nd * CH;
     for (int j0 = jlo + lane; j0 < jhi; j0 += 32 * kSweepUnroll) {
-      uint2 w[kSweepUnroll], d8[kSweepUnroll];
+      uint4 w[kSweepUnroll];
+      uint2 d8[kSweepUnroll];
       int64_t off[kSweepUnroll];
 #pragma unroll
       for (int k = 0; k < kSweepUnroll; ++k) {
@@ -630,30 +654,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
           off[k] = v ? lgx * sx + (ri.x - dx * sx) + base0 + 8 * ch : 0;
         }
         d8[k] = v ? dt[ri.y + ch] : make_uint2(0x40404040u, 0x40404040u);
-        w[k] = *reinterpret_cast<const uint2*>(a.dist + off[k]);
+        w[k] = *reinterpret_cast<const uint4*>(a.dist + off[k]);
       }
 #pragma unroll
-      for (int k = 0; k < kSweepUnroll; ++k) {
-        // per byte: cached distance L <= 32, table holds d + 1 <= 64, so
-        // (L | 0x80) - (d + 1) never borrows across bytes and its bit 7 is
-        // set exactly when d < L (the return lowers this voxel)
-        const uint32_t lt0 = ((w[k].x | 0x80808080u) - d8[k].x) & 0x80808080u;
-        const uint32_t lt1 = ((w[k].y | 0x80808080u) - d8[k].y) & 0x80808080u;
-        if (lt0 | lt1) {
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            const uint32_t lt = b < 4 ? lt0 : lt1;
-            if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
-            const uint32_t d = (((b < 4 ? d8[k].x : d8[k].y) >> (8 * (b & 3))) & 0xFF) - 1u;
-            atomicAnd(&a.cells.m[off[k] + b], run_mask_of((int)d));  // RED.AND, fire and forget
-            ++changed;
-          }
-          // the chunk's cache word in one store (see sweep_cull_kernel)
-          const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
-          *reinterpret_cast<uint2*>(a.dist + off[k]) = make_uint2((w[k].x & ~bm0) | ((d8[k].x - 0x01010101u) & bm0),
-                                                                (w[k].y & ~bm1) | ((d8[k].y - 0x01010101u) & bm1));
-        }
-      }
+      for (int k = 0; k < kSweepUnroll; ++k) changed += lower_chunk(a.dist + off[k], w[k], d8[k]);
     }
   }
   for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o);
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(SweepArgs a) {
 // over the block instead of serialising one warp.
 struct CullArgs {
   Cells cells;
-  uint8_t* dist;
+  uint16_t* dist;
   const uint64_t* uniq;
   LaunchCounters* lc;
   const uint2* dtab;     // [8][nd][CH]
@@ -720,23 +724,17 @@ __device__ __forceinline__ uint32_t ld_cert(const uint32_t* p) {
   return __ldcg(p);
 #endif
 }
-__device__ __forceinline__ uint2 ld_dist(const uint8_t* p) {
+__device__ __forceinline__ uint4 ld_dist(const uint16_t* p) {
 #ifndef DBT_NO_HINT_DIST_EL
-  uint2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_policy_last()));
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(l2_policy_last()));
   return v;
 #else
-  return *reinterpret_cast<const uint2*>(p);
+  return *reinterpret_cast<const uint4*>(p);
 #endif
 }
-__device__ __forceinline__ void red_and64(uint32_t* p, unsigned long long v) {
-#ifdef DBT_HINT_RED_EF
-  asm volatile("red.global.and.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(l2_policy_first()) : "memory");
-#else
-  atomicAnd(reinterpret_cast<unsigned long long*>(p), v);
-#endif
-}
-
 constexpr int kFar = 1 << 20;
 // phase A row emission: balanced over the warp's lanes when
 // ceil(rows / 32) * NUM < max rows per column * DEN (A/B knobs)
@@ -1025,13 +1023,12 @@ __device__ __forceinline__ RowTask decode_task64(uint64_t task) {
 }
 
 // Phase B of the culling sweep: one thread, two row tasks (c1 = -1: none)
-// with their chunk loads in flight together; a cached byte above the row's
-// run length marks a voxel this centre lowers: RED.AND into the record, and
-// the chunk's cache word written back once.
+// with their chunk loads in flight together; a cached length above the row's
+// run length marks a voxel this centre lowers: one MIN reduction per lowered
+// chunk on the length cache (lower_chunk).
 __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const RowTask rows[2], unsigned long long& changed,
                                             unsigned long long& rows_done) {
-  const uint2* dtab = a.dtab;
-  uint2 w[2][4], d8[2][4];
+  uint4 w[2][4];
   int64_t rb[2];
   int cb[2];
 #pragma unroll
@@ -1040,68 +1037,24 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const RowTask row
     rb[r] = rows[r].rb;
     const int c0 = rows[r].c0, c1 = rows[r].c1;
     cb[r] = c0;
-    const uint2* drow = dtab + rows[r].drow;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const bool act = c0 + j <= c1;
-      d8[r][j] = act ? __ldg(drow + c0 + j) : make_uint2(0x40404040u, 0x40404040u);
       // inactive chunks read one shared dummy sector
-      w[r][j] = ld_dist(act ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
+      w[r][j] = ld_dist(c0 + j <= c1 ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
     }
   }
+  // the d-table (L1-resident) is read after the cache loads are in flight
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+  for (int r = 0; r < 2; ++r) {
+    const uint2* drow = a.dtab + rows[r].drow + cb[r];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t lt0 = ((w[r][j].x | 0x80808080u) - d8[r][j].x) & 0x80808080u;
-      const uint32_t lt1 = ((w[r][j].y | 0x80808080u) - d8[r][j].y) & 0x80808080u;
-      if (lt0 | lt1) {
-        const int64_t off = rb[r] + 8 * (cb[r] + j);
-#if defined(DBT_RED_SINGLE)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const uint32_t lt = b < 4 ? lt0 : lt1;
-          if (!((lt >> (8 * (b & 3))) & 0x80u)) continue;
-          const uint32_t d = (((b < 4 ? d8[r][j].x : d8[r][j].y) >> (8 * (b & 3))) & 0xFF) - 1u;
+      if (cb[r] + j > rows[r].c1) continue;
 #if !defined(DBT_DIAG_NO_RED)
-          atomicAnd(&a.cells.m[off + b], run_mask_of((int)d));
+      changed += lower_chunk(a.dist + rb[r] + 8 * (cb[r] + j), w[r][j], __ldg(drow + j));
 #endif
-          ++changed;
-        }
-#else
-        // adjacent voxels (2p, 2p+1) of the chunk in one 64-bit RED.AND (the
-        // row start is a multiple of 8 voxels, so the pair is 8-byte
-        // aligned); a voxel of the pair that is not lowered ANDs all ones.
-        // Half the RED instructions and L2 sector operations of one RED per
-        // voxel on dense (fresh) rows.
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const uint32_t lt = p < 2 ? lt0 : lt1, dw = p < 2 ? d8[r][j].x : d8[r][j].y;
-          const int s0 = 16 * (p & 1);  // byte 2p (mod 4) of the word
-          const bool l0 = (lt >> (s0 + 7)) & 1u, l1 = (lt >> (s0 + 15)) & 1u;
-          if (!(l0 | l1)) continue;
-          // run_mask(d) = all ones >> (32 - d), d = table byte - 1 (clamped
-          // funnel shift: d = 0 gives 0); shift 0 (all ones) when not lowered
-          const uint32_t lo = __funnelshift_rc(kFullMask, 0u, l0 ? 33u - ((dw >> s0) & 0xFFu) : 0u);
-          const uint32_t hi = __funnelshift_rc(kFullMask, 0u, l1 ? 33u - ((dw >> (s0 + 8)) & 0xFFu) : 0u);
-#if !defined(DBT_DIAG_NO_RED)
-          red_and64(a.cells.m + off + 2 * p, ((unsigned long long)hi << 32) | lo);
-#endif
-          changed += (unsigned)l0 + (unsigned)l1;
-        }
-#endif
-        // the chunk's cache word in one store: lowered bytes take d (the
-        // table byte - 1, never borrows), the others the value read above.
-        // A concurrent lowering overwritten here only leaves its byte
-        // stale-high (>= the record's bit length): a redundant AND later.
-        const uint32_t bm0 = (lt0 >> 7) * 0xFFu, bm1 = (lt1 >> 7) * 0xFFu;
-#ifndef DBT_DIAG_NO_CACHE_STORE
-        *reinterpret_cast<uint2*>(a.dist + off) =
-            make_uint2((w[r][j].x & ~bm0) | ((d8[r][j].x - 0x01010101u) & bm0),
-                       (w[r][j].y & ~bm1) | ((d8[r][j].y - 0x01010101u) & bm1));
-#endif
-      }
     }
+  }
 }
 
 // 32 resident warps per SM (64 registers, a few bytes spilled): same-box A/B
@@ -1523,6 +1476,7 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
     g->pend_h_max = p->h_max;
     g->pend_t_occ = p->t_occ;
   }
+  g->lazy_m = true;  // the sweep lowers the length cache; masks folded before reads
   const int64_t hcap = [&] {
     int64_t w = 1024;
     while (w < 2 * n) w <<= 1;

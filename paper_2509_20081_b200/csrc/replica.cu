@@ -60,7 +60,7 @@ __global__ void replica_pack_kernel(const Cells cells, const uint8_t* __restrict
   }
 }
 
-__global__ void replica_apply_kernel(Cells cells, uint8_t* __restrict__ dist,
+__global__ void replica_apply_kernel(Cells cells, uint16_t* __restrict__ dist,
                                      uint32_t* __restrict__ bmask, uint8_t* __restrict__ bhits,
                                      const uint8_t* __restrict__ mlen, const uint8_t* __restrict__ sign,
                                      const __half* __restrict__ delta, int64_t n, int64_t nz, int64_t nzp, int h_max,
@@ -74,7 +74,7 @@ __global__ void replica_apply_kernel(Cells cells, uint8_t* __restrict__ dist,
     const int h = h0 >= h_max ? h0 : min(h0 + d, h_max);
     const uint32_t s = (d > 0 && h >= t_occ) ? 0u : (uint32_t)sign[i];
     cells.put(v, make_uint2(m, make_meta(s, (uint32_t)h)));
-    dist[v] = (uint8_t)mask_bitlen(m);
+    dist[v] = (uint16_t)mask_bitlen(m);
     bmask[v] = m;
     bhits[v] = (uint8_t)h;
   }
@@ -123,8 +123,10 @@ struct BrickMap {
 
 // packed buffers of the selected bricks: mls = [n_sel * 4096 mask bit
 // lengths | n_sel * 4096 signs], delta = n_sel * 4096 hit deltas; pending
-// shadow visits are folded on the fly (pend: the launch parameters)
-__global__ void replica_pack_bricks_kernel(const Cells cells, const uint8_t* __restrict__ bhits,
+// shadow visits and lazily lowered masks are folded on the fly (pend: the
+// launch parameters)
+__global__ void replica_pack_bricks_kernel(const Cells cells, const uint16_t* __restrict__ dist,
+                                           const uint8_t* __restrict__ bhits,
                                            const int32_t* __restrict__ sel, int64_t n_sel, BrickMap bm, int pend,
                                            uint32_t ph, uint32_t pt, uint8_t* __restrict__ mls,
                                            __half* __restrict__ delta) {
@@ -134,7 +136,7 @@ __global__ void replica_pack_bricks_kernel(const Cells cells, const uint8_t* __r
     uint8_t ml = 0, sg = 0;
     int d = 0;
     if (bm.voxel(sel[i >> (3 * kBrickShift)], (int)(i & (kBrickCells - 1)), v)) {
-      const uint32_t m = cells.m[v];
+      const uint32_t m = cells.m[v] & run_mask_of(dist[v]);  // the effective (lazily lowered) mask
       const uint32_t y = pend ? fold_meta(cells.y[v], ph, pt) : cells.y[v];
       ml = (uint8_t)mask_bitlen(m);
       sg = meta_sign(y);
@@ -146,7 +148,7 @@ __global__ void replica_pack_bricks_kernel(const Cells cells, const uint8_t* __r
   }
 }
 
-__global__ void replica_apply_bricks_kernel(Cells cells, uint8_t* __restrict__ dist, uint32_t* __restrict__ bmask,
+__global__ void replica_apply_bricks_kernel(Cells cells, uint16_t* __restrict__ dist, uint32_t* __restrict__ bmask,
                                             uint8_t* __restrict__ bhits, const int32_t* __restrict__ sel,
                                             int64_t n_sel, BrickMap bm, const uint8_t* __restrict__ mls,
                                             const __half* __restrict__ delta, int h_max, int t_occ) {
@@ -161,7 +163,7 @@ __global__ void replica_apply_bricks_kernel(Cells cells, uint8_t* __restrict__ d
     const int h = h0 >= h_max ? h0 : min(h0 + d, h_max);
     const uint32_t s = (d > 0 && h >= t_occ) ? 0u : (uint32_t)mls[tot + i];
     cells.put(v, make_uint2(m, make_meta(s, (uint32_t)h)));
-    dist[v] = (uint8_t)mask_bitlen(m);
+    dist[v] = (uint16_t)mask_bitlen(m);
     bmask[v] = m;
     bhits[v] = (uint8_t)h;
   }
@@ -319,7 +321,7 @@ int dbt_replica_pack_bricks(dbt_grid* g, uint8_t* mask_len_sign, uint16_t* delta
   if (!g->n_sel) return DBT_OK;
   const BrickMap bm{g->dby, g->dbz, g->nx, g->ny, g->nz, g->nzp};
   replica_pack_bricks_kernel<<<blocks_for(g->n_sel * kBrickCells), 256, 0, st>>>(
-      g->cells, g->d_base_hits, g->d_sel, g->n_sel, bm, g->pend ? 1 : 0, (uint32_t)g->pend_h_max,
+      g->cells, g->dist, g->d_base_hits, g->d_sel, g->n_sel, bm, g->pend ? 1 : 0, (uint32_t)g->pend_h_max,
       (uint32_t)g->pend_t_occ, mask_len_sign, reinterpret_cast<__half*>(delta_f16));
   DBT_CHECK_LAUNCH("replica_pack_bricks_kernel");
   return DBT_OK;
@@ -343,9 +345,10 @@ int dbt_replica_apply_bricks(dbt_grid* g, const uint8_t* mask_len_sign_min, cons
         reinterpret_cast<const __half*>(delta_sum_f16), h_max, t_occ);
     DBT_CHECK_LAUNCH("replica_apply_bricks_kernel");
   }
-  // every pending visit lay in a selected brick: the records are final and
-  // the base is the merged grid again
+  // every pending visit and every lowering since the mark lay in a selected
+  // brick: the records are final and the base is the merged grid again
   g->pend = false;
+  g->lazy_m = false;
   DBT_CUDA(cudaMemsetAsync(g->d_dirty, 0, (size_t)(g->dbx * g->dby * g->dbz), st));
   g->dirty_reach = 0;
   g->n_sel = 0;

@@ -5,8 +5,8 @@
 C-order field arrays ``mask`` (u32), ``sign`` (u8), ``hits`` (u8) — but the
 authoritative voxel store lives in HBM, owned by libdbtsdf (see
 csrc/engine.cuh): an 8-byte record per voxel (mask | sign, hits, pending
-shadow visits), a 1-byte distance cache and a 1-bit stamp certificate —
-9.125 B/voxel. The numpy field arrays are a host mirror:
+shadow visits), a 16-bit length cache and a 1-bit stamp certificate —
+10.125 B/voxel. The numpy field arrays are a host mirror:
 
 * they are materialised (downloaded) the first time ``mask``/``sign``/``hits``
   is touched;
@@ -185,8 +185,8 @@ def new_grid(dims, voxel_size: float, origin=(0.0, 0.0, 0.0), memory_cap: int = 
 
     ConfigurationError for degenerate dims/voxel_size; ResourceError when the
     reference payload (8 B/voxel) exceeds ``memory_cap`` or the device is out
-    of memory. The device store itself takes 9.125 B/voxel (8-byte record,
-    1-byte distance cache, 1-bit stamp certificate).
+    of memory. The device store itself takes 10.125 B/voxel (8-byte record,
+    16-bit length cache, 1-bit stamp certificate).
     """
     dims = tuple(int(d) for d in dims)
     if len(dims) != 3 or any(d < 1 for d in dims):
