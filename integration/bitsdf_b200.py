@@ -117,7 +117,7 @@ class McTables(ctypes.Structure):  # dbt_mc_tables
 
 
 DBT_F32, DBT_F64 = 0, 1
-FLAG_MAP_FRAME, FLAG_SKIP_NORM_CHECK = 1, 2
+FLAG_MAP_FRAME, FLAG_SKIP_NORM_CHECK, FLAG_EXACT_WRITTEN = 1, 2, 128
 _CODES = {2: "ConfigurationError", 3: "FormatError", 4: "CorruptionError", 5: "EvaluationError",
           6: "ResourceError"}  # cli.py:34-40
 
@@ -221,6 +221,13 @@ def sync_to_host(grid):
     _download(grid)
 
 
+def _exact_flag() -> int:
+    """DBT_FLAG_EXACT_WRITTEN when $DBT_EXACT_VOXELS_WRITTEN=1: FrameStats.
+    voxels_written is then the reference's serial count (integrator.py:
+    268-285) instead of the engine's concurrent change count."""
+    return FLAG_EXACT_WRITTEN if os.environ.get("DBT_EXACT_VOXELS_WRITTEN") == "1" else 0
+
+
 def _params(params, flags=0, downsample=None):
     return Params(int(params.h_max), int(params.t_occ), int(params.downsample if downsample is None else downsample),
                   int(bool(params.first_return_per_voxel)), flags, 0)
@@ -279,7 +286,7 @@ def integrate_frame(grid, bank, scan, params, threads: int = 1):
         ts = None if scan.timestamps is None else np.ascontiguousarray(scan.timestamps, np.float64)
         pose = np.ascontiguousarray(scan.pose, np.float64)
         g = _upload(grid)
-        prm = _params(params)
+        prm = _params(params, flags=_exact_flag())
         st = Stats()
         _check(lib().dbt_integrate_frame_deskew(
             g, device_bank(bank), _ptr(pts), DBT_F64, pts.shape[0], None if ts is None else _ptr(ts),
@@ -306,7 +313,7 @@ def integrate_frame(grid, bank, scan, params, threads: int = 1):
     payload, dtype = (p32, DBT_F32) if exact32 else (pts, DBT_F64)
     pose = np.ascontiguousarray(scan.pose, np.float64)
     g = _upload(grid)
-    prm = _params(params, downsample=downsample)
+    prm = _params(params, flags=_exact_flag(), downsample=downsample)
     st = Stats()
     _check(lib().dbt_integrate_frame(g, device_bank(bank), _ptr(payload), dtype, payload.shape[0],
                                      pose.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(prm),

@@ -710,9 +710,16 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// not volatile: the policy is a constant, so one CREATEPOLICY per thread is
+// hoisted out of the loops (it was 6 % of the sweep's instructions re-created
+// at every load)
 __device__ __forceinline__ uint64_t l2_policy_last() {
   uint64_t p;
+#ifdef DBT_POLICY_VOLATILE
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#else
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
   return p;
 }
 __device__ __forceinline__ uint32_t ld_cert(const uint32_t* p) {
@@ -1039,7 +1046,8 @@ __device__ __forceinline__ void sweep_rows2(const CullArgs& a, const RowTask row
     cb[r] = c0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // inactive chunks read one shared dummy sector
+      // inactive chunks read one shared dummy sector (predicated-off loads
+      // measured 6 % slower on config 4: profiles/README.md, s5)
       w[r][j] = ld_dist(c0 + j <= c1 ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
     }
   }

@@ -107,6 +107,86 @@ print("ok")
     assert out.stdout.strip().endswith("ok"), out.stderr
 
 
+REF_INSTALLED = ROOT / "baseline" / "_ref"  # pip --target install of the reference (git-ignored, travels)
+
+
+def _ref_path():
+    """The reference package on this machine: the build container's source
+    tree, else the installed copy that travels to the GPU box."""
+    if REF_SRC.exists():
+        return REF_SRC
+    return REF_INSTALLED if (REF_INSTALLED / "bitsdf").exists() else None
+
+
+@pytest.mark.skipif(_ref_path() is None, reason="reference package not present")
+def test_plugin_rebinds_reference_names():
+    """integration/pytest_b200.py (the plugin that runs the reference's own
+    suites against the drop-in): after install() every bitsdf module's
+    integrate_frame / integrate_point / extract_mesh is the plugin's, the
+    shim sits at bitsdf._b200, and the CPU originals stay reachable."""
+    code = f"""
+import sys
+sys.path.insert(0, {str(_ref_path())!r}); sys.path.insert(0, {str(ROOT / "integration")!r})
+import os
+os.environ["BITSDF_B200_LIB"] = {str(_native.LIB_PATH)!r}
+import bitsdf.integrator as ri, bitsdf.mesher as rm
+cpu = (ri.integrate_frame, ri.integrate_point, rm.extract_mesh)
+import pytest_b200 as P
+shim = P.install()
+import bitsdf, bitsdf.cli as cli
+assert bitsdf._b200 is shim and sys.modules["bitsdf._b200"] is shim
+for mod in (bitsdf, ri, cli):
+    assert mod.integrate_frame.__module__ == "pytest_b200", mod
+assert ri.integrate_point.__module__ == "pytest_b200"
+assert rm.extract_mesh.__module__ == "pytest_b200" and cli.extract_mesh is rm.extract_mesh
+assert tuple(bitsdf._b200_cpu[k] for k in ("integrate_frame", "integrate_point", "extract_mesh")) == cpu
+assert shim.FrameStats is ri.FrameStats
+print("ok")
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert out.stdout.strip().endswith("ok"), out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not (REF_INSTALLED / "bitsdf").exists(), reason="baseline/_ref (installed reference) not present")
+def test_live_reference_crosscheck(tmp_path):
+    """The reference itself, imported on the GPU box from baseline/_ref, as a
+    live oracle: a short trajectory through the plugin with
+    BITSDF_B200_CROSSCHECK=1 — every integrate_frame / integrate_point /
+    extract_mesh call is repeated by the reference's CPU code on a copy of the
+    grid and compared array for array, FrameStats included (exact
+    voxels_written)."""
+    t = tmp_path / "test_live.py"
+    t.write_text("""
+import numpy as np
+from bitsdf.grid import new_grid
+from bitsdf.integrator import IntegrationParams, ScanFrame, integrate_frame, integrate_point
+from bitsdf.kernels import build_kernel_bank
+from bitsdf.mesher import extract_mesh
+
+def test_trajectory():
+    rng = np.random.default_rng(11)
+    grid = new_grid((72, 64, 56), 0.1)
+    bank = build_kernel_bank(shadow_radius=2)
+    for k, prm in enumerate([IntegrationParams(t_occ=1), IntegrationParams(t_occ=2, first_return_per_voxel=True),
+                             IntegrationParams(t_occ=2, downsample=3), IntegrationParams(t_occ=1)]):
+        pose = np.eye(4); pose[:3, 3] = (3.0 + 0.3 * k, 3.2, 2.8)
+        d = rng.normal(size=(3000, 3)); d /= np.linalg.norm(d, axis=1, keepdims=True)
+        pts = d * rng.uniform(0.05, 4.5, size=(3000, 1))
+        dt = np.float32 if k % 2 else np.float64
+        st = integrate_frame(grid, bank, ScanFrame(points=pts.astype(dt), pose=pose), prm)
+        assert st.points_in > 0
+    assert integrate_point(grid, bank, (2.0, 2.0, 2.0), (3.0, 3.0, 3.0), IntegrationParams(t_occ=1)) == "applied"
+    assert len(extract_mesh(grid).triangles) > 0
+""")
+    env = dict(os.environ, PYTHONPATH=f"{REF_INSTALLED}:{ROOT / 'integration'}", BITSDF_B200_LIB=str(_native.LIB_PATH),
+               BITSDF_B200_CROSSCHECK="1", DBT_EXACT_VOXELS_WRITTEN="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-p", "pytest_b200", "--rootdir", str(tmp_path), "-c",
+                          "/dev/null", "-p", "no:cacheprovider", "-q", str(t)], capture_output=True, text=True, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "crosschecked 6" in out.stdout, out.stdout[-1500:]
+
+
 # ------------------------------------------------------------------ GPU
 def _standin(c):
     """A VoxelGrid-shaped object: what the reference's dataclass holds."""
