@@ -832,6 +832,14 @@ def run_e2e(args, w, B, pre, win, scans, sg, bank, params, dist, rank, world, re
     v2, el2, _ = e2e_pass(scans if (rank == 0 or replica) else {})
     out["e2e_pageable"] = {"value": v2, "unit": UNIT, "ms_per_step": el2 / args.steps * 1e3,
                            "api": api + ", pageable numpy float32 scans (staged by one H2D copy per scan)"}
+    if B == 1 and world == 1:
+        # what a stock fuse loop holds: plain numpy scans, pipelined calls
+        # (cudaMemcpyAsync from pageable memory stages through the driver and
+        # blocks the host for the copy, while the previous scan's kernels run)
+        v3, el3, _ = e2e_async_pass(scans)
+        out["e2e_pageable_async"] = {"value": v3, "unit": UNIT, "ms_per_step": el3 / args.steps * 1e3,
+                                     "api": "paper_2509_20081_b200.integrate_frame_async, pageable numpy float32 "
+                                            "scans, calls pipelined (<= 2 outstanding)"}
     for buf, _ in pinned.values():
         L.dbt_host_free(buf)
     return out

@@ -177,6 +177,8 @@ struct AsyncSlot {
   cudaEvent_t copied = nullptr, done = nullptr;
   void* d_buf = nullptr;
   int64_t cap = 0;
+  void* h_stage = nullptr;      // pinned staging of a pageable scan (hostcopy.cu)
+  int64_t cap_hstage = 0;
   LaunchCounters* h = nullptr;  // LaunchCounters + one ScanCounters, pinned
   int64_t points_in = 0;
   dbt_params p{};
@@ -363,6 +365,7 @@ int prof_flush(dbt_grid* g);
 // pageable scans -> pinned mapped staging with a host thread pool
 // (hostcopy.cu): out[i] = device pointer of scan i; false = not staged
 bool stage_pageable(dbt_grid* g, const void* const* srcs, const int64_t* bytes, int n, const void** out);
+void pooled_host_copy(void* dst, const void* src, size_t bytes);
 
 // scratch management (grid.cu)
 int ensure_stage(dbt_grid* g, int64_t bytes);

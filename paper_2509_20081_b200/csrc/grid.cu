@@ -406,6 +406,7 @@ int dbt_grid_destroy(dbt_grid* g) {
     if (sl.done) cudaEventDestroy(sl.done);
     if (sl.d_buf) cudaFree(sl.d_buf);
     if (sl.h) cudaFreeHost(sl.h);
+    if (sl.h_stage) cudaFreeHost(sl.h_stage);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
   for (auto& e : g->aexec)

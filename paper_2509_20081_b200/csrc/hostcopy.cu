@@ -136,4 +136,11 @@ bool stage_pageable(dbt_grid* g, const void* const* srcs, const int64_t* bytes, 
   return true;
 }
 
+// The same pooled copy into any host buffer (the asynchronous call's per-slot
+// pinned staging).
+void pooled_host_copy(void* dst, const void* src, size_t bytes) {
+  const int parts = (int)std::min<int64_t>(pool().size(), std::max<int64_t>(1, (int64_t)bytes / (128 << 10)));
+  if (bytes) pool().copy((char*)dst, (const char*)src, bytes, parts);
+}
+
 }  // namespace dbt

@@ -1029,37 +1029,37 @@ __device__ __forceinline__ RowTask decode_task64(uint64_t task) {
   return r;
 }
 
-// Phase B of the culling sweep: one thread, NR row tasks (c1 = -1: none)
+// Phase B of the culling sweep: one thread, two row tasks (c1 = -1: none)
 // with their chunk loads in flight together; a cached length above the row's
 // run length marks a voxel this centre lowers: one MIN reduction per lowered
-// chunk on the length cache (lower_chunk). Counters are 32-bit per thread (a
-// thread sees a few thousand rows per launch), widened once at the end.
-template <int NR>
-__device__ __forceinline__ void sweep_rows(const CullArgs& a, const RowTask (&rows)[NR], unsigned& changed,
-                                           unsigned& rows_done) {
-  uint4 w[NR][4];
-  const uint16_t* rp[NR];
+// chunk on the length cache (lower_chunk).
+__device__ __forceinline__ void sweep_rows2(const CullArgs& a, const RowTask rows[2], unsigned long long& changed,
+                                            unsigned long long& rows_done) {
+  uint4 w[2][4];
+  int64_t rb[2];
+  int cb[2];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
+  for (int r = 0; r < 2; ++r) {
+    rows_done += rows[r].c1 >= 0;
+    rb[r] = rows[r].rb;
     const int c0 = rows[r].c0, c1 = rows[r].c1;
-    rows_done += c1 >= 0;
-    // first chunk of the row; an empty task reads the shared dummy sector.
-    // Chunks past the last one re-read the last (an L1 hit, no 64-bit select
-    // per chunk; predicated-off loads measured 6 % slower: profiles/README.md)
-    rp[r] = c1 >= 0 ? a.dist + rows[r].rb + 8 * c0 : a.dist;
-    const int last = max(c1 - c0, 0);
+    cb[r] = c0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) w[r][j] = ld_dist(rp[r] + 8 * min(j, last));
+    for (int j = 0; j < 4; ++j) {
+      // inactive chunks read one shared dummy sector (predicated-off loads
+      // measured 6 % slower on config 4: profiles/README.md, s5)
+      w[r][j] = ld_dist(c0 + j <= c1 ? a.dist + rb[r] + 8 * (c0 + j) : a.dist);
+    }
   }
   // the d-table (L1-resident) is read after the cache loads are in flight
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const uint2* drow = a.dtab + rows[r].drow + rows[r].c0;
+  for (int r = 0; r < 2; ++r) {
+    const uint2* drow = a.dtab + rows[r].drow + cb[r];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (rows[r].c0 + j > rows[r].c1) continue;
+      if (cb[r] + j > rows[r].c1) continue;
 #if !defined(DBT_DIAG_NO_RED)
-      changed += lower_chunk(const_cast<uint16_t*>(rp[r]) + 8 * j, w[r][j], __ldg(drow + j));
+      changed += lower_chunk(a.dist + rb[r] + 8 * (cb[r] + j), w[r][j], __ldg(drow + j));
 #endif
     }
   }
@@ -1076,58 +1076,48 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_cu
   asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw);  // kCullWarps * K * K
-  // two barriers per batch: the queue counter is double-buffered by batch
-  // parity and the next batch index is fetched during phase B
-  __shared__ int q_n[2];
-  __shared__ long long batch_next;
+  __shared__ int q_n;
+  __shared__ long long batch0, batch_next;
   // the d-table (17 KB for K = 21) is read through L1 (__ldg), not staged
-  if (threadIdx.x == 0) {
-    batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
-    q_n[0] = q_n[1] = 0;
-  }
-  __syncthreads();
+  if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n_items = (int64_t)a.lc->n_unique;
-  unsigned changed = 0, rows_done = 0;
-  for (int par = 0;; par ^= 1) {
-    const int64_t batch0 = batch_next;  // written before the last barrier
-    if (batch0 >= n_items) break;
-    const int64_t item = batch0 + warp;
-    if (item < n_items) {
-      cull_centre(a, a.uniq[item], lane, &q_n[par], Put64{queue}, NoInfo{});
-    }
-    __syncthreads();  // the queue is complete; every thread has read batch_next
-    // next batch index: its atomic overlaps phase B
+  unsigned long long changed = 0, rows_done = 0;
+  while (true) {
     if (threadIdx.x == 0) {
-      batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
-      q_n[par ^ 1] = 0;
+      batch0 = batch_next;
+      q_n = 0;
     }
+    __syncthreads();
+    const int64_t item = batch0 + warp;
+    if (batch0 >= n_items) break;
+    if (item < n_items) {
+      cull_centre(a, a.uniq[item], lane, &q_n, Put64{queue}, NoInfo{});
+    }
+    __syncthreads();
+    // next batch index: its atomic overlaps phase B
+    if (threadIdx.x == 0) batch_next = (long long)atomicAdd(&a.lc->work, (unsigned long long)kCullWarps);
     // ===== phase B: the block sweeps the queued rows, one thread per row,
-    // two rows' chunk loads in flight per thread; a last pass of at most one
-    // row per thread runs the one-row code =====
-    const int nq = q_n[par];
-    int base = 0;
-    for (; nq - base > (int)blockDim.x; base += 2 * blockDim.x) {
-      const int i = base + threadIdx.x;
+    // two rows' chunk loads in flight per thread =====
+    const int nq = q_n;
+    for (int i = threadIdx.x; i < nq; i += 2 * blockDim.x) {
       const RowTask rows[2] = {decode_task64(i < nq ? queue[i] : kEmptyKey),
                                decode_task64(i + (int)blockDim.x < nq ? queue[i + blockDim.x] : kEmptyKey)};
-      sweep_rows<2>(a, rows, changed, rows_done);
+      sweep_rows2(a, rows, changed, rows_done);
     }
-    if (base + (int)threadIdx.x < nq) {
-      const RowTask rows[1] = {decode_task64(queue[base + threadIdx.x])};
-      sweep_rows<1>(a, rows, changed, rows_done);
-    }
-    __syncthreads();  // the queue is rewritten by the next batch; batch_next is visible
+    __syncthreads();  // queue and batch0 are rewritten by the next batch
   }
   // one atomic per block and counter (same-address atomics serialise at L2)
   __shared__ unsigned long long blk_changed, blk_rows;
   if (threadIdx.x == 0) blk_changed = blk_rows = 0;
-  changed = __reduce_add_sync(0xffffffffu, changed);
-  rows_done = __reduce_add_sync(0xffffffffu, rows_done);
+  for (int o = 16; o; o >>= 1) {
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    rows_done += __shfl_xor_sync(0xffffffffu, rows_done, o);
+  }
   __syncthreads();
-  if (lane == 0 && changed) atomicAdd(&blk_changed, (unsigned long long)changed);
-  if (lane == 0 && rows_done) atomicAdd(&blk_rows, (unsigned long long)rows_done);
+  if (lane == 0 && changed) atomicAdd(&blk_changed, changed);
+  if (lane == 0 && rows_done) atomicAdd(&blk_rows, rows_done);
   __syncthreads();
   if (threadIdx.x == 0 && blk_changed) atomicAdd(&a.lc->changed, blk_changed);
   if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
@@ -1144,7 +1134,7 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_wa
   uint64_t* queue = reinterpret_cast<uint64_t*>(smem_raw) + warp * a.K * a.K;
   __shared__ int q_n[kCullWarps];
   const int64_t n_items = (int64_t)a.lc->n_unique;
-  unsigned changed = 0, rows_done = 0;
+  unsigned long long changed = 0, rows_done = 0;
   constexpr int G = 4;  // centres per work fetch
   long long next = 0;
   if (lane == 0) next = (long long)atomicAdd(&a.lc->work, (unsigned long long)G);
@@ -1160,7 +1150,7 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_wa
       const int nq = q_n[warp];
       for (int i = lane; i < nq; i += 64) {
         const RowTask rows[2] = {decode_task64(queue[i]), decode_task64(i + 32 < nq ? queue[i + 32] : kEmptyKey)};
-        sweep_rows<2>(a, rows, changed, rows_done);
+        sweep_rows2(a, rows, changed, rows_done);
       }
       __syncwarp();
     }
@@ -1168,11 +1158,13 @@ __global__ void __launch_bounds__(kCullWarps * 32, DBT_CULL_MIN_BLOCKS) sweep_wa
   }
   __shared__ unsigned long long blk_changed, blk_rows;
   if (threadIdx.x == 0) blk_changed = blk_rows = 0;
-  changed = __reduce_add_sync(0xffffffffu, changed);
-  rows_done = __reduce_add_sync(0xffffffffu, rows_done);
+  for (int o = 16; o; o >>= 1) {
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    rows_done += __shfl_xor_sync(0xffffffffu, rows_done, o);
+  }
   __syncthreads();
-  if (lane == 0 && changed) atomicAdd(&blk_changed, (unsigned long long)changed);
-  if (lane == 0 && rows_done) atomicAdd(&blk_rows, (unsigned long long)rows_done);
+  if (lane == 0 && changed) atomicAdd(&blk_changed, changed);
+  if (lane == 0 && rows_done) atomicAdd(&blk_rows, rows_done);
   __syncthreads();
   if (threadIdx.x == 0 && blk_changed) atomicAdd(&a.lc->changed, blk_changed);
   if (threadIdx.x == 0 && blk_rows) atomicAdd(&a.lc->rows, blk_rows);
@@ -2222,7 +2214,34 @@ int dbt_integrate_frame_async(dbt_grid* g, const dbt_bank* b, const void* points
     *ticket = tk;
     return DBT_OK;
   }
-  DBT_CUDA(cudaMemcpyAsync(sl.d_buf, points, n * esz, cudaMemcpyHostToDevice, g->cstream));
+  // a pageable scan (plain numpy) goes through the slot's pinned staging with
+  // the host copy pool: cudaMemcpyAsync from pageable memory would block this
+  // thread on the driver's single-threaded bounce buffer (hostcopy.cu)
+  const void* h_src = points;
+  if ((int64_t)(n * esz) >= (64 << 10) && !getenv("DBT_NO_HOST_STAGE")) {
+    cudaPointerAttributes at;
+    const bool registered = cudaPointerGetAttributes(&at, points) == cudaSuccess &&
+                            (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged);
+    if (!registered) {
+      cudaGetLastError();  // pageable pointers report an error on some drivers
+      if ((int64_t)(n * esz) > sl.cap_hstage) {
+        if (sl.h_stage) cudaFreeHost(sl.h_stage);
+        sl.h_stage = nullptr;
+        sl.cap_hstage = 0;
+        const int64_t cap = (int64_t)(n * esz) * 5 / 4;
+        if (cudaHostAlloc(&sl.h_stage, (size_t)cap, cudaHostAllocDefault) == cudaSuccess)
+          sl.cap_hstage = cap;
+        else
+          cudaGetLastError();
+      }
+      if (sl.h_stage) {
+        // the slot's previous copy has completed (its `done` event was waited on above)
+        pooled_host_copy(sl.h_stage, points, n * esz);
+        h_src = sl.h_stage;
+      }
+    }
+  }
+  DBT_CUDA(cudaMemcpyAsync(sl.d_buf, h_src, n * esz, cudaMemcpyHostToDevice, g->cstream));
   DBT_CUDA(cudaEventRecord(sl.copied, g->cstream));
   DBT_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
   // the default path replays the slot's own executable graph; other launch
