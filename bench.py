@@ -195,6 +195,12 @@ def diag_reorder(pts, pose, w, how):
     on the order; the sweep's memory locality does."""
     if how == "random":
         return pts[np.random.default_rng(0).permutation(len(pts))]
+    if how.startswith("az"):
+        # sensor-frame azimuth sectors, scan order kept inside a sector: the
+        # beams that stamp overlapping cubes come close together in the list
+        n = int(how[2:])
+        sec = np.floor((np.arctan2(pts[:, 1].astype(np.float64), pts[:, 0]) / (2 * np.pi) + 0.5) * n).astype(np.int64) % n
+        return np.ascontiguousarray(pts[np.argsort(sec, kind="stable")])
     m = pts.astype(np.float64) @ pose[:3, :3].T + pose[:3, 3]
     v = np.clip(np.floor((m - np.asarray(w.origin)) / w.voxel_size), 0, (1 << 20) - 1).astype(np.uint64)
     if how == "xyz":
@@ -374,7 +380,7 @@ def main():
     ap.add_argument("--flush", default="clean", choices=["clean", "write"],
                     help="L2 flush before a step: write a 256 MB buffer, then (clean) read another 256 MB buffer so "
                          "the flush's dirty lines are written back before the step instead of inside it")
-    ap.add_argument("--diag-order", default=None, choices=["morton", "xyz", "random"],
+    ap.add_argument("--diag-order", default=None, choices=["morton", "xyz", "random", "az8", "az16", "az32", "az64", "az128", "az256"],
                     help="diagnostics only: reorder each scan's points (spatial locality of the sweep work list)")
     ap.add_argument("--interleave", type=int, default=None,
                     help="slab mode: x-block width of interleaved sharding (default 64, at most nx / 2N)")

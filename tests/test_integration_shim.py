@@ -17,6 +17,7 @@ meshes.
 import ctypes
 import importlib
 import json
+import os
 import shutil
 import subprocess
 import sys
