@@ -873,6 +873,87 @@ __device__ __forceinline__ void gather_certs(const CullArgs& a, int64_t cx, int6
   }
 }
 
+// The same gather with one instruction stream for all lanes (kernels with
+// R >= 5, grids whose y-z plane offsets fit 32 bits): every neighbour read is
+// "nbits certificate bits starting at voxel c + (ox, oy, oz)", so each lane
+// derives its offset and width from its index and all lanes run the index
+// arithmetic, the one or two loads and the extraction together, instead of
+// the 3 + 2 divergent lane groups of gather_certs (15 % of the sweep's
+// instructions at 12-15 active lanes). R >= 5 puts every neighbour read inside
+// the grid (boundary discard: c +- R is in the grid), so no bounds checks.
+// Returns the same nb / axm / plm.
+__device__ __forceinline__ void gather_certs_uniform(const CullArgs& a, int64_t cx, int64_t cy, int64_t cz, int lane,
+                                                     uint32_t& nb, uint32_t& axm, uint32_t& plm) {
+  const int ny = (int)a.ny, nzp = (int)a.nzp;
+  const int64_t base = (cx * a.ny + cy) * a.nzp + cz;
+  // round 1: lanes 0-8 the 3x3 columns (3 bits from cz-1), lanes 9-24 the
+  // x / y axis neighbours at k = 2..5 (1 bit), lane 25 the centre column
+  // (11 bits from cz-5)
+  int ox = 0, oy = 0, oz = 0, nbits = 1;
+  if (lane < 9) {
+    ox = lane / 3 - 1;
+    oy = lane % 3 - 1;
+    oz = -1;
+    nbits = 3;
+  } else if (lane < 25) {
+    const int j = (lane - 9) & 7, k = 2 + (j & 3), sk = j < 4 ? k : -k;
+    ox = lane < 17 ? sk : 0;
+    oy = lane < 17 ? 0 : sk;
+  } else {
+    oz = -5;
+    nbits = 11;
+  }
+  uint32_t bits = 0;
+  if (lane < 26) {
+    const int64_t idx = base + ((ox * ny + oy) * nzp + oz);
+    const int sft = (int)(idx & 31);
+    const uint32_t* wp = a.stamped + (idx >> 5);
+    const uint32_t w0 = ld_cert(wp);
+    const uint32_t w1 = sft + nbits > 32 ? ld_cert(wp + 1) : 0u;
+    bits = __funnelshift_r(w0, w1, sft) & ((1u << nbits) - 1u);
+  }
+  const uint32_t nbc = lane < 9 ? bits << (3 * lane) : 0u;
+  uint32_t axc = (lane >= 9 && lane < 25) ? bits << (lane - 9) : 0u;
+  if (lane == 25) axc = (((bits >> 7) & 0xFu) << 16) | ((__brev(bits & 0xFu) >> 28) << 20);
+  nb = __reduce_or_sync(0xffffffffu, nbc) & ~(1u << 13);  // not c itself
+  axm = __reduce_or_sync(0xffffffffu, axc);
+  plm = 0;
+  if (__popc(nb) < kPlaneGatherBelow) {
+    // round 2: lanes 0-11 the (a, b, 0) plane neighbours (1 bit at cz),
+    // lanes 12-15 the columns cx+1, cx-1, cx+2, cx-2 (5 bits from cz-2)
+    uint32_t plb = 0;
+    if (lane < 16) {
+      int px, py = 0, pz = 0, pbits = 1;
+      if (lane < 12) {
+        const int g = lane >> 2, sa = (lane & 2) ? -1 : 1, sb = (lane & 1) ? -1 : 1;
+        px = sa * (g == 1 ? 1 : 2);
+        py = sb * (g == 0 ? 1 : 2);
+      } else {
+        px = lane == 12 ? 1 : lane == 13 ? -1 : lane == 14 ? 2 : -2;
+        pz = -2;
+        pbits = 5;
+      }
+      const int64_t idx = base + ((px * ny + py) * nzp + pz);
+      const int sft = (int)(idx & 31);
+      const uint32_t* wp = a.stamped + (idx >> 5);
+      const uint32_t w0 = ld_cert(wp);
+      const uint32_t w1 = sft + pbits > 32 ? ld_cert(wp + 1) : 0u;
+      const uint32_t b = __funnelshift_r(w0, w1, sft) & ((1u << pbits) - 1u);
+      if (lane < 12) {
+        plb = b << lane;
+      } else {  // bit i of b: cz - 2 + i
+        const uint32_t cp1 = (b >> 3) & 1u, cm1 = (b >> 1) & 1u, cp2 = (b >> 4) & 1u, cm2 = b & 1u;
+        const uint32_t xz = lane == 12   ? (cp2 << 4) | (cm2 << 5)
+                            : lane == 13 ? (cp2 << 6) | (cm2 << 7)
+                            : lane == 14 ? cp1 | (cm1 << 1) | (cp2 << 8) | (cm2 << 9)
+                                         : (cp1 << 2) | (cm1 << 3) | (cp2 << 10) | (cm2 << 11);
+        plb = xz << 12;
+      }
+    }
+    plm = __reduce_or_sync(0xffffffffu, plb);
+  }
+}
+
 template <typename Put, typename Info>
 __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, int lane, int* q_n, Put put, Info info) {
   const int R = a.R, K = a.K;
@@ -881,7 +962,20 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
   int64_t cx, cy, cz;
   unpack_center(centre, cx, cy, cz);
   uint32_t nb, axm, plm;
+#if defined(DBT_GATHER_DIVERGENT)
   gather_certs(a, cx, cy, cz, lane, nb, axm, plm);
+#else
+  if (a.R >= 5 && a.ny * a.nzp < (int64_t(1) << 28)) {
+    gather_certs_uniform(a, cx, cy, cz, lane, nb, axm, plm);
+#if defined(DBT_GATHER_CHECK)
+    uint32_t nb2, axm2, plm2;
+    gather_certs(a, cx, cy, cz, lane, nb2, axm2, plm2);
+    if (nb != nb2 || axm != axm2 || plm != plm2) __trap();
+#endif
+  } else {
+    gather_certs(a, cx, cy, cz, lane, nb, axm, plm);
+  }
+#endif
 #define NB(A, B, C) ((nb >> (((A) + 1) * 9 + ((B) + 1) * 3 + ((C) + 1))) & 1u)
   // per lane: kernel x-offset dx, its dy interval and z-cut terms
   const int dx = lane - R;
