@@ -1018,6 +1018,7 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
   if (thr[5]) mm[1] = max(mm[1], -thr[5]);  // dz <= -thr culled
   // plane neighbours: (a, b, 0) cut b dy >= T - a dx, (a, 0, c) cut
   // c dz >= T - a dx, T = |delta|^2 / 2 + 1, each inside its window
+#if defined(DBT_PLM_UNROLLED)
   if (plm) {
 #pragma unroll
     for (int i = 0; i < 12; ++i) {
@@ -1036,6 +1037,29 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
       }
     }
   }
+#else
+  // one pass per certified plane neighbour (plm is the same in every lane, so
+  // the loop and the decode of its bit are warp-uniform; the unrolled,
+  // predicated form ran all 24 cuts for every sparse centre)
+  for (uint32_t m = plm; m; m &= m - 1) {
+    const int bit = __ffs(m) - 1;
+    const bool zcut = bit >= 12;  // (pa, 0, q): dz cut; else (pa, q, 0): dy cut
+    const int i = zcut ? bit - 12 : bit;
+    const int g = i >> 2, s1 = (i & 2) ? -1 : 1, s2 = (i & 1) ? -1 : 1;
+    const int pa = s1 * (g == 1 ? 1 : 2), q = s2 * (g == 0 ? 1 : 2);
+    const bool xw = dx - pa <= R && pa - dx <= R;  // v inside e's x-window
+    const int num = (g == 2 ? 5 : 3) - pa * dx;
+    const int cdiv = g == 0 ? num : (num + 1) >> 1;  // ceil(num / |q|)
+    if (!xw) continue;
+    if (!zcut) {
+      if (q > 0) yhi = min(yhi, max(cdiv, q - R) - 1);
+      else ylo = max(ylo, min(-cdiv, R + q) + 1);
+    } else {
+      if (q > 0) mp[1] = min(mp[1], max(cdiv, q - R));
+      else mm[1] = max(mm[1], min(-cdiv, R + q));
+    }
+  }
+#endif
   const int cnt = dead ? 0 : max(0, yhi - ylo + 1);
   int pre = cnt;  // inclusive scan
 #pragma unroll
