@@ -752,11 +752,15 @@ constexpr int kFar = 1 << 20;
 #define DBT_ROWS_BAL_DEN 3
 #endif
 constexpr int kPlaneGatherBelow = 8;  // certified adjacent centres below which plane neighbours are read
-// centres per block batch (one warp each). Same-box A/B at 64 registers
-// (4 resident blocks of 8 warps): 8 vs 4 config 2 +8.5 %, config 3 +11 %,
-// config 1 +2 %, config 4 +1.6 %, config 5 +1 %; 2, 12 and 16 are slower
+// centres per block batch (one warp each), 32 resident warps per SM at 64
+// registers. With the divergent certificate gather 8 (4 blocks per SM) beat 4
+// (config 2 +8.5 %, config 3 +11 %); since the gather became one instruction
+// stream, 4 centres per batch (8 blocks of 128 threads per SM: shorter
+// barriers, finer work fetch) win: same-box A/B 4 vs 8: config 4 +3.2 %,
+// config 5 (32 scans) +3.5 %, config 3 +0.7 %, configs 1-2 within 1 %; 2, 3,
+// 5, 6 and 16 are slower (profiles/README.md, s5_ab4 / s5_ab5)
 #ifndef DBT_CULL_WARPS
-#define DBT_CULL_WARPS 8
+#define DBT_CULL_WARPS 4
 #endif
 constexpr int kCullWarps = DBT_CULL_WARPS;
 
