@@ -1006,6 +1006,33 @@ class TestAsyncFrames:
             mb, sb, hb = b.download_range(x0, x1)
             assert np.array_equal(ma, mb) and np.array_equal(sa, sb) and np.array_equal(ha, hb)
 
+    def test_pageable_staging_equals_direct_copy(self, monkeypatch):
+        """Plain numpy scans of >= 64 KB go through the slot's pinned staging
+        (host copy pool); $DBT_NO_HOST_STAGE=1 hands the pageable pointer to
+        cudaMemcpyAsync instead. Same grids, same counts."""
+        import workloads
+        from paper_2509_20081_b200 import integrate_frame_async
+
+        w = workloads.get(2)
+        bank = build_kernel_bank(shadow_radius=w.shadow_radius)
+        scans = [w.scan(k) for k in range(6)]
+        assert min(s.nbytes for s in scans) >= (64 << 10)
+        grids, stats = [], []
+        for direct in (False, True):
+            if direct:
+                monkeypatch.setenv("DBT_NO_HOST_STAGE", "1")
+            g = new_grid(w.dims, w.voxel_size, w.origin)
+            futs = [integrate_frame_async(g, bank, ScanFrame(points=s, pose=w.poses[k]), IntegrationParams())
+                    for k, s in enumerate(scans[:3])]  # at most 4 calls outstanding
+            futs.append(integrate_frame_async(g, bank, ScanFrame(points=scans[3], pose=w.poses[3]), IntegrationParams()))
+            stats.append([(f.result().points_in, f.result().points_discarded) for f in futs])
+            grids.append(g)
+        assert stats[0] == stats[1]
+        for x0, x1 in ((0, 211), (211, w.dims[0])):
+            a = grids[0].download_range(x0, x1)
+            b = grids[1].download_range(x0, x1)
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
     def test_async_exact_voxels_written(self, golden):
         from paper_2509_20081_b200 import integrate_frame_async
 
