@@ -775,9 +775,12 @@ __device__ __forceinline__ uint64_t pack_task(int64_t rbase, int c0, int c1, int
 // dz interval is empty.
 struct Put64 {
   uint64_t* queue;
-  __device__ __forceinline__ void operator()(int i, bool valid, int, int c0, int c1, int64_t rbase,
+  // ch = row start / 8 (the low word of the task: a grid has < 2^35 cells,
+  // checked at launch), built with 32-bit arithmetic per row
+  __device__ __forceinline__ void operator()(int i, bool valid, int, int c0, int c1, uint32_t ch,
                                              const uint16_t* rowd, int drow0) const {
-    queue[i] = valid ? pack_task(rbase, c0, c1, drow0 + __ldg(rowd)) : kEmptyKey;
+    const uint32_t hi = ((uint32_t)c0 << 5) | ((uint32_t)c1 << 7) | ((uint32_t)(drow0 + __ldg(rowd)) << 9);
+    reinterpret_cast<uint2*>(queue)[i] = valid ? make_uint2(ch, hi) : make_uint2(~0u, ~0u);
   }
 };
 struct NoInfo {
@@ -1090,8 +1093,11 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
   // delta_z = +1 neighbours cut dz >= max(mp - b dy, -R+1), delta_z = -1
   // ones cut dz <= min(mm + b dy, R-1) (b = delta_y, only when v is in
   // their y-window) — and its task
+  const int nzp8 = (int)(a.nzp >> 3);
+  // chunk index of this lane's column at dy = 0 (xbase and cbase are multiples of 8)
+  const uint32_t colch = (uint32_t)((xbase + cbase) >> 3);
   auto emit = [&](int slot, int col, int rdy, int z_hi0, int z_lo0, int mp0, int mm0, int mp2, int mm2,
-                  int64_t xb) {
+                  uint32_t cch) {
     int zhi = z_hi0, zlo = z_lo0;
     if (rdy <= R - 1) {  // b = -1
       zhi = min(zhi, max(mp0 + rdy, -R + 1) - 1);
@@ -1103,7 +1109,7 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
     }
     const bool valid = zlo <= zhi;
     const int c0 = (int)(((cz + zlo) >> 3) - zb), c1 = (int)(((cz + zhi) >> 3) - zb);
-    put(qb + slot, valid, rdy, c0, c1, xb + cbase + rdy * a.nzp, rowd + col * K + R + rdy, drow0);
+    put(qb + slot, valid, rdy, c0, c1, cch + (uint32_t)(rdy * nzp8), rowd + col * K + R + rdy, drow0);
   };
   const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
   if (((total + 31) >> 5) * DBT_ROWS_BAL_NUM < cmax * DBT_ROWS_BAL_DEN) {
@@ -1126,12 +1132,12 @@ __device__ __forceinline__ void cull_centre(const CullArgs& a, uint64_t centre, 
       const int o_zhi0 = __shfl_sync(0xffffffffu, zhi0, col), o_zlo0 = __shfl_sync(0xffffffffu, zlo0, col);
       const int o_mp0 = __shfl_sync(0xffffffffu, mp[0], col), o_mm0 = __shfl_sync(0xffffffffu, mm[0], col);
       const int o_mp2 = __shfl_sync(0xffffffffu, mp[2], col), o_mm2 = __shfl_sync(0xffffffffu, mm[2], col);
-      const int64_t o_xb = __shfl_sync(0xffffffffu, xbase, col);
-      if (j < total) emit(j, col, o_ylo + (j - o_pre), o_zhi0, o_zlo0, o_mp0, o_mm0, o_mp2, o_mm2, o_xb);
+      const uint32_t o_ch = __shfl_sync(0xffffffffu, colch, col);
+      if (j < total) emit(j, col, o_ylo + (j - o_pre), o_zhi0, o_zlo0, o_mp0, o_mm0, o_mp2, o_mm2, o_ch);
     }
   } else {
     // each lane writes its own column's rows at its prefix offset
-    for (int k = 0; k < cnt; ++k) emit(pre + k, lane, ylo + k, zhi0, zlo0, mp[0], mm[0], mp[2], mm[2], xbase);
+    for (int k = 0; k < cnt; ++k) emit(pre + k, lane, ylo + k, zhi0, zlo0, mp[0], mm[0], mp[2], mm[2], colch);
   }
 }
 
@@ -1812,6 +1818,8 @@ int launch_integrate(dbt_grid* g, const dbt_bank* b, const void* d_pts, int dtyp
   }
 
   if (b->iso && !(p->flags & DBT_FLAG_GENERIC_SWEEP)) {
+    // row tasks carry the row start / 8 in 32 bits (Put64)
+    if (g->n_cells >> 35) return set_error(DBT_ERR_CONFIG, "grid part above 2^35 cells: unsupported by the culling sweep");
     const size_t smem = (size_t)kCullWarps * b->K * b->K * sizeof(uint64_t);
     if (g->sweep_ch != -b->K) {
       DBT_CUDA(cudaFuncSetAttribute(DBT_ISO_SWEEP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
