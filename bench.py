@@ -31,7 +31,8 @@ are written back before the step events rather than by the step's kernels
           FrameStats collected inside the timed region; `e2e_sync` is one
           synchronous integrate_frame per step (L2 flushed before each).
           Batches / N > 1: the synchronous calls. `e2e_pageable` repeats the
-          synchronous pass with the plain numpy scans a stock caller passes.
+          synchronous pass with the plain numpy scans a stock caller passes,
+          `e2e_pageable_async` the pipelined pass with them.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                 [--config 4] [--batch 1] [--multi slab|replica]
