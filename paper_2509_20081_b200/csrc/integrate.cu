@@ -751,7 +751,10 @@ constexpr int kFar = 1 << 20;
 #ifndef DBT_ROWS_BAL_DEN
 #define DBT_ROWS_BAL_DEN 3
 #endif
-constexpr int kPlaneGatherBelow = 8;  // certified adjacent centres below which plane neighbours are read
+#ifndef DBT_PLANE_GATHER_BELOW
+#define DBT_PLANE_GATHER_BELOW 8
+#endif
+constexpr int kPlaneGatherBelow = DBT_PLANE_GATHER_BELOW;  // certified adjacent centres below which plane neighbours are read
 // centres per block batch (one warp each), 32 resident warps per SM at 64
 // registers. With the divergent certificate gather 8 (4 blocks per SM) beat 4
 // (config 2 +8.5 %, config 3 +11 %); since the gather became one instruction
